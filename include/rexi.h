@@ -1,0 +1,187 @@
+/*
+ * rexi.h — C ABI of librexi.so: one REXII step e^{tau A} f0 of the linearised
+ * rotating shallow-water equations (LRSW) on a B200 (sm_100a).
+ *
+ * Method: Caliari, Einkemmer, Moriggl, Ostermann, "An accurate and time-parallel
+ * rational exponential integrator for hyperbolic and oscillatory PDEs",
+ * arXiv:2008.11607. Citations "PAPER.md:<line>" refer to the LaTeX source
+ * plus the equation label.
+ *
+ * Problem: d/dt f = A f, f = (eta, u, v), on the bi-periodic
+ * unit square with a D x D grid, x_j = j/D,
+ *     A = [[0, -d/dx, -d/dy], [-d/dx, 0, 1], [-d/dy, -1, 0]].
+ * One step of size tau is approximated by the REXII half-sum
+ * (eq:modifiedRexiMatrixReducedSum; procedure PAPER.md:427-435):
+ *     e^{tau A} f0 ~ Re sum_{n=0}^{N} Gamma_n [ C2_n g1_n + (C1_n - C2_n alpha_{-n}) g2_n ],
+ *     (alpha_n I + tau A) g1_n = f0,   (alpha_{-n} I - tau A) g2_n = g1_n,
+ * with alpha_n = h(mu + i n), N = M + 24 and the Appendix A coefficients
+ * (PAPER.md:815-851). All solves run per Fourier mode ("all computations ...
+ * in Fourier space"): tau A is block-diagonal per wavenumber.
+ *
+ * Conventions shared by every entry point
+ *  - Precision: IEEE fp64 throughout (complex fp64 in Fourier space).
+ *  - Physical fields: caller-owned DEVICE pointers (unless the name says _host) to
+ *    D*D contiguous doubles, row-major [y][x], x fastest (torch.float64 CUDA tensors).
+ *  - Spectral arrays ("fhat", "acc"): caller-owned device pointers to 3*D*D complex
+ *    values stored as interleaved (re, im) doubles, field-major (eta, u, v), then
+ *    row l (y-wavenumber index), then column k (x-wavenumber index); index j maps
+ *    to wavenumber j (j < D/2) or j - D. Forward transform:
+ *        fhat(k,l) = D^-2 sum_{y,x} X[y][x] exp(-2 pi i (k x + l y)/D).
+ *  - Readings of the paper: the operator is tau-scaled
+ *    (G3: symbols 2 pi k tau, Coriolis tau); the Nyquist index's first-derivative
+ *    symbol is zero (G2); the Appendix A sign column is the sign of the real part
+ *    (G1); the g3 combination is division-free (G4).
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream). Calls are stream-ordered and asynchronous unless stated. A plan is
+ *    not re-entrant: do not use one plan from two streams concurrently.
+ *  - Pole ranges [pole_begin, pole_end) index the half-sum n = 0..N
+ *    (0 <= pole_begin <= pole_end <= n_poles); otherwise REXI_ERANGE.
+ *  - Errors: every call returns a rexi_status_t; no C++ exception crosses the ABI.
+ *    rexi_last_error() gives a thread-local text for the last failure. On error no
+ *    output is guaranteed; inputs are never modified.
+ *  - In-place: outputs may alias inputs for rexi_apply / rexi_apply_partial (the
+ *    inputs are consumed into plan workspace first).
+ */
+#ifndef REXI_H
+#define REXI_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REXI_ABI_VERSION 1
+
+typedef struct rexi_plan_s *rexi_plan_t; /* opaque; owns device workspace + pole table */
+
+typedef enum {
+    REXI_OK = 0,
+    REXI_EINVAL = 1, /* bad argument (D, tau, tol, h, M, pointer, variant) */
+    REXI_ENOMEM = 2, /* host or device allocation failed                   */
+    REXI_ECUDA = 3,  /* a CUDA runtime call or kernel launch failed         */
+    REXI_ERANGE = 4  /* bad pole range                                     */
+} rexi_status_t;
+
+/* Per-pole solve formulation of the fused pole kernel.
+ * Both solve the same two shifted systems per mode and pole, Helmholtz-reduced
+ * (eq:lswEta), and accumulate in registers.
+ *  REXI_VARIANT_DZ: back-substitution in divergence/vorticity variables
+ *                   (delta, zeta of PAPER.md:493-496); velocities recovered once
+ *                   per mode from the accumulated sums (default; fewer fp64 ops).
+ *  REXI_VARIANT_UV: paper-literal back-substitution of (u, v) per pole with
+ *                   eq:lswVelocities. */
+typedef enum { REXI_VARIANT_DZ = 0, REXI_VARIANT_UV = 1 } rexi_variant_t;
+
+typedef struct {
+    int D;                  /* grid size (power of two, 4..8192)                     */
+    int variant;            /* rexi_variant_t                                         */
+    double tau;             /* step size                                              */
+    double tol;             /* requested tolerance (0 if M was given explicitly)      */
+    double h;               /* Gaussian spacing h (eq:bm)                             */
+    double mu;              /* Appendix A mu                                          */
+    long M;                 /* Gaussian-sum half width (eq:eixsumM)                   */
+    long L;                 /* 24                                      */
+    long N;                 /* M + L                                                  */
+    long n_poles;           /* N + 1 (half-sum, Remark 3)                             */
+    long m0;                /* the rule's offset: M = ceil(|tau| rho / h) + m0        */
+    double rho;             /* sqrt(2) pi D (eq:lswRoh, Sec. 4.2 form, reading G5)    */
+    double predicted_floor; /* predicted scalar error floor (readings G8, G9)         */
+    double flops_per_pole_mode; /* algorithmic fp64 flops per pole x Fourier mode     */
+    double fp64_ops_per_pole_mode; /* fp64-pipe instructions (FMA = 1) per pole x mode */
+} rexi_plan_info_t;
+
+/* Create a plan for one step of size tau on a D x D grid.
+ *  D:      power of two, 4 <= D <= 8192.
+ *  tau:    finite; tau < 0 allowed (REXII is valid for x of both signs, eq:modifiedRexi).
+ *  tol:    in (0, 1): sets m0 = ceil(2 sqrt(h^2 - ln(sqrt(4 pi) tol)) - 1) (reading G9,
+ *          from Appendix B). tol <= 0 means the paper's m0 = 11
+ *          (eq:Mformula).
+ *  h:      in (0, pi); h <= 0 selects 0.5.
+ *  M:      > 0: use this M (must be >= 12); <= 0: M from the rule
+ *          tau rho(A) <= (M - m0) h (eq:matrixAccuracyBound).
+ *  device: CUDA device ordinal.
+ * Allocates the pole table and all workspace on `device`; synchronous.
+ * Errors: EINVAL (arguments), ENOMEM, ECUDA. *out is NULL on error. */
+rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, double h,
+                               long M, int device);
+rexi_status_t rexi_plan_destroy(rexi_plan_t plan);
+rexi_status_t rexi_plan_info(rexi_plan_t plan, rexi_plan_info_t *info);
+
+/* Select the pole-kernel formulation (rexi_variant_t). EINVAL for unknown values. */
+rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
+
+/* Copy the plan's term table to HOST arrays of n_poles entries each (any may be NULL):
+ *   alpha[2n], C1[2n], C2[2n] (interleaved re, im) and gamma[n], for n = 0..N:
+ *   alpha_n = h(mu + i n), C1_n = c1_n h mu + c2_n h n, C2_n = i c2_n
+ *   (PAPER.md:270), Gamma_0 = 1, Gamma_n = 2. Synchronous. */
+rexi_status_t rexi_plan_coeffs(rexi_plan_t plan, double *alpha, double *C1, double *C2,
+                               double *gamma);
+
+/* S1: forward 2-D FFT of the three real fields into fhat (layout above), scaled by D^-2. */
+rexi_status_t rexi_forward(rexi_plan_t plan, const double *eta, const double *u, const double *v,
+                           double *fhat, void *stream);
+
+/* S2+S3: the fused pole kernel. For every Fourier mode and every pole n in
+ * [pole_begin, pole_end) solve both shifted systems and accumulate
+ *   acc = sum_n Gamma_n [ C2_n g1_n + (C1_n - C2_n alpha_{-n}) g2_n ]
+ * (complex, BEFORE the real part). acc is overwritten (an empty
+ * range gives zeros). fhat and acc must not alias. */
+rexi_status_t rexi_poles(rexi_plan_t plan, long pole_begin, long pole_end, const double *fhat,
+                         double *acc, void *stream);
+
+/* S5: eta,u,v = Re(inverse 2-D FFT of acc) (Alg. 1 last line PAPER.md:535). */
+rexi_status_t rexi_inverse(rexi_plan_t plan, const double *acc, double *eta, double *u, double *v,
+                           void *stream);
+
+/* S1..S5 for all poles: (eta_out, u_out, v_out) = REXII(tau A) (eta, u, v). */
+rexi_status_t rexi_apply(rexi_plan_t plan, const double *eta, const double *u, const double *v,
+                         double *eta_out, double *u_out, double *v_out, void *stream);
+
+/* S1..S5 restricted to poles [pole_begin, pole_end): the real, physical-space partial
+ * sum of one rank of a pole-partitioned step (SURVEY.md 8(e) option b). Summing the
+ * outputs over a partition of [0, n_poles) gives rexi_apply's result (S4 is the
+ * caller's allreduce; this library links no NCCL). */
+rexi_status_t rexi_apply_partial(rexi_plan_t plan, long pole_begin, long pole_end,
+                                 const double *eta, const double *u, const double *v,
+                                 double *eta_out, double *u_out, double *v_out, void *stream);
+
+/* rexi_apply with HOST buffers (any host memory; pinned is faster): copies the inputs
+ * host->device, applies, copies the result device->host, and returns when the result
+ * is in the host buffers (synchronous on `stream`). */
+rexi_status_t rexi_apply_host(rexi_plan_t plan, const double *eta, const double *u,
+                              const double *v, double *eta_out, double *u_out, double *v_out,
+                              void *stream);
+
+/* S6: `steps` successive REXII steps in place on device fields (T_final = steps * tau). */
+rexi_status_t rexi_run(rexi_plan_t plan, int steps, double *eta, double *u, double *v,
+                       void *stream);
+
+/* Kernel timing of the pole kernel (the dominant kernel): when enabled, every pole-kernel
+ * launch is bracketed by CUDA events on its stream. rexi_timing_read synchronises on
+ * those events, returns the summed duration (ms) and launch count since the last read,
+ * and resets. Also returns the number of kernels launched by the library (all kinds). */
+rexi_status_t rexi_timing_enable(rexi_plan_t plan, int enable);
+rexi_status_t rexi_timing_read(rexi_plan_t plan, double *pole_kernel_ms, long *pole_launches,
+                               long *total_launches);
+
+/* Host-only (no GPU needed): the Appendix A table compiled into the library
+ * (reading G1): *mu and a[2*(L+1)] = (Re a_l, Im a_l), l = 0..L;
+ * returns L (= 24). a may be NULL to query L. */
+int rexi_appendix_a(double *mu, double *a);
+
+/* Host-only (no GPU needed): the planner's half-sum term table for (h, M) — the same
+ * numbers rexi_plan_coeffs returns for a plan with that h and M. Returns n_poles = M + 25
+ * (or -1 if h is not in (0, pi) or M < 12); arrays of n_poles entries may be NULL. */
+long rexi_terms_host(double h, long M, double *alpha, double *C1, double *C2, double *gamma);
+
+/* Host-only (no GPU needed): the term-count rule used by rexi_plan_create:
+ * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0. */
+long rexi_rule_M(int D, double tau, double tol, double h);
+
+const char *rexi_status_string(rexi_status_t status);
+const char *rexi_last_error(void);
+int rexi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REXI_H */

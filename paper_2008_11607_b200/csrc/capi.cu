@@ -1,0 +1,476 @@
+// capi.cu — the C ABI of librexi.so (include/rexi.h): plan lifetime, the stream-ordered
+// step S1..S5, pole-range partial steps for pole-parallel multi-GPU runs, host-buffer
+// entry, multi-step driver and pole-kernel timing. No exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/rexi.h"
+#include "launch.h"
+#include "planner.h"
+
+using rexi::cd;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+rexi_status_t fail(rexi_status_t s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+
+rexi_status_t cuda_fail(cudaError_t e, const char *where) {
+    return fail(REXI_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                       \
+    do {                                                               \
+        cudaError_t e_ = (call);                                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);            \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(dev) == cudaSuccess) ok = true;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct rexi_plan_s {
+    rexi::Plan host;
+    int device = 0;
+    int variant = REXI_VARIANT_DZ;
+    long n_modes = 0;
+    int num_sms = 0;
+    int occ[2] = {0, 0};
+    int max_chunks = 1;
+    // device buffers
+    rexi::PoleConst *d_poles = nullptr;
+    double *d_ksym = nullptr;
+    cd *d_tw = nullptr;
+    cd *d_fhat = nullptr;   // [3][n_modes]
+    cd *d_acc = nullptr;    // [3][n_modes]
+    cd *d_tmp = nullptr;    // [3][n_modes]
+    cd *d_partial = nullptr;  // [max_chunks][3][n_modes]
+    double *d_stage = nullptr;  // [6][n_modes] (rexi_apply_host)
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+    size_t ev_used = 0;
+    long launches = 0;
+    long pole_launches = 0;
+
+    ~rexi_plan_s() {
+        DeviceGuard g(device);
+        for (void *p : {(void *)d_poles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
+                        (void *)d_tmp, (void *)d_partial, (void *)d_stage})
+            if (p) cudaFree(p);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+rexi_status_t check_plan(rexi_plan_t p) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    return REXI_OK;
+}
+
+// Number of pole chunks (grid.y) for a pole range: minimise the tail of the last wave of
+// blocks (grid sized in multiples of SMs x resident blocks), at most max_chunks, at least
+// 4 poles per chunk.
+int choose_chunks(const rexi_plan_s *p, long n_range) {
+    if (n_range <= 0) return 0;
+    const long mpb = rexi::pole_modes_per_block();
+    const long tiles = (p->n_modes + mpb - 1) / mpb;
+    const long conc = (long)p->num_sms * std::max(1, p->occ[p->variant]);
+    const long max_c = std::max(1L, std::min<long>(p->max_chunks, n_range / 4));
+    int best = 1;
+    double best_eff = 0.0;
+    for (long c = 1; c <= max_c; ++c) {
+        const long blocks = tiles * c;
+        const long waves = (blocks + conc - 1) / conc;
+        const double eff = (double)blocks / (double)(waves * conc);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = (int)c;
+        }
+        if (best_eff > 0.97) break;
+    }
+    return best;
+}
+
+rexi_status_t record(rexi_plan_s *p, cudaStream_t st, bool start) {
+    if (!p->timing) return REXI_OK;
+    if (p->ev_used >= p->ev.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        p->ev.push_back(e);
+    }
+    (void)start;
+    CK(cudaEventRecord(p->ev[p->ev_used++], st));
+    return REXI_OK;
+}
+
+rexi_status_t do_forward(rexi_plan_s *p, const double *eta, const double *u, const double *v,
+                         cd *fhat, cudaStream_t st) {
+    const long n = p->n_modes;
+    const int D = p->host.D;
+    const void *in[3] = {eta, u, v};
+    void *mid[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
+    const void *mid_c[3] = {mid[0], mid[1], mid[2]};
+    void *out[3] = {fhat, fhat + n, fhat + 2 * n};
+    CK(rexi::launch_fft_rows(in, mid, true, false, p->d_tw, D, 0, 1.0, st));
+    CK(rexi::launch_fft_cols(mid_c, out, p->d_tw, D, 0, 1.0 / ((double)D * (double)D), st));
+    p->launches += 2;
+    return REXI_OK;
+}
+
+rexi_status_t do_inverse(rexi_plan_s *p, const cd *acc, double *eta, double *u, double *v,
+                         cudaStream_t st) {
+    const long n = p->n_modes;
+    const int D = p->host.D;
+    const void *in[3] = {acc, acc + n, acc + 2 * n};
+    void *mid[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
+    const void *mid_c[3] = {mid[0], mid[1], mid[2]};
+    void *out[3] = {eta, u, v};
+    CK(rexi::launch_fft_cols(in, mid, p->d_tw, D, 1, 1.0, st));
+    CK(rexi::launch_fft_rows(mid_c, out, false, true, p->d_tw, D, 1, 1.0, st));
+    p->launches += 2;
+    return REXI_OK;
+}
+
+rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, cudaStream_t st) {
+    const long n = p->n_modes;
+    if (e <= b) {
+        CK(cudaMemsetAsync(acc, 0, sizeof(cd) * 3 * (size_t)n, st));
+        return REXI_OK;
+    }
+    const int chunks = choose_chunks(p, e - b);
+    rexi::PoleArgs a;
+    a.fhat = fhat;
+    a.partial = p->d_partial;
+    a.poles = p->d_poles;
+    a.ksym = p->d_ksym;
+    a.pole_begin = b;
+    a.pole_end = e;
+    a.n_modes = n;
+    a.n_chunks = chunks;
+    a.D = p->host.D;
+    a.log2D = 0;
+    while ((1 << a.log2D) < a.D) ++a.log2D;
+    a.tau = p->host.tau;
+    rexi_status_t s;
+    if ((s = record(p, st, true)) != REXI_OK) return s;
+    CK(rexi::launch_poles(a, p->variant, st));
+    if ((s = record(p, st, false)) != REXI_OK) return s;
+    p->pole_launches += 1;
+    rexi::FinishArgs f;
+    f.partial = p->d_partial;
+    f.acc = acc;
+    f.ksym = p->d_ksym;
+    f.n_modes = n;
+    f.n_chunks = chunks;
+    f.D = a.D;
+    f.log2D = a.log2D;
+    f.variant = p->variant;
+    CK(rexi::launch_finish(f, st));
+    p->launches += 2;
+    if (p->variant == REXI_VARIANT_DZ) {
+        rexi::FixupArgs x;
+        x.fhat = fhat;
+        x.acc = acc;
+        x.poles = p->d_poles;
+        x.pole_begin = b;
+        x.pole_end = e;
+        x.n_modes = n;
+        x.D = a.D;
+        CK(rexi::launch_fixup_k0(x, st));
+        p->launches += 1;
+    }
+    return REXI_OK;
+}
+
+rexi_status_t check_range(const rexi_plan_s *p, long b, long e) {
+    if (b < 0 || e < b || e > p->host.n_poles)
+        return fail(REXI_ERANGE, "pole range must satisfy 0 <= begin <= end <= n_poles");
+    return REXI_OK;
+}
+
+template <class F>
+rexi_status_t guarded(rexi_plan_t p, F &&f) {
+    rexi_status_t s = check_plan(p);
+    if (s != REXI_OK) return s;
+    try {
+        DeviceGuard g(p->device);
+        if (!g.ok) return fail(REXI_ECUDA, "cudaSetDevice failed");
+        return f();
+    } catch (const std::bad_alloc &) {
+        return fail(REXI_ENOMEM, "host allocation failed");
+    } catch (...) {
+        return fail(REXI_EINVAL, "unexpected exception");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rexi_abi_version(void) { return REXI_ABI_VERSION; }
+
+const char *rexi_status_string(rexi_status_t s) {
+    switch (s) {
+        case REXI_OK: return "REXI_OK";
+        case REXI_EINVAL: return "REXI_EINVAL: invalid argument";
+        case REXI_ENOMEM: return "REXI_ENOMEM: out of memory";
+        case REXI_ECUDA: return "REXI_ECUDA: CUDA error";
+        case REXI_ERANGE: return "REXI_ERANGE: bad pole range";
+    }
+    return "unknown rexi status";
+}
+
+const char *rexi_last_error(void) { return g_last_error.c_str(); }
+
+rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, double h, long M,
+                               int device) {
+    if (!out) return fail(REXI_EINVAL, "out is NULL");
+    *out = nullptr;
+    rexi_plan_s *p = nullptr;
+    try {
+        p = new rexi_plan_s();
+    } catch (...) {
+        return fail(REXI_ENOMEM, "host allocation failed");
+    }
+    std::vector<char> err;
+    int st;
+    try {
+        st = rexi::make_plan(p->host, D, tau, tol, h, M, err);
+    } catch (...) {
+        delete p;
+        return fail(REXI_ENOMEM, "planner allocation failed");
+    }
+    if (st != REXI_OK) {
+        delete p;
+        return fail((rexi_status_t)st, err.empty() ? "invalid argument" : std::string(err.data()));
+    }
+    p->device = device;
+    p->n_modes = (long)D * D;
+    {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || device < 0 || device >= ndev) {
+            delete p;
+            return e != cudaSuccess ? cuda_fail(e, "cudaGetDeviceCount")
+                                    : fail(REXI_EINVAL, "device ordinal out of range");
+        }
+    }
+    DeviceGuard g(device);
+    if (!g.ok) {
+        delete p;
+        return fail(REXI_ECUDA, "cudaSetDevice failed");
+    }
+    auto cleanup_fail = [&](rexi_status_t s) {
+        delete p;
+        return s;
+    };
+    cudaError_t e;
+    if ((e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device)))
+        return cleanup_fail(cuda_fail(e, "cudaDeviceGetAttribute"));
+    if ((e = rexi::fft_setup_attributes())) return cleanup_fail(cuda_fail(e, "cudaFuncSetAttribute"));
+    if ((e = rexi::pole_occupancy(0, &p->occ[0]))) return cleanup_fail(cuda_fail(e, "occupancy"));
+    if ((e = rexi::pole_occupancy(1, &p->occ[1]))) return cleanup_fail(cuda_fail(e, "occupancy"));
+    const size_t field = sizeof(cd) * 3 * (size_t)p->n_modes;
+    // Partial-sum buffer: at most 64 chunks and at most ~2 GiB.
+    const size_t budget = (size_t)2 << 30;
+    p->max_chunks = (int)std::max<size_t>(1, std::min<size_t>(64, budget / field));
+    auto alloc = [&](void **ptr, size_t bytes) -> cudaError_t { return cudaMalloc(ptr, bytes); };
+    if ((e = alloc((void **)&p->d_poles, sizeof(rexi::PoleConst) * (size_t)p->host.n_poles)) ||
+        (e = alloc((void **)&p->d_ksym, sizeof(double) * (size_t)D)) ||
+        (e = alloc((void **)&p->d_tw, sizeof(double) * (size_t)D)) ||
+        (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
+        (e = alloc((void **)&p->d_tmp, field)) ||
+        (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks))) {
+        cudaGetLastError();
+        return cleanup_fail(e == cudaErrorMemoryAllocation ? fail(REXI_ENOMEM, "cudaMalloc failed")
+                                                           : cuda_fail(e, "cudaMalloc"));
+    }
+    if ((e = cudaMemcpy(p->d_poles, p->host.poles.data(), sizeof(rexi::PoleConst) * (size_t)p->host.n_poles,
+                        cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(p->d_ksym, p->host.ksym.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
+        return cleanup_fail(cuda_fail(e, "cudaMemcpy"));
+    *out = p;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_destroy(rexi_plan_t p) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    delete p;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
+    if (!p || !info) return fail(REXI_EINVAL, "null argument");
+    const rexi::Plan &h = p->host;
+    info->D = h.D;
+    info->variant = p->variant;
+    info->tau = h.tau;
+    info->tol = h.tol;
+    info->h = h.h;
+    info->mu = h.mu;
+    info->M = h.M;
+    info->L = h.L;
+    info->N = h.N;
+    info->n_poles = h.n_poles;
+    info->m0 = h.m0;
+    info->rho = h.rho;
+    info->predicted_floor = h.predicted_floor;
+    info->flops_per_pole_mode = p->variant == REXI_VARIANT_DZ ? rexi::kFlopsDZ : rexi::kFlopsUV;
+    info->fp64_ops_per_pole_mode = p->variant == REXI_VARIANT_DZ ? rexi::kOpsDZ : rexi::kOpsUV;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    if (variant != REXI_VARIANT_DZ && variant != REXI_VARIANT_UV) return fail(REXI_EINVAL, "unknown variant");
+    p->variant = variant;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_coeffs(rexi_plan_t p, double *alpha, double *C1, double *C2, double *gamma) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    const rexi::Plan &h = p->host;
+    const size_t n = (size_t)h.n_poles;
+    if (alpha) std::memcpy(alpha, h.alpha.data(), 2 * n * sizeof(double));
+    if (C1) std::memcpy(C1, h.C1.data(), 2 * n * sizeof(double));
+    if (C2) std::memcpy(C2, h.C2.data(), 2 * n * sizeof(double));
+    if (gamma) std::memcpy(gamma, h.gamma.data(), n * sizeof(double));
+    return REXI_OK;
+}
+
+rexi_status_t rexi_forward(rexi_plan_t p, const double *eta, const double *u, const double *v,
+                           double *fhat, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!eta || !u || !v || !fhat) return fail(REXI_EINVAL, "null pointer");
+        return do_forward(p, eta, u, v, reinterpret_cast<cd *>(fhat), (cudaStream_t)stream);
+    });
+}
+
+rexi_status_t rexi_poles(rexi_plan_t p, long b, long e, const double *fhat, double *acc, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!fhat || !acc) return fail(REXI_EINVAL, "null pointer");
+        if (fhat == acc) return fail(REXI_EINVAL, "fhat and acc must not alias");
+        rexi_status_t s = check_range(p, b, e);
+        if (s != REXI_OK) return s;
+        return do_poles(p, b, e, reinterpret_cast<const cd *>(fhat), reinterpret_cast<cd *>(acc),
+                        (cudaStream_t)stream);
+    });
+}
+
+rexi_status_t rexi_inverse(rexi_plan_t p, const double *acc, double *eta, double *u, double *v,
+                           void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!acc || !eta || !u || !v) return fail(REXI_EINVAL, "null pointer");
+        return do_inverse(p, reinterpret_cast<const cd *>(acc), eta, u, v, (cudaStream_t)stream);
+    });
+}
+
+rexi_status_t rexi_apply_partial(rexi_plan_t p, long b, long e, const double *eta, const double *u,
+                                 const double *v, double *eo, double *uo, double *vo, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!eta || !u || !v || !eo || !uo || !vo) return fail(REXI_EINVAL, "null pointer");
+        rexi_status_t s = check_range(p, b, e);
+        if (s != REXI_OK) return s;
+        cudaStream_t st = (cudaStream_t)stream;
+        if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
+        if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+        return do_inverse(p, p->d_acc, eo, uo, vo, st);
+    });
+}
+
+rexi_status_t rexi_apply(rexi_plan_t p, const double *eta, const double *u, const double *v,
+                         double *eo, double *uo, double *vo, void *stream) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    return rexi_apply_partial(p, 0, p->host.n_poles, eta, u, v, eo, uo, vo, stream);
+}
+
+rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u, const double *v,
+                              double *eo, double *uo, double *vo, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!eta || !u || !v || !eo || !uo || !vo) return fail(REXI_EINVAL, "null pointer");
+        const size_t n = (size_t)p->n_modes;
+        if (!p->d_stage) {
+            cudaError_t e = cudaMalloc((void **)&p->d_stage, 6 * n * sizeof(double));
+            if (e != cudaSuccess) {
+                p->d_stage = nullptr;
+                cudaGetLastError();
+                return fail(REXI_ENOMEM, "cudaMalloc (staging) failed");
+            }
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        double *d[6];
+        for (int i = 0; i < 6; ++i) d[i] = p->d_stage + i * n;
+        const double *hin[3] = {eta, u, v};
+        double *hout[3] = {eo, uo, vo};
+        for (int i = 0; i < 3; ++i)
+            CK(cudaMemcpyAsync(d[i], hin[i], n * sizeof(double), cudaMemcpyHostToDevice, st));
+        rexi_status_t s;
+        if ((s = do_forward(p, d[0], d[1], d[2], p->d_fhat, st)) != REXI_OK) return s;
+        if ((s = do_poles(p, 0, p->host.n_poles, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+        if ((s = do_inverse(p, p->d_acc, d[3], d[4], d[5], st)) != REXI_OK) return s;
+        for (int i = 0; i < 3; ++i)
+            CK(cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return REXI_OK;
+    });
+}
+
+rexi_status_t rexi_run(rexi_plan_t p, int steps, double *eta, double *u, double *v, void *stream) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    if (steps < 0) return fail(REXI_EINVAL, "steps must be >= 0");
+    for (int s = 0; s < steps; ++s) {
+        rexi_status_t r = rexi_apply(p, eta, u, v, eta, u, v, stream);
+        if (r != REXI_OK) return r;
+    }
+    return REXI_OK;
+}
+
+rexi_status_t rexi_timing_enable(rexi_plan_t p, int enable) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    p->timing = enable != 0;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_timing_read(rexi_plan_t p, double *ms, long *pole_launches, long *total_launches) {
+    return guarded(p, [&]() -> rexi_status_t {
+        double sum = 0.0;
+        for (size_t i = 0; i + 1 < p->ev_used; i += 2) {
+            CK(cudaEventSynchronize(p->ev[i + 1]));
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, p->ev[i], p->ev[i + 1]));
+            sum += t;
+        }
+        if (ms) *ms = sum;
+        if (pole_launches) *pole_launches = p->pole_launches;
+        if (total_launches) *total_launches = p->launches;
+        p->ev_used = 0;
+        p->pole_launches = 0;
+        p->launches = 0;
+        return REXI_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// kernels.cuh — device code of librexi (sm_100a): batched fp64 FFT passes, the fused
+// REXII pole kernel, the chunk reduction / velocity recovery and the K = 0 fix-up.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "planner.h"
+
+namespace rexi {
+
+// ----------------------------------------------------------------------------- complex fp64
+struct __align__(16) cd {
+    double x, y;
+};
+
+__device__ __forceinline__ cd mk(double x, double y) { return cd{x, y}; }
+// a*b
+__device__ __forceinline__ cd cmul(cd a, cd b) {
+    return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a*b + c
+__device__ __forceinline__ cd cfma(cd a, cd b, cd c) {
+    return mk(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+// c - a*b
+__device__ __forceinline__ cd cfms(cd a, cd b, cd c) {
+    return mk(fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+// conj(a)*b + c
+__device__ __forceinline__ cd cjfma(cd a, cd b, cd c) {
+    return mk(fma(a.x, b.x, fma(a.y, b.y, c.x)), fma(a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+// c - conj(a)*b
+__device__ __forceinline__ cd cjfms(cd a, cd b, cd c) {
+    return mk(fma(-a.x, b.x, fma(-a.y, b.y, c.x)), fma(-a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+// 1/d for d > 0 (normal range): MUFU.RCP64H seed + one cubic Newton step
+// (relative error ~ e0^3 with e0 ~ 2^-20 seed error). Not correctly rounded; <= 1 ulp.
+__device__ __forceinline__ double rcp_pos(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    e = fma(e, e, e);
+    return fma(e, r, r);
+}
+
+// ----------------------------------------------------------------------------- pole kernel
+struct PoleArgs {
+    const cd *fhat;        // [3][D*D]
+    cd *partial;           // [n_chunks][3][D*D]
+    const PoleConst *poles;
+    const double *ksym;    // [D]
+    long pole_begin, pole_end;
+    long n_modes;          // D*D
+    int n_chunks;
+    int D, log2D;
+    double tau;            // c (tau-scaled Coriolis)
+};
+
+struct FinishArgs {
+    const cd *partial;     // [n_chunks][3][D*D]
+    cd *acc;               // [3][D*D]
+    const double *ksym;
+    long n_modes;
+    int n_chunks;
+    int D, log2D;
+    int variant;
+};
+
+struct FixupArgs {
+    const cd *fhat;
+    cd *acc;
+    const PoleConst *poles;
+    long pole_begin, pole_end;
+    long n_modes;
+    int D;
+};
+
+// ----------------------------------------------------------------------------- FFT passes
+struct FftArgs {
+    const void *in[3];
+    void *out[3];
+    const cd *twiddle;     // D/2 entries e^{-2 pi i j/D}
+    int D, log2D;
+    int per_block;         // rows (row pass) or columns (column pass) per block
+    int inverse;           // 0: e^{-}, 1: e^{+}
+    double scale;
+};
+
+}  // namespace rexi

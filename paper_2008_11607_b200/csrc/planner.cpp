@@ -1,0 +1,216 @@
+// planner.cpp — host planner (S0 of SURVEY.md 8(a)): term count, b_m, c_{1,n}, c_{2,n},
+// C_{1,n}, C_{2,n}, Gamma_n and the per-pole constants of the fused pole kernel.
+// Extended precision (long double) throughout, rounded to fp64 once at the end.
+#include "planner.h"
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/rexi.h"
+
+namespace rexi {
+
+using ld = long double;
+using cld = std::complex<long double>;
+
+// Appendix A, PAPER.md:815-851 (tab:coef_al), L = 24. Reading G1: the printed sign
+// column is the sign of the real part. a_{-l} = conj(a_l).
+static const char *const kMu = "-5.133333333333333";
+static const char *const kA[25][2] = {
+    {"-6.520430828919864e+01", "0"},
+    {"4.261818064131437e+01", "2.761406741120911e+01"},
+    {"-9.801650304425239e+00", "-2.189295463610722e+01"},
+    {"-1.054225194693395e+00", "6.791786454153551e+00"},
+    {"7.950505668209775e-01", "-8.904997258367445e-01"},
+    {"-1.218558380859130e-01", "3.321241563407446e-02"},
+    {"7.365401806949337e-03", "2.212802103193251e-03"},
+    {"-2.801087265991056e-04", "-5.566945197754387e-04"},
+    {"1.254835436432561e-04", "-2.467200513365371e-04"},
+    {"2.295472292491263e-04", "-8.494118951459107e-05"},
+    {"1.858484460459430e-04", "9.242889460185034e-05"},
+    {"4.068056518449676e-05", "1.653479957565515e-04"},
+    {"-8.341508001647741e-05", "1.045331460447588e-04"},
+    {"-9.970528169841103e-05", "-5.856228484297677e-06"},
+    {"-3.499639858693093e-05", "-6.129059473910835e-05"},
+    {"2.295021920298455e-05", "-4.099832469456381e-05"},
+    {"2.931048772724314e-05", "1.708815129697846e-07"},
+    {"7.502088478301169e-06", "1.525082051744077e-05"},
+    {"-5.815291167450100e-06", "6.919604247338349e-06"},
+    {"-4.069948458364005e-06", "-1.440010113050771e-06"},
+    {"7.932524475429588e-08", "-1.794169428574330e-06"},
+    {"6.120984882186265e-07", "-1.131894636585849e-07"},
+    {"5.531365159161319e-08", "1.585749903175946e-07"},
+    {"-2.867805871375946e-08", "1.239499740327838e-08"},
+    {"-1.143081277095316e-09", "-2.763239274253499e-09"},
+};
+static const int kL = 24;
+static const long double kPiL = 3.141592653589793238462643383279502884L;
+
+static ld parse(const char *s) { return std::strtold(s, nullptr); }
+
+// a_l for l = -L..L (conjugate-symmetric extension)
+static cld a_coeff(int l) {
+    int al = l < 0 ? -l : l;
+    cld a(parse(kA[al][0]), parse(kA[al][1]));
+    return l < 0 ? std::conj(a) : a;
+}
+
+long m0_for_tol(double tol, double h) {
+    // Reading G9: Appendix B applied to the shifted-Gaussian tail
+    // e^{h^2} psi_h((j+1) h) <= tol  =>  m0 = ceil(2 sqrt(h^2 - ln(sqrt(4 pi) tol)) - 1).
+    if (!(tol > 0.0)) return 11;  // eq:Mformula
+    double v = 2.0 * std::sqrt(h * h - std::log(std::sqrt(4.0 * M_PI) * tol)) - 1.0;
+    return (long)std::ceil(v);
+}
+
+static void set_err(std::vector<char> &err, const char *msg) {
+    err.assign(msg, msg + std::strlen(msg) + 1);
+}
+
+int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err) {
+    if (D < 4 || D > 8192 || (D & (D - 1)) != 0) {
+        set_err(err, "D must be a power of two in [4, 8192]");
+        return REXI_EINVAL;
+    }
+    if (!std::isfinite(tau)) { set_err(err, "tau must be finite"); return REXI_EINVAL; }
+    if (!(h > 0.0)) h = 0.5;
+    if (!(h < M_PI)) { set_err(err, "h must lie in (0, pi) (PAPER.md:98)"); return REXI_EINVAL; }
+    if (!(tol < 1.0) || std::isnan(tol)) { set_err(err, "tol must lie in (0, 1) (or <= 0 for m0 = 11)"); return REXI_EINVAL; }
+    p.D = D;
+    p.tau = tau;
+    p.tol = tol > 0.0 ? tol : 0.0;
+    p.h = h;
+    p.m0 = m0_for_tol(tol, h);
+    // eq:lswRoh in the sqrt(2) pi D form of the Sec. 4.2 display, reading G5.
+    p.rho = std::sqrt(2.0) * M_PI * D;
+    if (M <= 0) {
+        double x = std::fabs(tau) * p.rho;                 // eq:matrixAccuracyBound
+        M = (long)std::ceil(x / h) + p.m0;
+    }
+    if (M < 12) { set_err(err, "M must be >= 12 (eq:Mformula needs M - 11 >= 1)"); return REXI_EINVAL; }
+    if (M > 50000000L) { set_err(err, "M too large"); return REXI_EINVAL; }
+    p.M = M;
+    p.L = kL;
+    p.N = M + kL;
+    p.n_poles = p.N + 1;
+    const ld hh = (ld)h;
+    const ld mu = parse(kMu);
+    p.mu = (double)mu;
+    {
+        ld alias = std::exp(-4.0L * kPiL * (kPiL - hh));                 // reading G8
+        ld j1 = (ld)(p.m0 + 1) * hh;
+        ld tail = std::exp(hh * hh) * std::exp(-j1 * j1 / (4.0L * hh * hh)) / std::sqrt(4.0L * kPiL);
+        p.predicted_floor = (double)(alias + tail);
+    }
+
+    // eq:bm: b_m = e^{-i m h} e^{h^2}, m = -M..M (phase m*h in long double, G12).
+    std::vector<cld> b((size_t)(2 * M + 1));
+    const ld eh2 = std::exp(hh * hh);
+    for (long m = -M; m <= M; ++m) {
+        ld ph = (ld)m * hh;
+        b[(size_t)(m + M)] = cld(eh2 * std::cos(ph), -eh2 * std::sin(ph));
+    }
+    const long N = p.N;
+    p.alpha.assign(2 * (size_t)p.n_poles, 0.0);
+    p.C1.assign(2 * (size_t)p.n_poles, 0.0);
+    p.C2.assign(2 * (size_t)p.n_poles, 0.0);
+    p.gamma.assign((size_t)p.n_poles, 0.0);
+    p.poles.assign((size_t)p.n_poles, PoleConst{});
+    const ld c = (ld)tau;  // tau-scaled Coriolis coefficient (reading G3)
+    for (long n = 0; n <= N; ++n) {
+        // c_{1,n} = h sum_{k=L1}^{L2} Re(a_k) b_{n-k},  c_{2,n} = h sum Im(a_k) b_{n-k}
+        // L1(n) = max(-L, n - M), L2(n) = min(L, n + M)
+        long L1 = std::max<long>(-kL, n - M), L2 = std::min<long>(kL, n + M);
+        cld c1(0, 0), c2(0, 0);
+        for (long k = L1; k <= L2; ++k) {
+            cld ak = a_coeff((int)k);
+            const cld &bnk = b[(size_t)(n - k + M)];
+            c1 += ak.real() * bnk;
+            c2 += ak.imag() * bnk;
+        }
+        c1 *= hh;
+        c2 *= hh;
+        // C_{1,n} = c_{1,n} h mu + c_{2,n} h n ; C_{2,n} = i c_{2,n}
+        cld C1 = c1 * hh * mu + c2 * hh * (ld)n;
+        cld C2 = cld(0, 1) * c2;
+        cld alpha(hh * mu, hh * (ld)n);                   // alpha_n = h(mu + i n)
+        ld gam = (n == 0) ? 1.0L : 2.0L;                  // Gamma_n
+        p.alpha[2 * n] = (double)alpha.real();  p.alpha[2 * n + 1] = (double)alpha.imag();
+        p.C1[2 * n] = (double)C1.real();        p.C1[2 * n + 1] = (double)C1.imag();
+        p.C2[2 * n] = (double)C2.real();        p.C2[2 * n + 1] = (double)C2.imag();
+        p.gamma[n] = (double)gam;
+
+        // Per-pole constants of the fused kernel.
+        cld kappa = alpha * alpha + c * c;                // kappa_n (tau-scaled)
+        cld w1 = gam * C2;                                // reading G4 (division-free g3)
+        cld w2 = gam * (C1 - C2 * std::conj(alpha));
+        cld s2 = c / alpha, ia = 1.0L / alpha, s1c = std::conj(kappa / alpha);
+        cld s3 = alpha / kappa, s4 = c / kappa;
+        PoleConst &q = p.poles[(size_t)n];
+        q.ar = (double)alpha.real();  q.ai = (double)alpha.imag();
+        q.s2r = (double)s2.real();    q.s2i = (double)s2.imag();
+        q.iar = (double)ia.real();    q.iai = (double)ia.imag();
+        q.s1cr = (double)s1c.real();  q.s1ci = (double)s1c.imag();
+        q.kr = (double)kappa.real();  q.ki = (double)kappa.imag();
+        q.ki2 = (double)(kappa.imag() * kappa.imag());
+        q.w1r = (double)w1.real();    q.w1i = (double)w1.imag();
+        q.w2r = (double)w2.real();    q.w2i = (double)w2.imag();
+        q.s3r = (double)s3.real();    q.s3i = (double)s3.imag();
+        q.s4r = (double)s4.real();    q.s4i = (double)s4.imag();
+        q.pad = 0.0;
+    }
+
+    // Fourier symbols: index j -> wavenumber k = j (j < D/2) else j - D; 2 pi k tau;
+    // Nyquist index D/2 -> 0 (reading G2).
+    p.ksym.assign((size_t)D, 0.0);
+    for (int j = 0; j < D; ++j) {
+        long k = (j < D / 2) ? j : (long)j - D;
+        p.ksym[(size_t)j] = (j == D / 2) ? 0.0 : (double)(2.0L * kPiL * (ld)k * (ld)tau);
+    }
+    // FFT twiddles e^{-2 pi i j / D}, j = 0..D/2-1.
+    p.twiddle.assign((size_t)D, 0.0);
+    for (int j = 0; j < D / 2; ++j) {
+        ld th = 2.0L * kPiL * (ld)j / (ld)D;
+        p.twiddle[2 * (size_t)j] = (double)std::cos(th);
+        p.twiddle[2 * (size_t)j + 1] = (double)(-std::sin(th));
+    }
+    return REXI_OK;
+}
+
+}  // namespace rexi
+
+extern "C" int rexi_appendix_a(double *mu, double *a) {
+    if (mu) *mu = (double)rexi::parse(rexi::kMu);
+    if (a)
+        for (int l = 0; l <= rexi::kL; ++l) {
+            a[2 * l] = (double)rexi::parse(rexi::kA[l][0]);
+            a[2 * l + 1] = (double)rexi::parse(rexi::kA[l][1]);
+        }
+    return rexi::kL;
+}
+
+extern "C" long rexi_rule_M(int D, double tau, double tol, double h) {
+    if (!(h > 0.0)) h = 0.5;
+    double x = std::fabs(tau) * (std::sqrt(2.0) * M_PI * D);
+    return (long)std::ceil(x / h) + rexi::m0_for_tol(tol, h);
+}
+
+extern "C" long rexi_terms_host(double h, long M, double *alpha, double *C1, double *C2, double *gamma) {
+    if (!(h > 0.0 && h < M_PI) || M < 12) return -1;
+    rexi::Plan p;
+    std::vector<char> err;
+    try {
+        // D and tau do not enter the term table; D = 4, tau = 0 keep the rest cheap.
+        if (rexi::make_plan(p, 4, 0.0, 0.0, h, M, err) != REXI_OK) return -1;
+    } catch (...) {
+        return -1;
+    }
+    const size_t n = (size_t)p.n_poles;
+    if (alpha) std::memcpy(alpha, p.alpha.data(), 2 * n * sizeof(double));
+    if (C1) std::memcpy(C1, p.C1.data(), 2 * n * sizeof(double));
+    if (C2) std::memcpy(C2, p.C2.data(), 2 * n * sizeof(double));
+    if (gamma) std::memcpy(gamma, p.gamma.data(), n * sizeof(double));
+    return p.n_poles;
+}

@@ -1,0 +1,47 @@
+// planner.h — host planner of librexi (internal header; not part of the C ABI).
+//
+// Produces, in x87 extended precision rounded to fp64, the REXII term table of
+// arXiv:2008.11607 and the per-pole constants consumed by the fused pole kernel.
+#pragma once
+
+#include <vector>
+
+namespace rexi {
+
+// Per-pole constants of the pole kernel (device layout, 20 doubles = 160 B).
+// c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
+// the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
+struct alignas(16) PoleConst {
+    double ar, ai;      // alpha_n = h(mu + i n)
+    double s2r, s2i;    // c / alpha
+    double iar, iai;    // 1 / alpha
+    double s1cr, s1ci;  // conj(kappa / alpha) = conj(kappa)/conj(alpha)
+    double kr, ki;      // kappa
+    double ki2;         // Im(kappa)^2
+    double w1r, w1i;    // Gamma_n C2_n
+    double w2r, w2i;    // Gamma_n (C1_n - C2_n alpha_{-n})
+    double s3r, s3i;    // alpha / kappa   (eq:lswVelocities, UV variant)
+    double s4r, s4i;    // c / kappa
+    double pad;
+};
+static_assert(sizeof(PoleConst) == 160, "PoleConst layout");
+
+struct Plan {
+    int D = 0;
+    double tau = 0, tol = 0, h = 0, mu = 0;
+    long M = 0, L = 24, N = 0, n_poles = 0, m0 = 11;
+    double rho = 0, predicted_floor = 0;
+    // term table, n = 0..N (interleaved re/im for complex entries)
+    std::vector<double> alpha, C1, C2, gamma;
+    std::vector<PoleConst> poles;
+    std::vector<double> ksym;        // D tau-scaled derivative symbols, Nyquist zeroed (G2)
+    std::vector<double> twiddle;     // D/2 complex e^{-2 pi i j / D}
+};
+
+// Validates the arguments (see rexi.h) and fills `p`. Returns 0 or a rexi_status_t code;
+// `err` receives a message.
+int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err);
+
+long m0_for_tol(double tol, double h);
+
+}  // namespace rexi

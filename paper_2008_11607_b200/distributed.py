@@ -1,0 +1,44 @@
+"""Pole ("time") parallelism across GPUs.
+
+The N+1 poles of the half-sum are independent and cost the same, so rank r of P
+evaluates the contiguous block [r (N+1) / P, (r+1)(N+1) / P) through
+``rexi_apply_partial`` (forward FFT, its poles, inverse FFT + Re — the inverse
+transform and Re are real-linear, so they commute with the sum), and ONE
+all-reduce (sum, fp64) over NCCL/NVLink combines the three real fields
+(option b of SURVEY.md 8(e): 3 D^2 doubles instead of 3 D^2 complex).
+"""
+from __future__ import annotations
+
+
+def pole_partition(n_poles, world_size, rank):
+    """Contiguous block of rank `rank`; block sizes differ by at most one pole."""
+    if world_size < 1 or not (0 <= rank < world_size):
+        raise ValueError("bad rank / world size")
+    return (n_poles * rank) // world_size, (n_poles * (rank + 1)) // world_size
+
+
+def pole_parallel_step(partial_fn, n_poles, out, group=None):
+    """Generic S3 + S4: ``partial_fn(begin, end, out)`` writes this rank's partial result
+    into ``out`` (a tensor holding the three fields); then one all-reduce(sum)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    b, e = pole_partition(n_poles, world, rank)
+    partial_fn(b, e, out)
+    if world > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out
+
+
+def apply_distributed(plan, eta, u, v, out=None, group=None):
+    """One REXII step with the poles split over the ranks of `group` (one GPU per rank).
+
+    ``out`` (optional) is a contiguous (3, D, D) float64 CUDA tensor; returns it."""
+    import torch
+    if out is None:
+        out = torch.empty((3, plan.D, plan.D), dtype=torch.float64, device=eta.device)
+
+    def partial(b, e, buf):
+        plan.apply_partial(b, e, eta, u, v, out=(buf[0], buf[1], buf[2]))
+
+    return pole_parallel_step(partial, plan.n_poles, out, group)

@@ -1,0 +1,281 @@
+"""Thin ctypes binding of librexi.so (include/rexi.h) — argument marshalling only.
+
+Every step of the REXII path runs in the library's CUDA kernels; this module only
+checks tensor shapes/dtypes/devices, passes raw pointers and the current torch
+stream, and turns status codes into exceptions. There is no CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librexi.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_2008_11607_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
+VARIANTS = {"dz": 0, "uv": 1}
+
+_vp = ctypes.c_void_p
+_dp = ctypes.POINTER(ctypes.c_double)
+_lp = ctypes.POINTER(ctypes.c_long)
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("D", ctypes.c_int), ("variant", ctypes.c_int), ("tau", ctypes.c_double),
+                ("tol", ctypes.c_double), ("h", ctypes.c_double), ("mu", ctypes.c_double),
+                ("M", ctypes.c_long), ("L", ctypes.c_long), ("N", ctypes.c_long),
+                ("n_poles", ctypes.c_long), ("m0", ctypes.c_long), ("rho", ctypes.c_double),
+                ("predicted_floor", ctypes.c_double), ("flops_per_pole_mode", ctypes.c_double),
+                ("fp64_ops_per_pole_mode", ctypes.c_double)]
+
+
+EXPORTS = {
+    "rexi_plan_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_long, ctypes.c_int]),
+    "rexi_plan_destroy": (ctypes.c_int, [_vp]),
+    "rexi_plan_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
+    "rexi_plan_set_variant": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
+    "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "rexi_poles": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp]),
+    "rexi_inverse": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "rexi_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rexi_apply_partial": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp,
+                                          _vp, _vp, _vp, _vp]),
+    "rexi_apply_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rexi_run": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "rexi_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_timing_read": (ctypes.c_int, [_vp, _dp, _lp, _lp]),
+    "rexi_appendix_a": (ctypes.c_int, [_dp, _dp]),
+    "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, _dp, _dp, _dp, _dp]),
+    "rexi_rule_M": (ctypes.c_long, [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
+    "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "rexi_last_error": (ctypes.c_char_p, []),
+    "rexi_abi_version": (ctypes.c_int, []),
+}
+for _name, (_res, _args) in EXPORTS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+class RexiError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        msg = _lib.rexi_status_string(status).decode()
+        detail = _lib.rexi_last_error().decode()
+        super().__init__(f"{where}: {msg} ({detail})")
+
+
+def _check(status, where):
+    if status != REXI_OK:
+        raise RexiError(status, where)
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+# ----------------------------------------------------------------------------- host-only
+def appendix_a():
+    """(mu, a[25] complex) compiled into the library."""
+    mu = ctypes.c_double()
+    L = _lib.rexi_appendix_a(ctypes.byref(mu), None)
+    a = np.zeros(2 * (L + 1))
+    _lib.rexi_appendix_a(ctypes.byref(mu), _np_ptr(a))
+    return mu.value, a[0::2] + 1j * a[1::2]
+
+
+def terms_host(h, M):
+    """The planner's half-sum table (alpha, C1, C2, gamma) for (h, M), computed on the host."""
+    n = _lib.rexi_terms_host(float(h), int(M), None, None, None, None)
+    if n < 0:
+        raise ValueError("invalid h or M")
+    al, c1, c2 = (np.zeros(2 * n) for _ in range(3))
+    g = np.zeros(n)
+    _lib.rexi_terms_host(float(h), int(M), _np_ptr(al), _np_ptr(c1), _np_ptr(c2), _np_ptr(g))
+    z = lambda x: x[0::2] + 1j * x[1::2]
+    return z(al), z(c1), z(c2), g
+
+
+def rule_M(D, tau, tol, h=0.5):
+    return int(_lib.rexi_rule_M(int(D), float(tau), float(tol), float(h)))
+
+
+def abi_version():
+    return _lib.rexi_abi_version()
+
+
+# ----------------------------------------------------------------------------- plans
+def _torch():
+    import torch
+    return torch
+
+
+class Plan:
+    """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
+
+    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="dz"):
+        torch = _torch()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self._h = _vp()
+        _check(_lib.rexi_plan_create(ctypes.byref(self._h), int(D), float(tau),
+                                     float(tol if tol is not None else 0.0),
+                                     float(h), int(M), self.device), "rexi_plan_create")
+        self.set_variant(variant)
+        inf = self.info
+        self.D = inf["D"]
+        self.n_poles = inf["n_poles"]
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.rexi_plan_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- metadata
+    @property
+    def info(self):
+        i = PlanInfo()
+        _check(_lib.rexi_plan_info(self._h, ctypes.byref(i)), "rexi_plan_info")
+        return {k: getattr(i, k) for k, _ in PlanInfo._fields_}
+
+    def set_variant(self, variant):
+        v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+        _check(_lib.rexi_plan_set_variant(self._h, v), "rexi_plan_set_variant")
+        self.variant = v
+
+    def coeffs(self):
+        n = self.n_poles
+        al, c1, c2 = (np.zeros(2 * n) for _ in range(3))
+        g = np.zeros(n)
+        _check(_lib.rexi_plan_coeffs(self._h, _np_ptr(al), _np_ptr(c1), _np_ptr(c2), _np_ptr(g)),
+               "rexi_plan_coeffs")
+        z = lambda x: x[0::2] + 1j * x[1::2]
+        return z(al), z(c1), z(c2), g
+
+    # -- tensor checks
+    def _stream(self):
+        torch = _torch()
+        return _vp(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _field(self, t, name):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda \
+                or t.device.index != self.device or tuple(t.shape) != (self.D, self.D) \
+                or not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous float64 ({self.D}, {self.D}) tensor "
+                             f"on cuda:{self.device}")
+        return _vp(t.data_ptr())
+
+    def _spec(self, t, name):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or not t.is_cuda \
+                or t.device.index != self.device or tuple(t.shape) != (3, self.D, self.D) \
+                or not t.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous complex128 (3, {self.D}, {self.D}) "
+                             f"tensor on cuda:{self.device}")
+        return _vp(t.data_ptr())
+
+    def _new_fields(self):
+        torch = _torch()
+        return tuple(torch.empty((self.D, self.D), dtype=torch.float64, device=f"cuda:{self.device}")
+                     for _ in range(3))
+
+    def _new_spec(self):
+        torch = _torch()
+        return torch.empty((3, self.D, self.D), dtype=torch.complex128, device=f"cuda:{self.device}")
+
+    # -- the path
+    def forward(self, eta, u, v, fhat=None):
+        fhat = self._new_spec() if fhat is None else fhat
+        _check(_lib.rexi_forward(self._h, self._field(eta, "eta"), self._field(u, "u"),
+                                 self._field(v, "v"), self._spec(fhat, "fhat"), self._stream()),
+               "rexi_forward")
+        return fhat
+
+    def poles(self, fhat, begin=0, end=None, acc=None):
+        end = self.n_poles if end is None else end
+        acc = self._new_spec() if acc is None else acc
+        _check(_lib.rexi_poles(self._h, int(begin), int(end), self._spec(fhat, "fhat"),
+                               self._spec(acc, "acc"), self._stream()), "rexi_poles")
+        return acc
+
+    def inverse(self, acc, out=None):
+        out = self._new_fields() if out is None else out
+        _check(_lib.rexi_inverse(self._h, self._spec(acc, "acc"), *(self._field(o, "out") for o in out),
+                                 self._stream()), "rexi_inverse")
+        return out
+
+    def apply(self, eta, u, v, out=None):
+        out = self._new_fields() if out is None else out
+        _check(_lib.rexi_apply(self._h, self._field(eta, "eta"), self._field(u, "u"), self._field(v, "v"),
+                               *(self._field(o, "out") for o in out), self._stream()), "rexi_apply")
+        return out
+
+    def apply_partial(self, begin, end, eta, u, v, out=None):
+        out = self._new_fields() if out is None else out
+        _check(_lib.rexi_apply_partial(self._h, int(begin), int(end), self._field(eta, "eta"),
+                                       self._field(u, "u"), self._field(v, "v"),
+                                       *(self._field(o, "out") for o in out), self._stream()),
+               "rexi_apply_partial")
+        return out
+
+    def apply_host(self, eta, u, v, out=None):
+        """Host buffers in and out (numpy float64 arrays or CPU tensors, ideally pinned)."""
+        def ptr(a, name):
+            if isinstance(a, np.ndarray):
+                if a.dtype != np.float64 or a.shape != (self.D, self.D) or not a.flags.c_contiguous:
+                    raise ValueError(f"{name}: expected C-contiguous float64 ({self.D}, {self.D})")
+                return _vp(a.ctypes.data)
+            torch = _torch()
+            if a.device.type != "cpu" or a.dtype != torch.float64 or tuple(a.shape) != (self.D, self.D) \
+                    or not a.is_contiguous():
+                raise ValueError(f"{name}: expected a contiguous float64 CPU tensor")
+            return _vp(a.data_ptr())
+        if out is None:
+            out = tuple(np.empty((self.D, self.D)) for _ in range(3))
+        _check(_lib.rexi_apply_host(self._h, ptr(eta, "eta"), ptr(u, "u"), ptr(v, "v"),
+                                    *(ptr(o, "out") for o in out), self._stream()), "rexi_apply_host")
+        return out
+
+    def run(self, steps, eta, u, v):
+        """`steps` REXII steps in place (S6, T_final = steps * tau)."""
+        _check(_lib.rexi_run(self._h, int(steps), self._field(eta, "eta"), self._field(u, "u"),
+                             self._field(v, "v"), self._stream()), "rexi_run")
+        return eta, u, v
+
+    # -- timing of the dominant kernel
+    def timing_enable(self, on=True):
+        _check(_lib.rexi_timing_enable(self._h, int(bool(on))), "rexi_timing_enable")
+
+    def timing_read(self):
+        ms = ctypes.c_double()
+        pl = ctypes.c_long()
+        tl = ctypes.c_long()
+        _check(_lib.rexi_timing_read(self._h, ctypes.byref(ms), ctypes.byref(pl), ctypes.byref(tl)),
+               "rexi_timing_read")
+        return ms.value, pl.value, tl.value

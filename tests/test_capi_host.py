@@ -1,0 +1,79 @@
+"""Host-side checks of the C ABI (no GPU): librexi.so loads, exports every function that
+include/rexi.h declares, and its host-only planner entries (S0 of SURVEY.md 8(a)) agree with
+the independent oracle and the paper."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, read_appendix_a
+from oracle import coeffs as C
+
+
+@pytest.fixture(scope="module")
+def rexi():
+    from paper_2008_11607_b200 import build
+    build.build()
+    from paper_2008_11607_b200 import rexi as R
+    return R
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "rexi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rexi_[A-Za-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(rexi):
+    names = header_functions()
+    assert len(names) >= 20
+    lib = ctypes.CDLL(rexi.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    # and the binding declares a prototype for each one
+    assert set(names) == set(rexi.EXPORTS), set(names) ^ set(rexi.EXPORTS)
+
+
+def test_abi_version(rexi):
+    assert rexi.abi_version() == 1
+
+
+def test_appendix_a_compiled_table_matches_golden(rexi):
+    mu, rows = read_appendix_a()
+    lmu, a = rexi.appendix_a()
+    assert lmu == float(mu)
+    assert len(a) == len(rows) == 25
+    for (l, re_, im_), al in zip(rows, a):
+        assert al.real == float(re_) and al.imag == float(im_), l
+
+
+@pytest.mark.parametrize("h,M", [(0.5, 22), (0.5, 65), (1.0, 38), (0.1, 278), (0.5, 1149),
+                                 (0.2, 150), (0.5, 4558), (0.3, 2000)])
+def test_planner_terms_match_oracle(rexi, h, M):
+    """S0 parity: the planner's alpha_n, C_{1,n}, C_{2,n}, Gamma_n (C++ long double) vs the
+    oracle's (numpy longdouble), two independent implementations of PAPER.md:201-282, 321."""
+    al, c1, c2, g = rexi.terms_host(h, M)
+    n, oal, oc1, oc2, og = C.rexii_terms(h, M).half()
+    assert len(al) == len(oal) == M + 25
+    assert np.array_equal(g, og)
+    assert np.abs(al - oal).max() <= 1e-15 * np.abs(oal).max()
+    scale = max(np.abs(oc1).max(), np.abs(oc2).max())
+    assert np.abs(c1 - oc1).max() <= 2e-15 * scale
+    assert np.abs(c2 - oc2).max() <= 2e-15 * scale
+
+
+@pytest.mark.parametrize("D,tau,tol,h", [(512, 1.0, 1e-8, 0.5), (64, 0.02, 1e-12, 0.5),
+                                         (1024, 0.1, 1e-12, 0.5), (4096, 1.0, 1e-12, 0.5),
+                                         (128, 1.0, 0.0, 0.5), (128, 1.0, 0.0, 1.0),
+                                         (128, -3.0, 1e-10, 0.3)])
+def test_rule_M_matches_oracle(rexi, D, tau, tol, h):
+    assert rexi.rule_M(D, tau, tol, h) == C.M_lrsw(D, tau, h, tol if tol > 0 else None)
+
+
+def test_terms_host_rejects_bad_args(rexi):
+    with pytest.raises(ValueError):
+        rexi.terms_host(3.5, 50)
+    with pytest.raises(ValueError):
+        rexi.terms_host(0.5, 5)

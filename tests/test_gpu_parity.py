@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element on the
+same seeded inputs. Tolerance (north_star): relative L2 <= 1e-12 in fp64 with identical
+coefficients (the planner's and the oracle's tables agree to ~1e-15, test_capi_host.py)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import coeffs as C
+from oracle import lrsw
+from paper_2008_11607_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def R():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2008_11607_b200 import build
+    build.build()
+    from paper_2008_11607_b200 import rexi
+    return rexi
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_l2(a, b):
+    a = np.concatenate([np.ravel(x) for x in a])
+    b = np.concatenate([np.ravel(x) for x in b])
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def oracle_terms(plan):
+    h, M = plan.info["h"], plan.info["M"]
+    return C.rexii_terms(h, M)
+
+
+# ----------------------------------------------------------------------------- S0
+def test_plan_coeffs_match_oracle(R):
+    p = R.Plan(512, 1.0, tol=1e-8)
+    assert p.info["M"] == 4558 and p.n_poles == 4583
+    al, c1, c2, g = p.coeffs()
+    n, oal, oc1, oc2, og = oracle_terms(p).half()
+    s = np.abs(oc1).max()
+    assert np.abs(al - oal).max() < 1e-14 * np.abs(oal).max()
+    assert np.abs(c1 - oc1).max() < 2e-15 * s and np.abs(c2 - oc2).max() < 2e-15 * s
+    assert np.array_equal(g, og)
+
+
+def test_plan_errors(R):
+    with pytest.raises(R.RexiError):
+        R.Plan(100, 1.0)                # not a power of two
+    with pytest.raises(R.RexiError):
+        R.Plan(64, 1.0, h=3.5)
+    with pytest.raises(R.RexiError):
+        R.Plan(64, float("nan"))
+    with pytest.raises(R.RexiError):
+        R.Plan(64, 1.0, M=5)
+    p = R.Plan(16, 0.1)
+    import torch
+    f = torch.zeros((3, 16, 16), dtype=torch.complex128, device="cuda")
+    with pytest.raises(R.RexiError):
+        p.poles(f, 0, p.n_poles + 1)
+    with pytest.raises(R.RexiError):
+        p.poles(f, 5, 4)
+    with pytest.raises(ValueError):
+        p.apply(*(torch.zeros((8, 8), dtype=torch.float64, device="cuda") for _ in range(3)))
+
+
+# ----------------------------------------------------------------------------- S1 / S5
+@pytest.mark.parametrize("D", [4, 8, 64, 128, 256, 512])
+def test_forward_fft_vs_naive_dft(R, D):
+    p = R.Plan(D, 0.1)
+    f = inputs.white_noise(D)
+    F = host(p.forward(*(dev(x) for x in f)))
+    import torch
+    torch.cuda.synchronize()
+    for c in range(3):
+        O = lrsw.dft2(f[c])
+        assert np.linalg.norm(F[c] - O) / np.linalg.norm(O) < 1e-14
+
+
+@pytest.mark.parametrize("D", [4, 8, 64, 512])
+def test_inverse_fft_vs_naive_dft(R, D):
+    p = R.Plan(D, 0.1)
+    A = inputs.spectral_white(D, seed=3)
+    out = [host(t) for t in p.inverse(dev(A))]
+    for c in range(3):
+        O = lrsw.idft2_real(A[c])
+        assert np.linalg.norm(out[c] - O) / np.linalg.norm(O) < 1e-14
+
+
+def test_fft_4096_sampled(R):
+    """Full C4 grid size: sampled entries of the forward transform vs the DFT definition."""
+    D = 4096
+    p = R.Plan(D, 1.0, tol=1e-12)
+    g = np.random.Generator(np.random.PCG64(1))
+    X = g.standard_normal((D, D))
+    import torch
+    Z = torch.zeros((D, D), dtype=torch.float64, device="cuda")
+    F = p.forward(dev(X), Z, Z)
+    F0 = host(F[0])
+    x = np.arange(D)
+    for (l, k) in [(0, 0), (1, 0), (0, 2048), (2048, 2048), (17, 4095), (3000, 1234)]:
+        ph = np.exp(-2j * np.pi * ((k * x[None, :] + l * x[:, None]) % D) / D)
+        ref = (X * ph).sum() / D ** 2
+        assert abs(F0[l, k] - ref) < 1e-13 * np.sqrt(D * D) / D ** 2 * 50
+
+
+# ----------------------------------------------------------------------------- S2 + S3
+def _pole_parity(R, D, tau, tol, variant, modes=None, begin=0, end=None, seed=5):
+    p = R.Plan(D, tau, tol=tol, variant=variant)
+    end = p.n_poles if end is None else end
+    F = inputs.spectral_white(D, seed=seed)
+    acc = host(p.poles(dev(F), begin, end))
+    n, al, c1, c2, gm = oracle_terms(p).half()
+    if modes is None:
+        ml, mk = lrsw.all_modes(D)
+    else:
+        ml, mk = modes
+    fm = np.stack([F[c][ml, mk] for c in range(3)], axis=-1)
+    ref = lrsw.rexii_pole_sum(D, tau, fm, ml, mk, al[begin:end], c1[begin:end], c2[begin:end],
+                              gm[begin:end])
+    got = np.stack([acc[c][ml, mk] for c in range(3)], axis=-1)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    # per-mode check too: each sampled mode within 1e-11 relative of its own magnitude
+    pm = np.linalg.norm(got - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+    return err, float(pm.max())
+
+
+@pytest.mark.parametrize("variant", ["dz", "uv"])
+@pytest.mark.parametrize("D,tau,tol", [(4, 0.5, 1e-12), (8, 1.0, 1e-12), (64, 0.02, 1e-12),
+                                       (64, 1.0, 1e-12), (32, 5.0, 1e-8)])
+def test_pole_kernel_full_grid(R, variant, D, tau, tol):
+    err, pm = _pole_parity(R, D, tau, tol, variant)
+    assert err < TOL, err
+    assert pm < 1e-11, pm
+
+
+@pytest.mark.parametrize("variant", ["dz", "uv"])
+def test_pole_kernel_ranges(R, variant):
+    D, tau = 64, 1.0
+    for (b, e) in [(0, 1), (1, 2), (0, 37), (100, 333), (500, 604)]:
+        err, pm = _pole_parity(R, D, tau, 1e-12, variant, begin=b, end=e)
+        assert err < TOL, (b, e, err)
+
+
+def test_pole_kernel_empty_range_is_zero(R):
+    p = R.Plan(16, 1.0)
+    import torch
+    F = dev(inputs.spectral_white(16))
+    acc = p.poles(F, 7, 7)
+    assert float(acc.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("variant", ["dz", "uv"])
+def test_pole_kernel_c2_full_size_sampled(R, variant):
+    """BASELINE configs[1] (512^2, tau = 1, tol 1e-8, 4583 poles) in the launch configuration
+    bench.py times; 2048 sampled modes incl. K = 0, Nyquist row/column and the corner."""
+    modes = inputs.sample_modes(512, 2048)
+    err, pm = _pole_parity(R, 512, 1.0, 1e-8, variant, modes=modes)
+    assert err < TOL, err
+    assert pm < 1e-11, pm
+
+
+def test_pole_kernel_c4_size_sampled(R):
+    """4096^2 grid (configs[3]) on a pole sub-range, 512 sampled modes."""
+    modes = inputs.sample_modes(4096, 512)
+    err, pm = _pole_parity(R, 4096, 1.0, 1e-12, "dz", modes=modes, begin=30000, end=30400)
+    assert err < TOL, err
+
+
+# ----------------------------------------------------------------------------- S1..S5
+@pytest.mark.parametrize("variant", ["dz", "uv"])
+@pytest.mark.parametrize("D,tau,tol,scen", [(64, 0.02, 1e-12, "gauss"), (64, 0.02, 1e-12, "white"),
+                                            (128, 1.0, 1e-12, "gauss"), (32, 3.0, 1e-10, "white"),
+                                            (8, 0.7, 1e-12, "white")])
+def test_apply_vs_oracle(R, variant, D, tau, tol, scen):
+    f = inputs.gaussian_scenario(D) if scen == "gauss" else inputs.white_noise(D)
+    p = R.Plan(D, tau, tol=tol, variant=variant)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    info = p.info
+    ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])
+    assert rel_l2(got, ref) < TOL
+    ex = lrsw.exact_step(*f, tau)
+    assert rel_l2(got, ex) < max(tol, 1e-13)
+
+
+def test_apply_c2_full_size_properties(R):
+    """Full C2 (512^2, tau=1, tol=1e-8), Gaussian scenario: vs the exact per-mode propagator
+    within tol, energy conservation and mean(eta) conservation."""
+    D = 512
+    f = inputs.gaussian_scenario(D)
+    p = R.Plan(D, 1.0, tol=1e-8)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    ex = lrsw.exact_step(*f, 1.0)
+    assert rel_l2(got, ex) < 1e-8
+    e0 = sum(float((x ** 2).sum()) for x in f)
+    e1 = sum(float((x ** 2).sum()) for x in got)
+    assert abs(e1 - e0) / e0 < 1e-8
+    assert abs(got[0].mean() - f[0].mean()) < 1e-13
+
+
+def test_apply_partial_partition_invariance(R):
+    """S4 on one GPU: sum over a pole partition of rexi_apply_partial == rexi_apply."""
+    from paper_2008_11607_b200.distributed import pole_partition
+    D = 64
+    f = [dev(x) for x in inputs.white_noise(D)]
+    p = R.Plan(D, 1.0)
+    full = [host(t) for t in p.apply(*f)]
+    for P in (2, 3, 8):
+        tot = [np.zeros((D, D)) for _ in range(3)]
+        for r in range(P):
+            b, e = pole_partition(p.n_poles, P, r)
+            part = p.apply_partial(b, e, *f)
+            for c in range(3):
+                tot[c] += host(part[c])
+        assert rel_l2(tot, full) < 1e-14
+
+
+def test_apply_in_place_and_host_and_run(R):
+    import torch
+    D, tau = 32, 0.4
+    f = inputs.white_noise(D)
+    p = R.Plan(D, tau)
+    ref = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    # host-buffer entry
+    hout = p.apply_host(*(np.ascontiguousarray(x) for x in f))
+    assert rel_l2(hout, ref) == 0.0
+    # in place
+    t = [dev(x) for x in f]
+    p.apply(*t, out=t)
+    assert rel_l2([host(x) for x in t], ref) == 0.0
+    # multi-step driver (S6): 3 steps vs 3 oracle steps
+    t = [dev(x) for x in f]
+    p.run(3, *t)
+    g = f
+    info = p.info
+    terms = C.rexii_terms(info["h"], info["M"])
+    for _ in range(3):
+        g = lrsw.rexii_step(*g, tau, info["h"], info["M"], terms=terms)
+    assert rel_l2([host(x) for x in t], g) < TOL
+
+
+def test_variants_agree(R):
+    D = 128
+    f = [dev(x) for x in inputs.white_noise(D)]
+    a = R.Plan(D, 2.0, variant="dz")
+    b = R.Plan(D, 2.0, variant="uv")
+    ra = [host(t) for t in a.apply(*f)]
+    rb = [host(t) for t in b.apply(*f)]
+    assert rel_l2(ra, rb) < TOL
+
+
+def test_timing_counters(R):
+    D = 64
+    f = [dev(x) for x in inputs.white_noise(D)]
+    p = R.Plan(D, 1.0)
+    p.timing_enable(True)
+    p.timing_read()
+    for _ in range(3):
+        p.apply(*f)
+    ms, pl, tl = p.timing_read()
+    assert pl == 3 and ms > 0.0 and tl == 3 * 7

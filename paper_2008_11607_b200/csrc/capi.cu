@@ -53,9 +53,9 @@ struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
     int variant = REXI_VARIANT_DZ;
+    int mpt = 2;            // Fourier modes per thread in the pole kernel
     long n_modes = 0;
     int num_sms = 0;
-    int occ[2] = {0, 0};
     int max_chunks = 1;
     // device buffers
     rexi::PoleConst *d_poles = nullptr;
@@ -94,9 +94,11 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range) {
     if (n_range <= 0) return 0;
-    const long mpb = rexi::pole_modes_per_block();
+    const long mpb = rexi::pole_modes_per_block(p->mpt);
     const long tiles = (p->n_modes + mpb - 1) / mpb;
-    const long conc = (long)p->num_sms * std::max(1, p->occ[p->variant]);
+    int occ = 1;
+    if (rexi::pole_occupancy(p->variant, p->mpt, &occ) != cudaSuccess) occ = 1;
+    const long conc = (long)p->num_sms * std::max(1, occ);
     const long max_c = std::max(1L, std::min<long>(p->max_chunks, n_range / 4));
     int best = 1;
     double best_eff = 0.0;
@@ -173,9 +175,10 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.log2D = 0;
     while ((1 << a.log2D) < a.D) ++a.log2D;
     a.tau = p->host.tau;
+    a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    CK(rexi::launch_poles(a, p->variant, st));
+    CK(rexi::launch_poles(a, p->variant, p->mpt, st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     rexi::FinishArgs f;
@@ -290,8 +293,6 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     if ((e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device)))
         return cleanup_fail(cuda_fail(e, "cudaDeviceGetAttribute"));
     if ((e = rexi::fft_setup_attributes())) return cleanup_fail(cuda_fail(e, "cudaFuncSetAttribute"));
-    if ((e = rexi::pole_occupancy(0, &p->occ[0]))) return cleanup_fail(cuda_fail(e, "occupancy"));
-    if ((e = rexi::pole_occupancy(1, &p->occ[1]))) return cleanup_fail(cuda_fail(e, "occupancy"));
     const size_t field = sizeof(cd) * 3 * (size_t)p->n_modes;
     // Partial-sum buffer: at most 64 chunks and at most ~2 GiB.
     const size_t budget = (size_t)2 << 30;
@@ -347,6 +348,13 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
     if (variant != REXI_VARIANT_DZ && variant != REXI_VARIANT_UV) return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    if (!rexi::pole_mpt_supported(modes_per_thread)) return fail(REXI_EINVAL, "modes_per_thread must be 1, 2 or 4");
+    p->mpt = modes_per_thread;
     return REXI_OK;
 }
 

@@ -106,38 +106,42 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftArgs a) {
 // Per mode (k, l): Kx = 2 pi k tau, Ky = 2 pi l tau (Nyquist zeroed), K2 = Kx^2 + Ky^2,
 // c = tau. Input f0 = (e0, a, b) = (eta0^, u0^, v0^).
 //   delta0 = i(Kx a + Ky b), zeta0 = i(Kx b - Ky a)        (tau-scaled)
-//   m0 = zeta0 - c e0
+//   m0 = zeta0 - c e0,  B0 = h mu e0 + delta0              (per mode, pole-independent)
 // Solve 1, (alpha I + tau A) g1 = f0 — Helmholtz reduction (eq:lswEta):
 //   eta1 (kappa + K2) = kappa/alpha e0 + delta0 - c/alpha zeta0 = alpha e0 + delta0 - (c/alpha) m0
+//                     = B0 + i h n e0 - (c/alpha) m0          (alpha = h mu + i h n)
+//   q = 1/(kappa + K2) = (dr - i ki)/(dr^2 + ki^2), dr = Re(kappa) + K2, ki = Im(kappa)
 // Solve 2, (conj(alpha) I - tau A) g2 = g1: same with (alpha, Kx, Ky, c) -> (conj alpha, -Kx,
-//   -Ky, -c); its denominator is conj(kappa + K2), so one reciprocal serves both solves.
+//   -Ky, -c); its denominator is conj(kappa + K2): eta2 = num2 * conj(q) (one reciprocal).
 // DZ variant (default): back-substitution in (delta, zeta) = divergence/vorticity of g:
-//   delta1 = alpha eta1 - e0,          zeta1 = (m0)/alpha + c eta1
-//   eta2 (conj(kappa) + K2) = conj(kappa/alpha) eta1 - delta1 - (c/conj(alpha)) zeta1
-//   delta2 = eta1 - conj(alpha) eta2,  zeta2 = (zeta1 - c delta2)/conj(alpha)
+//   delta1 = alpha eta1 - e0,  zeta1 = m0/alpha + c eta1
+//   num2 = conj(kappa/alpha) eta1 - delta1 - (c/conj(alpha)) zeta1,  eta2 = num2 conj(q)
+//   delta2 = eta1 - conj(alpha) eta2,  zeta2 = (zeta1 - c delta2)/conj(alpha) = |1/alpha|^2 m0 + c eta2
 //   acc(eta, delta, zeta) += w1 g1 + w2 g2;  (u, v) recovered per mode in finish_kernel.
 // UV variant (paper-literal eq:lswVelocities): (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (p,q),
 //   p = a + i Kx eta1, q = b + i Ky eta1; delta1, zeta1 from (u1, v1); likewise for g2.
+// fp64-pipe instructions per (pole, mode): DZ 71, UV 102 (launch.h).
 constexpr int kPoleBlock = 128;
 constexpr int kPoleTile = 32;
-constexpr int kMPT = 2;
 
-template <int VARIANT>
-__global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(PoleArgs a) {
+template <int VARIANT, int MPT>
+__global__ void __launch_bounds__(kPoleBlock, (VARIANT == 0 ? 8 : 6) / MPT)
+pole_kernel(PoleArgs a) {
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
-    const long tile0 = (long)blockIdx.x * (kPoleBlock * kMPT);
+    const long tile0 = (long)blockIdx.x * (kPoleBlock * MPT);
     const int chunk = blockIdx.y;
     const long len = a.pole_end - a.pole_begin;
     const long p0 = a.pole_begin + len * chunk / a.n_chunks;
     const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
     const double c = a.tau;
+    const double hmu = a.hmu;
 
-    cd e0[kMPT], d0[kMPT], m0[kMPT], ua[kMPT], vb[kMPT];
-    double K2[kMPT], Kx[kMPT], Ky[kMPT];
-    cd A0[kMPT], A1[kMPT], A2[kMPT];
+    cd e0[MPT], B0[MPT], m0[MPT], ua[MPT], vb[MPT];
+    double K2[MPT], Kx[MPT], Ky[MPT];
+    cd A0[MPT], A1[MPT], A2[MPT];
 #pragma unroll
-    for (int j = 0; j < kMPT; ++j) {
+    for (int j = 0; j < MPT; ++j) {
         const long m = tile0 + j * kPoleBlock + threadIdx.x;
         const long mm = m < n_modes ? m : 0;
         const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
@@ -149,8 +153,9 @@ __global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(
         Kx[j] = kx;
         Ky[j] = ky;
         // delta0 = i (kx u + ky v) ; zeta0 = i (kx v - ky u)
-        d0[j] = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
+        const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
         const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
+        B0[j] = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
         m0[j] = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
         K2[j] = fma(kx, kx, ky * ky);
         A0[j] = mk(0, 0);
@@ -172,16 +177,16 @@ __global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(
             const PoleConst &P = sp[q];
             const cd al = mk(P.ar, P.ai), s2 = mk(P.s2r, P.s2i), s1c = mk(P.s1cr, P.s1ci);
             const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
-            const double kr = P.kr, ki = P.ki, ki2 = P.ki2;
+            const double kr = P.kr, ki = P.ki, ki2 = P.ki2, hn = P.ai;
 #pragma unroll
-            for (int j = 0; j < kMPT; ++j) {
+            for (int j = 0; j < MPT; ++j) {
                 // ---- solve 1: Helmholtz for eta1 (eq:lswEta)
-                cd num = cfma(al, e0[j], d0[j]);
-                num = cfms(s2, m0[j], num);
+                const cd t = mk(fma(-hn, e0[j].y, B0[j].x), fma(hn, e0[j].x, B0[j].y));
+                const cd num = cfms(s2, m0[j], t);
                 const double dr = kr + K2[j];
                 const double r = rcp_pos(fma(dr, dr, ki2));
-                // eta1 = num / (dr + i ki) = r * num * conj(den)
-                const cd eta1 = mk(r * fma(num.x, dr, num.y * ki), r * fma(num.y, dr, -num.x * ki));
+                const cd qd = mk(dr * r, -ki * r);                  // 1/(kappa + K2)
+                const cd eta1 = cmul(num, qd);
                 if (VARIANT == 0) {
                     const cd ia = mk(P.iar, P.iai);
                     const cd del1 = cfma(al, eta1, mk(-e0[j].x, -e0[j].y));
@@ -189,10 +194,10 @@ __global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(
                     // ---- solve 2
                     cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
                     num2 = cjfms(s2, zet1, num2);                      // - conj(c/alpha) zeta1
-                    const cd eta2 = mk(r * fma(num2.x, dr, -num2.y * ki), r * fma(num2.y, dr, num2.x * ki));
+                    const cd eta2 = cjfma(qd, num2, mk(0, 0));         // num2 * conj(q)
                     const cd del2 = cjfms(al, eta2, eta1);             // eta1 - conj(alpha) eta2
-                    const cd tz = mk(fma(-c, del2.x, zet1.x), fma(-c, del2.y, zet1.y));
-                    const cd zet2 = cmul(mk(ia.x, -ia.y), tz);
+                    const double ia2 = P.ia2;
+                    const cd zet2 = mk(fma(ia2, m0[j].x, c * eta2.x), fma(ia2, m0[j].y, c * eta2.y));
                     // ---- accumulate w1 g1 + w2 g2
                     A0[j] = cfma(w2, eta2, cfma(w1, eta1, A0[j]));
                     A1[j] = cfma(w2, del2, cfma(w1, del1, A1[j]));
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(
                     // ---- solve 2
                     cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
                     num2 = cjfms(s2, zet1, num2);
-                    const cd eta2 = mk(r * fma(num2.x, dr, -num2.y * ki), r * fma(num2.y, dr, num2.x * ki));
+                    const cd eta2 = cjfma(qd, num2, mk(0, 0));
                     // p' = u1 - i kx eta2, q' = v1 - i ky eta2
                     const cd p2 = mk(fma(kx, eta2.y, u1.x), fma(-kx, eta2.x, u1.y));
                     const cd q2 = mk(fma(ky, eta2.y, v1.x), fma(-ky, eta2.x, v1.y));
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(kPoleBlock, VARIANT == 0 ? 4 : 3) pole_kernel(
     }
     cd *out = a.partial + (size_t)chunk * 3 * n_modes;
 #pragma unroll
-    for (int j = 0; j < kMPT; ++j) {
+    for (int j = 0; j < MPT; ++j) {
         const long m = tile0 + j * kPoleBlock + threadIdx.x;
         if (m < n_modes) {
             out[m] = A0[j];
@@ -368,19 +373,40 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     return cudaGetLastError();
 }
 
-int pole_modes_per_block() { return kPoleBlock * kMPT; }
-
-cudaError_t pole_occupancy(int variant, int *blocks_per_sm) {
-    if (variant == 0)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel<0>, kPoleBlock, 0);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel<1>, kPoleBlock, 0);
+template <int V, int MPT>
+static cudaError_t occ_one(int *b) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, pole_kernel<V, MPT>, kPoleBlock, 0);
 }
 
-cudaError_t launch_poles(const PoleArgs &a, int variant, cudaStream_t st) {
-    const long tiles = (a.n_modes + kPoleBlock * kMPT - 1) / (kPoleBlock * kMPT);
+int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
+
+bool pole_mpt_supported(int mpt) { return mpt == 1 || mpt == 2 || mpt == 4; }
+
+cudaError_t pole_occupancy(int variant, int mpt, int *blocks_per_sm) {
+    switch (variant * 8 + mpt) {
+        case 1: return occ_one<0, 1>(blocks_per_sm);
+        case 2: return occ_one<0, 2>(blocks_per_sm);
+        case 4: return occ_one<0, 4>(blocks_per_sm);
+        case 9: return occ_one<1, 1>(blocks_per_sm);
+        case 10: return occ_one<1, 2>(blocks_per_sm);
+        case 12: return occ_one<1, 4>(blocks_per_sm);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, cudaStream_t st) {
+    const long mpb = kPoleBlock * mpt;
+    const long tiles = (a.n_modes + mpb - 1) / mpb;
     dim3 grid((unsigned)tiles, (unsigned)a.n_chunks);
-    if (variant == 0) pole_kernel<0><<<grid, kPoleBlock, 0, st>>>(a);
-    else pole_kernel<1><<<grid, kPoleBlock, 0, st>>>(a);
+    switch (variant * 8 + mpt) {
+        case 1: pole_kernel<0, 1><<<grid, kPoleBlock, 0, st>>>(a); break;
+        case 2: pole_kernel<0, 2><<<grid, kPoleBlock, 0, st>>>(a); break;
+        case 4: pole_kernel<0, 4><<<grid, kPoleBlock, 0, st>>>(a); break;
+        case 9: pole_kernel<1, 1><<<grid, kPoleBlock, 0, st>>>(a); break;
+        case 10: pole_kernel<1, 2><<<grid, kPoleBlock, 0, st>>>(a); break;
+        case 12: pole_kernel<1, 4><<<grid, kPoleBlock, 0, st>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

@@ -57,6 +57,7 @@ struct PoleArgs {
     int n_chunks;
     int D, log2D;
     double tau;            // c (tau-scaled Coriolis)
+    double hmu;            // Re(alpha_n) = h mu (same for every pole)
 };
 
 struct FinishArgs {

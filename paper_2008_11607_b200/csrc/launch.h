@@ -12,16 +12,17 @@ cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool re
                             const cd *tw, int D, int inverse, double scale, cudaStream_t st);
 cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const cd *tw, int D,
                             int inverse, double scale, cudaStream_t st);
-int pole_modes_per_block();
-cudaError_t pole_occupancy(int variant, int *blocks_per_sm);
-cudaError_t launch_poles(const PoleArgs &a, int variant, cudaStream_t st);
+int pole_modes_per_block(int mpt);
+bool pole_mpt_supported(int mpt);
+cudaError_t pole_occupancy(int variant, int mpt, int *blocks_per_sm);
+cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:
 // flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each).
 // DESIGN.md "Pole kernel" lists the count line by line.
-constexpr double kFlopsDZ = 141.0, kOpsDZ = 77.0;
-constexpr double kFlopsUV = 194.0, kOpsUV = 106.0;
+constexpr double kFlopsDZ = 131.0, kOpsDZ = 71.0;
+constexpr double kFlopsUV = 186.0, kOpsUV = 102.0;
 
 }  // namespace rexi

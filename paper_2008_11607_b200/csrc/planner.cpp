@@ -159,7 +159,7 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         q.w2r = (double)w2.real();    q.w2i = (double)w2.imag();
         q.s3r = (double)s3.real();    q.s3i = (double)s3.imag();
         q.s4r = (double)s4.real();    q.s4i = (double)s4.imag();
-        q.pad = 0.0;
+        q.ia2 = (double)std::norm(ia);
     }
 
     // Fourier symbols: index j -> wavenumber k = j (j < D/2) else j - D; 2 pi k tau;

@@ -22,7 +22,7 @@ struct alignas(16) PoleConst {
     double w2r, w2i;    // Gamma_n (C1_n - C2_n alpha_{-n})
     double s3r, s3i;    // alpha / kappa   (eq:lswVelocities, UV variant)
     double s4r, s4i;    // c / kappa
-    double pad;
+    double ia2;         // |1/alpha|^2
 };
 static_assert(sizeof(PoleConst) == 160, "PoleConst layout");
 

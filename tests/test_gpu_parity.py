@@ -276,3 +276,21 @@ def test_timing_counters(R):
         p.apply(*f)
     ms, pl, tl = p.timing_read()
     assert pl == 3 and ms > 0.0 and tl == 3 * 7
+
+
+@pytest.mark.parametrize("variant", ["dz", "uv"])
+@pytest.mark.parametrize("mpt", [1, 2, 4])
+def test_pole_kernel_tunings(R, variant, mpt):
+    """Every modes-per-thread instantiation gives the same result (ragged tail: D = 32 has
+    1024 modes = 2 tiles of 512 at mpt 4; D = 8 has one partial tile)."""
+    for D in (8, 32):
+        p = R.Plan(D, 1.3, variant=variant)
+        p.set_tuning(mpt)
+        F = inputs.spectral_white(D, seed=9)
+        acc = host(p.poles(dev(F)))
+        n, al, c1, c2, gm = oracle_terms(p).half()
+        ml, mk = lrsw.all_modes(D)
+        fm = np.stack([F[c][ml, mk] for c in range(3)], axis=-1)
+        ref = lrsw.rexii_pole_sum(D, 1.3, fm, ml, mk, al, c1, c2, gm)
+        got = np.stack([acc[c][ml, mk] for c in range(3)], axis=-1)
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < TOL

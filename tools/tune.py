@@ -1,0 +1,40 @@
+"""Time the pole kernel for each (variant, modes-per-thread) on a config (GPU box)."""
+import json
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+
+from paper_2008_11607_b200 import inputs, rexi
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+D, tau, tol = {"c1": (64, 0.02, 1e-12), "c2": (512, 1.0, 1e-8), "c3": (1024, 0.1, 1e-12),
+               "c4": (4096, 1.0, 1e-12)}[cfg]
+f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
+res = []
+for variant in ("dz", "uv"):
+    for mpt in (1, 2, 4):
+        p = rexi.Plan(D, tau, tol=tol, variant=variant)
+        p.set_tuning(mpt)
+        F = p.forward(*f)
+        acc = p.poles(F)
+        torch.cuda.synchronize()
+        p.timing_enable(True)
+        p.timing_read()
+        reps = 20 if D <= 1024 else 2
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(reps):
+            p.poles(F, acc=acc)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms, pl, tl = p.timing_read()
+        info = p.info
+        units = info["n_poles"] * D * D
+        k_ms = ms / pl
+        res.append({"variant": variant, "mpt": mpt, "pole_kernel_ms": k_ms,
+                    "poles_call_ms": ev0.elapsed_time(ev1) / reps,
+                    "pgp_per_s": units / (k_ms / 1e3),
+                    "fp64_pipe_frac": info["fp64_ops_per_pole_mode"] * units / (k_ms / 1e3) / (148 * 64 * 1.965e9)})
+        print(json.dumps(res[-1]), flush=True)

@@ -109,9 +109,10 @@ rexi_status_t rexi_plan_info(rexi_plan_t plan, rexi_plan_info_t *info);
 /* Select the pole-kernel formulation (rexi_variant_t). EINVAL for unknown values. */
 rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
 
-/* Pole-kernel tuning: Fourier modes per thread (1, 2 or 4; default 2). Results are identical
- * up to rounding order; only the speed changes. EINVAL for unsupported values. */
-rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread);
+/* Pole-kernel tuning: Fourier modes per thread and poles per loop trip; supported pairs
+ * (1,1) (1,2) (1,4) (2,1) (2,2) (4,1); default (2,1). Results are bit-identical across
+ * tunings (same per-mode operation order); only the speed changes. EINVAL otherwise. */
+rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter);
 
 /* Copy the plan's term table to HOST arrays of n_poles entries each (any may be NULL):
  *   alpha[2n], C1[2n], C2[2n] (interleaved re, im) and gamma[n], for n = 0..N:

@@ -54,6 +54,8 @@ struct rexi_plan_s {
     int device = 0;
     int variant = REXI_VARIANT_DZ;
     int mpt = 2;            // Fourier modes per thread in the pole kernel
+    int pu = 1;             // poles per loop trip in the pole kernel
+    int occ_cache[2][8][8] = {};  // resident blocks per SM, by (variant, mpt, pu); 0 = unknown
     long n_modes = 0;
     int num_sms = 0;
     int max_chunks = 1;
@@ -96,8 +98,8 @@ int choose_chunks(const rexi_plan_s *p, long n_range) {
     if (n_range <= 0) return 0;
     const long mpb = rexi::pole_modes_per_block(p->mpt);
     const long tiles = (p->n_modes + mpb - 1) / mpb;
-    int occ = 1;
-    if (rexi::pole_occupancy(p->variant, p->mpt, &occ) != cudaSuccess) occ = 1;
+    int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[p->variant][p->mpt][p->pu];
+    if (occ <= 0 && rexi::pole_occupancy(p->variant, p->mpt, p->pu, &occ) != cudaSuccess) occ = 1;
     const long conc = (long)p->num_sms * std::max(1, occ);
     const long max_c = std::max(1L, std::min<long>(p->max_chunks, n_range / 4));
     int best = 1;
@@ -178,7 +180,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    CK(rexi::launch_poles(a, p->variant, p->mpt, st));
+    CK(rexi::launch_poles(a, p->variant, p->mpt, p->pu, st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     rexi::FinishArgs f;
@@ -351,10 +353,12 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     return REXI_OK;
 }
 
-rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread) {
+rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int poles_per_iter) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (!rexi::pole_mpt_supported(modes_per_thread)) return fail(REXI_EINVAL, "modes_per_thread must be 1, 2 or 4");
+    if (!rexi::pole_config_supported(modes_per_thread, poles_per_iter))
+        return fail(REXI_EINVAL, "unsupported (modes_per_thread, poles_per_iter)");
     p->mpt = modes_per_thread;
+    p->pu = poles_per_iter;
     return REXI_OK;
 }
 

@@ -124,8 +124,79 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftArgs a) {
 constexpr int kPoleBlock = 128;
 constexpr int kPoleTile = 32;
 
-template <int VARIANT, int MPT>
-__global__ void __launch_bounds__(kPoleBlock, (VARIANT == 0 ? 8 : 6) / MPT)
+struct ModeState {
+    cd e0, B0, m0, ua, vb;   // f0 = (e0, ua, vb); B0 = h mu e0 + delta0; m0 = zeta0 - c e0
+    double K2, Kx, Ky;
+    cd A0, A1, A2;           // accumulators: (eta, delta, zeta) [DZ] or (eta, u, v) [UV]
+};
+
+// One pole, one mode: both shifted solves and the weighted accumulation.
+template <int VARIANT>
+__device__ __forceinline__ void pole_body(const PoleConst &P, ModeState &s, const double c) {
+    const cd al = mk(P.ar, P.ai), s2 = mk(P.s2r, P.s2i), s1c = mk(P.s1cr, P.s1ci);
+    const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
+    const double hn = P.ai;
+    // ---- solve 1: Helmholtz for eta1 (eq:lswEta)
+    const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));
+    const cd num = cfms(s2, s.m0, t);
+    const double dr = P.kr + s.K2;
+    const double r = rcp_pos(fma(dr, dr, P.ki2));
+    const cd qd = mk(dr * r, -P.ki * r);                        // 1/(kappa + K2)
+    const cd eta1 = cmul(num, qd);
+    if (VARIANT == 0) {
+        const cd ia = mk(P.iar, P.iai);
+        const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
+        const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
+        // ---- solve 2
+        cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
+        num2 = cjfms(s2, zet1, num2);                            // - conj(c/alpha) zeta1
+        const cd eta2 = cjfma(qd, num2, mk(0, 0));               // num2 * conj(q)
+        const cd del2 = cjfms(al, eta2, eta1);                   // eta1 - conj(alpha) eta2
+        const cd zet2 = mk(fma(P.ia2, s.m0.x, c * eta2.x), fma(P.ia2, s.m0.y, c * eta2.y));
+        // ---- accumulate w1 g1 + w2 g2
+        s.A0 = cfma(w2, eta2, cfma(w1, eta1, s.A0));
+        s.A1 = cfma(w2, del2, cfma(w1, del1, s.A1));
+        s.A2 = cfma(w2, zet2, cfma(w1, zet1, s.A2));
+    } else {
+        const cd s3 = mk(P.s3r, P.s3i), s4 = mk(P.s4r, P.s4i);
+        const double kx = s.Kx, ky = s.Ky;
+        // eq:lswVelocities: (u1, v1) = (s3 p - s4 q, s4 p + s3 q)
+        const cd p = mk(fma(-kx, eta1.y, s.ua.x), fma(kx, eta1.x, s.ua.y));
+        const cd qq = mk(fma(-ky, eta1.y, s.vb.x), fma(ky, eta1.x, s.vb.y));
+        const cd u1 = cfms(s4, qq, cmul(s3, p));
+        const cd v1 = cfma(s3, qq, cmul(s4, p));
+        // delta1 = i(kx u1 + ky v1), zeta1 = i(kx v1 - ky u1)
+        const cd sd = mk(fma(kx, u1.x, ky * v1.x), fma(kx, u1.y, ky * v1.y));
+        const cd sz = mk(fma(kx, v1.x, -ky * u1.x), fma(kx, v1.y, -ky * u1.y));
+        const cd del1 = mk(-sd.y, sd.x), zet1 = mk(-sz.y, sz.x);
+        // ---- solve 2
+        cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
+        num2 = cjfms(s2, zet1, num2);
+        const cd eta2 = cjfma(qd, num2, mk(0, 0));
+        // p' = u1 - i kx eta2, q' = v1 - i ky eta2
+        const cd p2 = mk(fma(kx, eta2.y, u1.x), fma(-kx, eta2.x, u1.y));
+        const cd q2 = mk(fma(ky, eta2.y, v1.x), fma(-ky, eta2.x, v1.y));
+        // (u2, v2) = (conj(s3) p' + conj(s4) q', -conj(s4) p' + conj(s3) q')
+        const cd u2 = cjfma(s4, q2, cjfma(s3, p2, mk(0, 0)));
+        const cd v2 = cjfms(s4, p2, cjfma(s3, q2, mk(0, 0)));
+        s.A0 = cfma(w2, eta2, cfma(w1, eta1, s.A0));
+        s.A1 = cfma(w2, u2, cfma(w1, u1, s.A1));
+        s.A2 = cfma(w2, v2, cfma(w1, v1, s.A2));
+    }
+}
+
+// Resident blocks per SM requested from ptxas (register budget 65536 / (128 * blocks)).
+template <int VARIANT, int MPT, int PU>
+struct PoleBounds {
+    static constexpr int work = MPT * PU;
+    static constexpr int value = VARIANT == 0 ? (work == 1 ? 8 : work == 2 ? (MPT == 2 ? 4 : 5) : 2)
+                                              : (work == 1 ? 6 : work == 2 ? 3 : 2);
+};
+
+// grid = (mode tiles of kPoleBlock * MPT modes, pole chunks). Each thread owns MPT modes and
+// runs every pole of its chunk, PU poles per loop trip (independent work for the scheduler).
+template <int VARIANT, int MPT, int PU>
+__global__ void __launch_bounds__(kPoleBlock, PoleBounds<VARIANT, MPT, PU>::value)
 pole_kernel(PoleArgs a) {
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
@@ -137,9 +208,7 @@ pole_kernel(PoleArgs a) {
     const double c = a.tau;
     const double hmu = a.hmu;
 
-    cd e0[MPT], B0[MPT], m0[MPT], ua[MPT], vb[MPT];
-    double K2[MPT], Kx[MPT], Ky[MPT];
-    cd A0[MPT], A1[MPT], A2[MPT];
+    ModeState st[MPT];
 #pragma unroll
     for (int j = 0; j < MPT; ++j) {
         const long m = tile0 + j * kPoleBlock + threadIdx.x;
@@ -147,20 +216,21 @@ pole_kernel(PoleArgs a) {
         const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
         const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
         const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
-        e0[j] = e;
-        ua[j] = uu;
-        vb[j] = vv;
-        Kx[j] = kx;
-        Ky[j] = ky;
+        ModeState &s = st[j];
+        s.e0 = e;
+        s.ua = uu;
+        s.vb = vv;
+        s.Kx = kx;
+        s.Ky = ky;
         // delta0 = i (kx u + ky v) ; zeta0 = i (kx v - ky u)
         const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
         const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
-        B0[j] = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
-        m0[j] = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
-        K2[j] = fma(kx, kx, ky * ky);
-        A0[j] = mk(0, 0);
-        A1[j] = mk(0, 0);
-        A2[j] = mk(0, 0);
+        s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+        s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+        s.K2 = fma(kx, kx, ky * ky);
+        s.A0 = mk(0, 0);
+        s.A1 = mk(0, 0);
+        s.A2 = mk(0, 0);
     }
 
     for (long pt = p0; pt < p1; pt += kPoleTile) {
@@ -172,63 +242,19 @@ pole_kernel(PoleArgs a) {
             for (int i = threadIdx.x; i < cnt * 10; i += kPoleBlock) dst[i] = src[i];
         }
         __syncthreads();
+        int q = 0;
 #pragma unroll 1
-        for (int q = 0; q < cnt; ++q) {
-            const PoleConst &P = sp[q];
-            const cd al = mk(P.ar, P.ai), s2 = mk(P.s2r, P.s2i), s1c = mk(P.s1cr, P.s1ci);
-            const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
-            const double kr = P.kr, ki = P.ki, ki2 = P.ki2, hn = P.ai;
+        for (; q + PU <= cnt; q += PU) {
 #pragma unroll
-            for (int j = 0; j < MPT; ++j) {
-                // ---- solve 1: Helmholtz for eta1 (eq:lswEta)
-                const cd t = mk(fma(-hn, e0[j].y, B0[j].x), fma(hn, e0[j].x, B0[j].y));
-                const cd num = cfms(s2, m0[j], t);
-                const double dr = kr + K2[j];
-                const double r = rcp_pos(fma(dr, dr, ki2));
-                const cd qd = mk(dr * r, -ki * r);                  // 1/(kappa + K2)
-                const cd eta1 = cmul(num, qd);
-                if (VARIANT == 0) {
-                    const cd ia = mk(P.iar, P.iai);
-                    const cd del1 = cfma(al, eta1, mk(-e0[j].x, -e0[j].y));
-                    const cd zet1 = cfma(ia, m0[j], mk(c * eta1.x, c * eta1.y));
-                    // ---- solve 2
-                    cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
-                    num2 = cjfms(s2, zet1, num2);                      // - conj(c/alpha) zeta1
-                    const cd eta2 = cjfma(qd, num2, mk(0, 0));         // num2 * conj(q)
-                    const cd del2 = cjfms(al, eta2, eta1);             // eta1 - conj(alpha) eta2
-                    const double ia2 = P.ia2;
-                    const cd zet2 = mk(fma(ia2, m0[j].x, c * eta2.x), fma(ia2, m0[j].y, c * eta2.y));
-                    // ---- accumulate w1 g1 + w2 g2
-                    A0[j] = cfma(w2, eta2, cfma(w1, eta1, A0[j]));
-                    A1[j] = cfma(w2, del2, cfma(w1, del1, A1[j]));
-                    A2[j] = cfma(w2, zet2, cfma(w1, zet1, A2[j]));
-                } else {
-                    const cd s3 = mk(P.s3r, P.s3i), s4 = mk(P.s4r, P.s4i);
-                    const double kx = Kx[j], ky = Ky[j];
-                    // eq:lswVelocities: (u1, v1) = (s3 p - s4 q, s4 p + s3 q)
-                    const cd p = mk(fma(-kx, eta1.y, ua[j].x), fma(kx, eta1.x, ua[j].y));
-                    const cd qq = mk(fma(-ky, eta1.y, vb[j].x), fma(ky, eta1.x, vb[j].y));
-                    const cd u1 = cfms(s4, qq, cmul(s3, p));
-                    const cd v1 = cfma(s3, qq, cmul(s4, p));
-                    // delta1 = i(kx u1 + ky v1), zeta1 = i(kx v1 - ky u1)
-                    const cd sd = mk(fma(kx, u1.x, ky * v1.x), fma(kx, u1.y, ky * v1.y));
-                    const cd sz = mk(fma(kx, v1.x, -ky * u1.x), fma(kx, v1.y, -ky * u1.y));
-                    const cd del1 = mk(-sd.y, sd.x), zet1 = mk(-sz.y, sz.x);
-                    // ---- solve 2
-                    cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
-                    num2 = cjfms(s2, zet1, num2);
-                    const cd eta2 = cjfma(qd, num2, mk(0, 0));
-                    // p' = u1 - i kx eta2, q' = v1 - i ky eta2
-                    const cd p2 = mk(fma(kx, eta2.y, u1.x), fma(-kx, eta2.x, u1.y));
-                    const cd q2 = mk(fma(ky, eta2.y, v1.x), fma(-ky, eta2.x, v1.y));
-                    // (u2, v2) = (conj(s3) p' + conj(s4) q', -conj(s4) p' + conj(s3) q')
-                    const cd u2 = cjfma(s4, q2, cjfma(s3, p2, mk(0, 0)));
-                    const cd v2 = cjfms(s4, p2, cjfma(s3, q2, mk(0, 0)));
-                    A0[j] = cfma(w2, eta2, cfma(w1, eta1, A0[j]));
-                    A1[j] = cfma(w2, u2, cfma(w1, u1, A1[j]));
-                    A2[j] = cfma(w2, v2, cfma(w1, v1, A2[j]));
-                }
-            }
+            for (int u = 0; u < PU; ++u)
+#pragma unroll
+                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(sp[q + u], st[j], c);
+        }
+        if (PU > 1) {
+#pragma unroll 1
+            for (; q < cnt; ++q)
+#pragma unroll
+                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(sp[q], st[j], c);
         }
     }
     cd *out = a.partial + (size_t)chunk * 3 * n_modes;
@@ -236,9 +262,9 @@ pole_kernel(PoleArgs a) {
     for (int j = 0; j < MPT; ++j) {
         const long m = tile0 + j * kPoleBlock + threadIdx.x;
         if (m < n_modes) {
-            out[m] = A0[j];
-            out[n_modes + m] = A1[j];
-            out[2 * n_modes + m] = A2[j];
+            out[m] = st[j].A0;
+            out[n_modes + m] = st[j].A1;
+            out[2 * n_modes + m] = st[j].A2;
         }
     }
 }
@@ -373,41 +399,42 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     return cudaGetLastError();
 }
 
-template <int V, int MPT>
-static cudaError_t occ_one(int *b) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, pole_kernel<V, MPT>, kPoleBlock, 0);
-}
+// Supported (modes per thread, poles per loop trip) instantiations.
+#define REXI_POLE_CONFIGS(X) \
+    X(0, 1, 1) X(0, 1, 2) X(0, 2, 1) X(0, 2, 2) X(0, 4, 1) X(0, 1, 4) \
+    X(1, 1, 1) X(1, 1, 2) X(1, 2, 1) X(1, 2, 2) X(1, 4, 1) X(1, 1, 4)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 
-bool pole_mpt_supported(int mpt) { return mpt == 1 || mpt == 2 || mpt == 4; }
+bool pole_config_supported(int mpt, int pu) {
+#define X(V, M, U) if (V == 0 && mpt == M && pu == U) return true;
+    REXI_POLE_CONFIGS(X)
+#undef X
+    return false;
+}
 
-cudaError_t pole_occupancy(int variant, int mpt, int *blocks_per_sm) {
-    switch (variant * 8 + mpt) {
-        case 1: return occ_one<0, 1>(blocks_per_sm);
-        case 2: return occ_one<0, 2>(blocks_per_sm);
-        case 4: return occ_one<0, 4>(blocks_per_sm);
-        case 9: return occ_one<1, 1>(blocks_per_sm);
-        case 10: return occ_one<1, 2>(blocks_per_sm);
-        case 12: return occ_one<1, 4>(blocks_per_sm);
-    }
+cudaError_t pole_occupancy(int variant, int mpt, int pu, int *blocks_per_sm) {
+#define X(V, M, U)                                                                              \
+    if (variant == V && mpt == M && pu == U)                                                     \
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel<V, M, U>, \
+                                                             kPoleBlock, 0);
+    REXI_POLE_CONFIGS(X)
+#undef X
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, cudaStream_t st) {
+cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, cudaStream_t st) {
     const long mpb = kPoleBlock * mpt;
     const long tiles = (a.n_modes + mpb - 1) / mpb;
     dim3 grid((unsigned)tiles, (unsigned)a.n_chunks);
-    switch (variant * 8 + mpt) {
-        case 1: pole_kernel<0, 1><<<grid, kPoleBlock, 0, st>>>(a); break;
-        case 2: pole_kernel<0, 2><<<grid, kPoleBlock, 0, st>>>(a); break;
-        case 4: pole_kernel<0, 4><<<grid, kPoleBlock, 0, st>>>(a); break;
-        case 9: pole_kernel<1, 1><<<grid, kPoleBlock, 0, st>>>(a); break;
-        case 10: pole_kernel<1, 2><<<grid, kPoleBlock, 0, st>>>(a); break;
-        case 12: pole_kernel<1, 4><<<grid, kPoleBlock, 0, st>>>(a); break;
-        default: return cudaErrorInvalidValue;
+#define X(V, M, U)                                                   \
+    if (variant == V && mpt == M && pu == U) {                       \
+        pole_kernel<V, M, U><<<grid, kPoleBlock, 0, st>>>(a);        \
+        return cudaGetLastError();                                   \
     }
-    return cudaGetLastError();
+    REXI_POLE_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st) {

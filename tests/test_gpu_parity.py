@@ -279,13 +279,13 @@ def test_timing_counters(R):
 
 
 @pytest.mark.parametrize("variant", ["dz", "uv"])
-@pytest.mark.parametrize("mpt", [1, 2, 4])
-def test_pole_kernel_tunings(R, variant, mpt):
+@pytest.mark.parametrize("mpt,pu", [(1, 1), (1, 2), (1, 4), (2, 1), (2, 2), (4, 1)])
+def test_pole_kernel_tunings(R, variant, mpt, pu):
     """Every modes-per-thread instantiation gives the same result (ragged tail: D = 32 has
     1024 modes = 2 tiles of 512 at mpt 4; D = 8 has one partial tile)."""
     for D in (8, 32):
         p = R.Plan(D, 1.3, variant=variant)
-        p.set_tuning(mpt)
+        p.set_tuning(mpt, pu)
         F = inputs.spectral_white(D, seed=9)
         acc = host(p.poles(dev(F)))
         n, al, c1, c2, gm = oracle_terms(p).half()

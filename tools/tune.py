@@ -14,9 +14,9 @@ D, tau, tol = {"c1": (64, 0.02, 1e-12), "c2": (512, 1.0, 1e-8), "c3": (1024, 0.1
 f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
 res = []
 for variant in ("dz", "uv"):
-    for mpt in (1, 2, 4):
+    for mpt, pu in ((1, 1), (1, 2), (1, 4), (2, 1), (2, 2), (4, 1)):
         p = rexi.Plan(D, tau, tol=tol, variant=variant)
-        p.set_tuning(mpt)
+        p.set_tuning(mpt, pu)
         F = p.forward(*f)
         acc = p.poles(F)
         torch.cuda.synchronize()
@@ -33,7 +33,7 @@ for variant in ("dz", "uv"):
         info = p.info
         units = info["n_poles"] * D * D
         k_ms = ms / pl
-        res.append({"variant": variant, "mpt": mpt, "pole_kernel_ms": k_ms,
+        res.append({"variant": variant, "mpt": mpt, "pu": pu, "pole_kernel_ms": k_ms,
                     "poles_call_ms": ev0.elapsed_time(ev1) / reps,
                     "pgp_per_s": units / (k_ms / 1e3),
                     "fp64_pipe_frac": info["fp64_ops_per_pole_mode"] * units / (k_ms / 1e3) / (148 * 64 * 1.965e9)})

@@ -109,10 +109,14 @@ rexi_status_t rexi_plan_info(rexi_plan_t plan, rexi_plan_info_t *info);
 /* Select the pole-kernel formulation (rexi_variant_t). EINVAL for unknown values. */
 rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
 
-/* Pole-kernel tuning: Fourier modes per thread and poles per loop trip; supported pairs
- * (1,1) (1,2) (1,4) (2,1) (2,2) (4,1); default (2,1). Results are bit-identical across
- * tunings (same per-mode operation order); only the speed changes. EINVAL otherwise. */
-rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter);
+/* Pole-kernel tuning for the plan's CURRENT variant: Fourier modes per thread, poles per loop
+ * trip and resident blocks per SM requested of the compiler (register budget). Supported:
+ *   DZ: (1,1,8) (2,1,4) (2,1,5) (2,2,3) (3,1,3) (3,1,4) (4,1,2) (4,1,3) (4,1,4)  default (4,1,4)
+ *   UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (2,1,4)
+ * Results are bit-identical across tunings (same per-mode operation order); only the speed
+ * changes. EINVAL otherwise. */
+rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter,
+                                   int min_blocks_per_sm);
 
 /* Copy the plan's term table to HOST arrays of n_poles entries each (any may be NULL):
  *   alpha[2n], C1[2n], C2[2n] (interleaved re, im) and gamma[n], for n = 0..N:

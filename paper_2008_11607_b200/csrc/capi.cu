@@ -53,9 +53,9 @@ struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
     int variant = REXI_VARIANT_DZ;
-    int mpt = 2;            // Fourier modes per thread in the pole kernel
-    int pu = 1;             // poles per loop trip in the pole kernel
-    int occ_cache[2][8][8] = {};  // resident blocks per SM, by (variant, mpt, pu); 0 = unknown
+    // pole-kernel tuning per variant: modes per thread, poles per loop trip, min blocks/SM
+    int mpt[2] = {4, 2}, pu[2] = {1, 1}, minb[2] = {4, 4};
+    int occ_cache[2] = {0, 0};    // resident blocks per SM of the current tuning; 0 = unknown
     long n_modes = 0;
     int num_sms = 0;
     int max_chunks = 1;
@@ -96,10 +96,11 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range) {
     if (n_range <= 0) return 0;
-    const long mpb = rexi::pole_modes_per_block(p->mpt);
+    const int v = p->variant;
+    const long mpb = rexi::pole_modes_per_block(p->mpt[v]);
     const long tiles = (p->n_modes + mpb - 1) / mpb;
-    int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[p->variant][p->mpt][p->pu];
-    if (occ <= 0 && rexi::pole_occupancy(p->variant, p->mpt, p->pu, &occ) != cudaSuccess) occ = 1;
+    int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];
+    if (occ <= 0 && rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ) != cudaSuccess) occ = 1;
     const long conc = (long)p->num_sms * std::max(1, occ);
     const long max_c = std::max(1L, std::min<long>(p->max_chunks, n_range / 4));
     int best = 1;
@@ -180,7 +181,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    CK(rexi::launch_poles(a, p->variant, p->mpt, p->pu, st));
+    CK(rexi::launch_poles(a, p->variant, p->mpt[p->variant], p->pu[p->variant], p->minb[p->variant], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     rexi::FinishArgs f;
@@ -353,12 +354,16 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     return REXI_OK;
 }
 
-rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int poles_per_iter) {
+rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int poles_per_iter,
+                                   int min_blocks_per_sm) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (!rexi::pole_config_supported(modes_per_thread, poles_per_iter))
-        return fail(REXI_EINVAL, "unsupported (modes_per_thread, poles_per_iter)");
-    p->mpt = modes_per_thread;
-    p->pu = poles_per_iter;
+    const int v = p->variant;
+    if (!rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm))
+        return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
+    p->mpt[v] = modes_per_thread;
+    p->pu[v] = poles_per_iter;
+    p->minb[v] = min_blocks_per_sm;
+    p->occ_cache[v] = 0;
     return REXI_OK;
 }
 

@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftArgs a) {
 // UV variant (paper-literal eq:lswVelocities): (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (p,q),
 //   p = a + i Kx eta1, q = b + i Ky eta1; delta1, zeta1 from (u1, v1); likewise for g2.
 // fp64-pipe instructions per (pole, mode): DZ 71, UV 102 (launch.h).
-constexpr int kPoleBlock = 128;
+#ifndef REXI_POLE_BLOCK
+#define REXI_POLE_BLOCK 128
+#endif
+constexpr int kPoleBlock = REXI_POLE_BLOCK;
 constexpr int kPoleTile = 32;
 
 struct ModeState {
@@ -185,18 +188,11 @@ __device__ __forceinline__ void pole_body(const PoleConst &P, ModeState &s, cons
     }
 }
 
-// Resident blocks per SM requested from ptxas (register budget 65536 / (128 * blocks)).
-template <int VARIANT, int MPT, int PU>
-struct PoleBounds {
-    static constexpr int work = MPT * PU;
-    static constexpr int value = VARIANT == 0 ? (work == 1 ? 8 : work == 2 ? (MPT == 2 ? 4 : 5) : 2)
-                                              : (work == 1 ? 6 : work == 2 ? 3 : 2);
-};
-
 // grid = (mode tiles of kPoleBlock * MPT modes, pole chunks). Each thread owns MPT modes and
-// runs every pole of its chunk, PU poles per loop trip (independent work for the scheduler).
-template <int VARIANT, int MPT, int PU>
-__global__ void __launch_bounds__(kPoleBlock, PoleBounds<VARIANT, MPT, PU>::value)
+// runs every pole of its chunk, PU poles per loop trip. MINB = resident blocks per SM asked
+// of ptxas (register budget 65536 / (kPoleBlock * MINB) per thread).
+template <int VARIANT, int MPT, int PU, int MINB>
+__global__ void __launch_bounds__(kPoleBlock, MINB)
 pole_kernel(PoleArgs a) {
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
@@ -205,7 +201,10 @@ pole_kernel(PoleArgs a) {
     const long len = a.pole_end - a.pole_begin;
     const long p0 = a.pole_begin + len * chunk / a.n_chunks;
     const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
-    const double c = a.tau;
+    double c = a.tau;
+#if REXI_C_IN_REG
+    asm volatile("mov.b64 %0, %0;" : "+d"(c));   // keep c in a per-thread register
+#endif
     const double hmu = a.hmu;
 
     ModeState st[MPT];
@@ -245,10 +244,19 @@ pole_kernel(PoleArgs a) {
         int q = 0;
 #pragma unroll 1
         for (; q + PU <= cnt; q += PU) {
+#if REXI_ABLATE_LDS
+            // timing ablation only (wrong results): constants stay in registers
+            const PoleConst Pr = sp[0];
+#pragma unroll
+            for (int u = 0; u < PU; ++u)
+#pragma unroll
+                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(Pr, st[j], c);
+#else
 #pragma unroll
             for (int u = 0; u < PU; ++u)
 #pragma unroll
                 for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(sp[q + u], st[j], c);
+#endif
         }
         if (PU > 1) {
 #pragma unroll 1
@@ -399,38 +407,40 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     return cudaGetLastError();
 }
 
-// Supported (modes per thread, poles per loop trip) instantiations.
-#define REXI_POLE_CONFIGS(X) \
-    X(0, 1, 1) X(0, 1, 2) X(0, 2, 1) X(0, 2, 2) X(0, 4, 1) X(0, 1, 4) \
-    X(1, 1, 1) X(1, 1, 2) X(1, 2, 1) X(1, 2, 2) X(1, 4, 1) X(1, 1, 4)
+// Supported (variant, modes per thread, poles per loop trip, min blocks per SM) instantiations.
+#define REXI_POLE_CONFIGS(X)                                                             \
+    X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 2, 2, 3) X(0, 3, 1, 3) X(0, 3, 1, 4)  \
+    X(0, 4, 1, 2) X(0, 4, 1, 3) X(0, 4, 1, 4)                                             \
+    X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 
-bool pole_config_supported(int mpt, int pu) {
-#define X(V, M, U) if (V == 0 && mpt == M && pu == U) return true;
+bool pole_config_supported(int variant, int mpt, int pu, int minb) {
+#define X(V, M, U, B) if (variant == V && mpt == M && pu == U && minb == B) return true;
     REXI_POLE_CONFIGS(X)
 #undef X
     return false;
 }
 
-cudaError_t pole_occupancy(int variant, int mpt, int pu, int *blocks_per_sm) {
-#define X(V, M, U)                                                                              \
-    if (variant == V && mpt == M && pu == U)                                                     \
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel<V, M, U>, \
+cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_per_sm) {
+#define X(V, M, U, B)                                                                       \
+    if (variant == V && mpt == M && pu == U && minb == B)                                   \
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm,                  \
+                                                             pole_kernel<V, M, U, B>,        \
                                                              kPoleBlock, 0);
     REXI_POLE_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, cudaStream_t st) {
+cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st) {
     const long mpb = kPoleBlock * mpt;
     const long tiles = (a.n_modes + mpb - 1) / mpb;
     dim3 grid((unsigned)tiles, (unsigned)a.n_chunks);
-#define X(V, M, U)                                                   \
-    if (variant == V && mpt == M && pu == U) {                       \
-        pole_kernel<V, M, U><<<grid, kPoleBlock, 0, st>>>(a);        \
-        return cudaGetLastError();                                   \
+#define X(V, M, U, B)                                                   \
+    if (variant == V && mpt == M && pu == U && minb == B) {             \
+        pole_kernel<V, M, U, B><<<grid, kPoleBlock, 0, st>>>(a);        \
+        return cudaGetLastError();                                      \
     }
     REXI_POLE_CONFIGS(X)
 #undef X

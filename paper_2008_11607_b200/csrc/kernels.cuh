@@ -7,6 +7,10 @@
 
 #include "planner.h"
 
+#ifndef REXI_RCP_F32_SEED
+#define REXI_RCP_F32_SEED 0
+#endif
+
 namespace rexi {
 
 // ----------------------------------------------------------------------------- complex fp64
@@ -40,7 +44,16 @@ __device__ __forceinline__ cd cjfms(cd a, cd b, cd c) {
 // (relative error ~ e0^3 with e0 ~ 2^-20 seed error). Not correctly rounded; <= 1 ulp.
 __device__ __forceinline__ double rcp_pos(double d) {
     double r;
+#if REXI_ABLATE_RCP
+    r = d * 1.0e-3;   // timing ablation only (wrong results)
+#elif REXI_RCP_F32_SEED
+    // seed from the fp32 MUFU (XU pipe) instead of MUFU.RCP64H; |d| in fp32 range
+    float rf;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"(__double2float_rn(d)));
+    r = (double)rf;
+#else
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+#endif
     double e = fma(-d, r, 1.0);
     e = fma(e, e, e);
     return fma(e, r, r);

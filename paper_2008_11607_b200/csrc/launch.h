@@ -13,9 +13,9 @@ cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool re
 cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const cd *tw, int D,
                             int inverse, double scale, cudaStream_t st);
 int pole_modes_per_block(int mpt);
-bool pole_config_supported(int mpt, int pu);
-cudaError_t pole_occupancy(int variant, int mpt, int pu, int *blocks_per_sm);
-cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, cudaStream_t st);
+bool pole_config_supported(int variant, int mpt, int pu, int minb);
+cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_per_sm);
+cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 

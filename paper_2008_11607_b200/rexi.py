@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librexi.so")
+LIB_PATH = os.environ.get("REXI_LIB") or os.path.join(_HERE, "librexi.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_2008_11607_b200.build` "
@@ -44,7 +44,7 @@ EXPORTS = {
     "rexi_plan_destroy": (ctypes.c_int, [_vp]),
     "rexi_plan_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "rexi_plan_set_variant": (ctypes.c_int, [_vp, ctypes.c_int]),
-    "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
+    "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "rexi_poles": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp]),
@@ -169,9 +169,10 @@ class Plan:
         _check(_lib.rexi_plan_set_variant(self._h, v), "rexi_plan_set_variant")
         self.variant = v
 
-    def set_tuning(self, modes_per_thread, poles_per_iter=1):
-        _check(_lib.rexi_plan_set_tuning(self._h, int(modes_per_thread), int(poles_per_iter)),
-               "rexi_plan_set_tuning")
+    def set_tuning(self, modes_per_thread, poles_per_iter=1, min_blocks_per_sm=4):
+        """Tune the pole kernel of the current variant (see rexi_plan_set_tuning)."""
+        _check(_lib.rexi_plan_set_tuning(self._h, int(modes_per_thread), int(poles_per_iter),
+                                         int(min_blocks_per_sm)), "rexi_plan_set_tuning")
 
     def coeffs(self):
         n = self.n_poles

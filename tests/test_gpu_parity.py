@@ -278,19 +278,34 @@ def test_timing_counters(R):
     assert pl == 3 and ms > 0.0 and tl == 3 * 7
 
 
-@pytest.mark.parametrize("variant", ["dz", "uv"])
-@pytest.mark.parametrize("mpt,pu", [(1, 1), (1, 2), (1, 4), (2, 1), (2, 2), (4, 1)])
-def test_pole_kernel_tunings(R, variant, mpt, pu):
-    """Every modes-per-thread instantiation gives the same result (ragged tail: D = 32 has
-    1024 modes = 2 tiles of 512 at mpt 4; D = 8 has one partial tile)."""
+TUNINGS = [("dz", 1, 1, 8), ("dz", 2, 1, 4), ("dz", 2, 1, 5), ("dz", 2, 2, 3), ("dz", 3, 1, 3),
+           ("dz", 3, 1, 4), ("dz", 4, 1, 2), ("dz", 4, 1, 3), ("dz", 4, 1, 4),
+           ("uv", 1, 1, 6), ("uv", 2, 1, 3), ("uv", 2, 1, 4), ("uv", 3, 1, 3), ("uv", 4, 1, 2),
+           ("uv", 4, 1, 3)]
+
+
+@pytest.mark.parametrize("variant,mpt,pu,minb", TUNINGS)
+def test_pole_kernel_tunings(R, variant, mpt, pu, minb):
+    """Every pole-kernel instantiation gives the same result, bit for bit, and matches the
+    oracle (ragged tails: D = 32 has 1024 modes, not a multiple of 384 at mpt 3 or 512 at
+    mpt 4; D = 8 has one partial tile)."""
     for D in (8, 32):
         p = R.Plan(D, 1.3, variant=variant)
-        p.set_tuning(mpt, pu)
-        F = inputs.spectral_white(D, seed=9)
-        acc = host(p.poles(dev(F)))
+        F = dev(inputs.spectral_white(D, seed=9))
+        base = host(p.poles(F))
+        p.set_tuning(mpt, pu, minb)
+        acc = host(p.poles(F))
+        assert np.array_equal(acc, base)
         n, al, c1, c2, gm = oracle_terms(p).half()
         ml, mk = lrsw.all_modes(D)
-        fm = np.stack([F[c][ml, mk] for c in range(3)], axis=-1)
+        Fh = host(F)
+        fm = np.stack([Fh[c][ml, mk] for c in range(3)], axis=-1)
         ref = lrsw.rexii_pole_sum(D, 1.3, fm, ml, mk, al, c1, c2, gm)
         got = np.stack([acc[c][ml, mk] for c in range(3)], axis=-1)
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < TOL
+
+
+def test_tuning_rejects_unsupported(R):
+    p = R.Plan(16, 1.0)
+    with pytest.raises(R.RexiError):
+        p.set_tuning(3, 3, 3)

@@ -13,10 +13,13 @@ D, tau, tol = {"c1": (64, 0.02, 1e-12), "c2": (512, 1.0, 1e-8), "c3": (1024, 0.1
                "c4": (4096, 1.0, 1e-12)}[cfg]
 f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
 res = []
+TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (2, 2, 3), (3, 1, 3), (3, 1, 4), (4, 1, 2),
+                  (4, 1, 3), (4, 1, 4)],
+           "uv": [(1, 1, 6), (2, 1, 3), (2, 1, 4), (3, 1, 3), (4, 1, 2), (4, 1, 3)]}
 for variant in ("dz", "uv"):
-    for mpt, pu in ((1, 1), (1, 2), (1, 4), (2, 1), (2, 2), (4, 1)):
+    for mpt, pu, minb in TUNINGS[variant]:
         p = rexi.Plan(D, tau, tol=tol, variant=variant)
-        p.set_tuning(mpt, pu)
+        p.set_tuning(mpt, pu, minb)
         F = p.forward(*f)
         acc = p.poles(F)
         torch.cuda.synchronize()
@@ -33,7 +36,7 @@ for variant in ("dz", "uv"):
         info = p.info
         units = info["n_poles"] * D * D
         k_ms = ms / pl
-        res.append({"variant": variant, "mpt": mpt, "pu": pu, "pole_kernel_ms": k_ms,
+        res.append({"variant": variant, "mpt": mpt, "pu": pu, "minb": minb, "pole_kernel_ms": k_ms,
                     "poles_call_ms": ev0.elapsed_time(ev1) / reps,
                     "pgp_per_s": units / (k_ms / 1e3),
                     "fp64_pipe_frac": info["fp64_ops_per_pole_mode"] * units / (k_ms / 1e3) / (148 * 64 * 1.965e9)})

@@ -112,9 +112,10 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
 /* Pole-kernel tuning for the plan's CURRENT variant: Fourier modes per thread, poles per loop
  * trip and resident blocks per SM requested of the compiler (register budget). Supported:
  *   DZ: (1,1,8) (2,1,4) (2,1,5) (2,2,3) (3,1,3) (3,1,4) (4,1,2) (4,1,3) (4,1,4)  default (4,1,4)
- *   UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (2,1,4)
- * Results are bit-identical across tunings (same per-mode operation order); only the speed
- * changes. EINVAL otherwise. */
+ *   UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (3,1,3)
+ * Per pole and mode the operation order is the same for every tuning; the number of pole
+ * chunks (and so the order in which chunk partial sums are added) follows the tile count, so
+ * results agree to rounding, not bit for bit. EINVAL otherwise. */
 rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter,
                                    int min_blocks_per_sm);
 

@@ -54,7 +54,7 @@ struct rexi_plan_s {
     int device = 0;
     int variant = REXI_VARIANT_DZ;
     // pole-kernel tuning per variant: modes per thread, poles per loop trip, min blocks/SM
-    int mpt[2] = {4, 2}, pu[2] = {1, 1}, minb[2] = {4, 4};
+    int mpt[2] = {4, 3}, pu[2] = {1, 1}, minb[2] = {4, 3};
     int occ_cache[2] = {0, 0};    // resident blocks per SM of the current tuning; 0 = unknown
     long n_modes = 0;
     int num_sms = 0;

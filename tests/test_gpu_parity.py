@@ -286,8 +286,8 @@ TUNINGS = [("dz", 1, 1, 8), ("dz", 2, 1, 4), ("dz", 2, 1, 5), ("dz", 2, 2, 3), (
 
 @pytest.mark.parametrize("variant,mpt,pu,minb", TUNINGS)
 def test_pole_kernel_tunings(R, variant, mpt, pu, minb):
-    """Every pole-kernel instantiation gives the same result, bit for bit, and matches the
-    oracle (ragged tails: D = 32 has 1024 modes, not a multiple of 384 at mpt 3 or 512 at
+    """Every pole-kernel instantiation gives the same result up to the summation order of the
+    pole chunks (the chunk count follows the tile count) and matches the oracle (ragged tails: D = 32 has 1024 modes, not a multiple of 384 at mpt 3 or 512 at
     mpt 4; D = 8 has one partial tile)."""
     for D in (8, 32):
         p = R.Plan(D, 1.3, variant=variant)
@@ -295,7 +295,7 @@ def test_pole_kernel_tunings(R, variant, mpt, pu, minb):
         base = host(p.poles(F))
         p.set_tuning(mpt, pu, minb)
         acc = host(p.poles(F))
-        assert np.array_equal(acc, base)
+        assert np.linalg.norm(acc - base) <= 1e-14 * np.linalg.norm(base)
         n, al, c1, c2, gm = oracle_terms(p).half()
         ml, mk = lrsw.all_modes(D)
         Fh = host(F)

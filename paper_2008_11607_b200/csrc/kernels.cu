@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) fft_cols_kernel(FftArgs a) {
 //   acc(eta, delta, zeta) += w1 g1 + w2 g2;  (u, v) recovered per mode in finish_kernel.
 // UV variant (paper-literal eq:lswVelocities): (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (p,q),
 //   p = a + i Kx eta1, q = b + i Ky eta1; delta1, zeta1 from (u1, v1); likewise for g2.
-// fp64-pipe instructions per (pole, mode): DZ 71, UV 102 (launch.h).
+// fp64-pipe instructions per (pole, mode): DZ 71, UV 101 (launch.h).
 #ifndef REXI_POLE_BLOCK
 #define REXI_POLE_BLOCK 128
 #endif

@@ -23,6 +23,6 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 // flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each).
 // DESIGN.md "Pole kernel" lists the count line by line.
 constexpr double kFlopsDZ = 131.0, kOpsDZ = 71.0;
-constexpr double kFlopsUV = 186.0, kOpsUV = 102.0;
+constexpr double kFlopsUV = 183.0, kOpsUV = 101.0;
 
 }  // namespace rexi

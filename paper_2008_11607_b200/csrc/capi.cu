@@ -303,7 +303,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     auto alloc = [&](void **ptr, size_t bytes) -> cudaError_t { return cudaMalloc(ptr, bytes); };
     if ((e = alloc((void **)&p->d_poles, sizeof(rexi::PoleConst) * (size_t)p->host.n_poles)) ||
         (e = alloc((void **)&p->d_ksym, sizeof(double) * (size_t)D)) ||
-        (e = alloc((void **)&p->d_tw, sizeof(double) * (size_t)D)) ||
+        (e = alloc((void **)&p->d_tw, 2 * sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
         (e = alloc((void **)&p->d_tmp, field)) ||
         (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks))) {
@@ -314,7 +314,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     if ((e = cudaMemcpy(p->d_poles, p->host.poles.data(), sizeof(rexi::PoleConst) * (size_t)p->host.n_poles,
                         cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_ksym, p->host.ksym.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
+        (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), 2 * sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
         return cleanup_fail(cuda_fail(e, "cudaMemcpy"));
     *out = p;
     return REXI_OK;

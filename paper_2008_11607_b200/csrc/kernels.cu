@@ -16,89 +16,172 @@
 namespace rexi {
 
 // ============================================================================= FFT
-__device__ __forceinline__ int bitrev(int x, int log2n) {
-    return (int)(__brev((unsigned)x) >> (32 - log2n));
+// Batched complex FFT of length D (power of two) in shared memory: Stockham autosort passes of
+// radix 8 (then one radix-4 or radix-2 pass), each thread holding 8 values in registers per
+// pass, twiddles e^{-2 pi i j / D} from a host table (long double, rounded). A block owns `nb`
+// transforms (rows, or a strip of adjacent columns so global accesses stay coalesced); its
+// threads = nb * max(1, D/8). Forward: e^{-}; inverse: e^{+} (conjugated twiddles/butterflies).
+
+template <bool INV>
+__device__ __forceinline__ cd mul_mi(cd a) {  // a * (-i) forward, a * (+i) inverse
+    return INV ? mk(-a.y, a.x) : mk(a.y, -a.x);
+}
+__device__ __forceinline__ cd cadd(cd a, cd b) { return mk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cd csub(cd a, cd b) { return mk(a.x - b.x, a.y - b.y); }
+
+template <bool INV>
+__device__ __forceinline__ void dft2(cd *v) {
+    const cd a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
 }
 
-// In-place iterative radix-2 DIT on `nfft` arrays of length D stored at s + f*stride,
-// input already in bit-reversed order. Twiddle w_len^pos = tw[pos * D/len].
-__device__ __forceinline__ void fft_stages(cd *s, int stride, int D, int log2D, int nfft,
-                                           const cd *__restrict__ tw, int inverse) {
-    const int halfD = D >> 1;
-    const int nb = nfft * halfD;
-    for (int lh = 1; lh <= log2D; ++lh) {
-        const int half = 1 << (lh - 1);
-        const int tstride = D >> lh;
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-            const int f = b >> (log2D - 1);
-            const int bb = b & (halfD - 1);
-            const int grp = bb >> (lh - 1);
-            const int pos = bb & (half - 1);
-            const int i0 = f * stride + (grp << lh) + pos;
-            const int i1 = i0 + half;
-            const double2 tw2 = __ldg(reinterpret_cast<const double2 *>(tw) + pos * tstride);
-            cd w = mk(tw2.x, tw2.y);
-            if (inverse) w.y = -w.y;
-            const cd u = s[i0];
-            const cd t = cmul(s[i1], w);
-            s[i0] = mk(u.x + t.x, u.y + t.y);
-            s[i1] = mk(u.x - t.x, u.y - t.y);
-        }
-        __syncthreads();
+template <bool INV>
+__device__ __forceinline__ void dft4(cd *v) {
+    // DIF: (v0 + v2, v1 + v3) -> X0, X2 ; (v0 - v2, -i (v1 - v3)) -> X1, X3
+    const cd c0 = cadd(v[0], v[2]), c1 = cadd(v[1], v[3]);
+    const cd c2 = csub(v[0], v[2]), c3 = mul_mi<INV>(csub(v[1], v[3]));
+    v[0] = cadd(c0, c1);
+    v[2] = csub(c0, c1);
+    v[1] = cadd(c2, c3);
+    v[3] = csub(c2, c3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(cd *v) {
+    const double h = 0.70710678118654752440;  // cos(pi/4)
+    cd b[8];
+    for (int n = 0; n < 4; ++n) {
+        b[n] = cadd(v[n], v[n + 4]);
+        b[n + 4] = csub(v[n], v[n + 4]);
     }
+    // odd half twiddles w8^n, n = 1, 2, 3 (forward w8 = e^{-i pi/4})
+    {
+        const cd x = b[5];
+        b[5] = INV ? mk(h * (x.x - x.y), h * (x.x + x.y)) : mk(h * (x.x + x.y), h * (x.y - x.x));
+        b[6] = mul_mi<INV>(b[6]);
+        const cd y = b[7];
+        b[7] = INV ? mk(-h * (y.x + y.y), h * (y.x - y.y)) : mk(h * (y.y - y.x), -h * (y.x + y.y));
+    }
+    dft4<INV>(b);       // -> X0, X2, X4, X6 in b[0], b[1], b[2], b[3]
+    dft4<INV>(b + 4);   // -> X1, X3, X5, X7 in b[4..7]
+    v[0] = b[0]; v[2] = b[1]; v[4] = b[2]; v[6] = b[3];
+    v[1] = b[4]; v[3] = b[5]; v[5] = b[6]; v[7] = b[7];
 }
 
-// One block = `per_block` consecutive rows of one field. grid = (D/per_block, 3).
-template <bool REAL_IN, bool REAL_OUT>
-__global__ void __launch_bounds__(256) fft_rows_kernel(FftArgs a) {
-    extern __shared__ cd smem[];
-    const int f = blockIdx.y;
-    const int D = a.D, log2D = a.log2D, R = a.per_block;
-    const size_t row0 = (size_t)blockIdx.x * R;
-    const int n = R << log2D;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> log2D, x = i & (D - 1);
-        const size_t g = (row0 + r) * (size_t)D + x;
-        cd v;
-        if (REAL_IN) v = mk(static_cast<const double *>(a.in[f])[g], 0.0);
-        else v = static_cast<const cd *>(a.in[f])[g];
-        smem[(r << log2D) + bitrev(x, log2D)] = v;
+template <int R, bool INV>
+__device__ __forceinline__ void dftR(cd *v) {
+    if (R == 8) dft8<INV>(v);
+    else if (R == 4) dft4<INV>(v);
+    else dft2<INV>(v);
+}
+
+// One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
+// tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
+template <int R, bool INV>
+__device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, int t, int tf,
+                                              const cd *__restrict__ tw) {
+    constexpr int PERMAX = 8 / R;
+    const int nbf = N / R;
+    cd v[8];
+#pragma unroll
+    for (int b = 0; b < PERMAX; ++b) {
+        const int j = t + b * tf;
+        if (b * tf < nbf && j < nbf) {
+            const int k = j & (Ns - 1);
+            const int step = k * (N / (Ns * R));  // twiddle index step: r * k * N / (Ns R)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                cd x = s[j + r * nbf];
+                if (r > 0 && Ns > 1) {
+                    const double2 w2 = __ldg(reinterpret_cast<const double2 *>(tw) + ((r * step) & (N - 1)));
+                    const cd w = mk(w2.x, INV ? -w2.y : w2.y);
+                    x = cmul(x, w);
+                }
+                v[b * R + r] = x;
+            }
+        }
     }
     __syncthreads();
-    fft_stages(smem, D, D, log2D, R, a.twiddle, a.inverse);
+#pragma unroll
+    for (int b = 0; b < PERMAX; ++b) {
+        const int j = t + b * tf;
+        if (b * tf < nbf && j < nbf) {
+            dftR<R, INV>(v + b * R);
+            const int k = j & (Ns - 1);
+            const int d = (j - k) * R + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) s[d + r * Ns] = v[b * R + r];
+        }
+    }
+    __syncthreads();
+}
+
+template <bool INV>
+__device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw) {
+    int Ns = 1, rem = logN;
+    while (rem >= 3) {
+        stockham_pass<8, INV>(s, N, logN, Ns, t, tf, tw);
+        Ns <<= 3;
+        rem -= 3;
+    }
+    if (rem == 2) stockham_pass<4, INV>(s, N, logN, Ns, t, tf, tw);
+    else if (rem == 1) stockham_pass<2, INV>(s, N, logN, Ns, t, tf, tw);
+}
+
+// Row pass: block = nb consecutive rows of one field; threads = nb * tf, tf = max(1, D/8).
+template <bool INV, bool REAL_IN, bool REAL_OUT>
+__global__ void __launch_bounds__(1024) fft_rows_kernel(FftArgs a) {
+    extern __shared__ cd smem[];
+    const int f = blockIdx.y;
+    const int D = a.D, log2D = a.log2D, nb = a.per_block;
+    const int tf = D >= 8 ? D / 8 : 1;
+    const size_t row0 = (size_t)blockIdx.x * nb;
+    const int n = nb * D;
+    const void *inp = f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2];
+    void *outp = f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const size_t g = row0 * D + i;
+        smem[i] = REAL_IN ? mk(static_cast<const double *>(inp)[g], 0.0) : static_cast<const cd *>(inp)[g];
+    }
+    __syncthreads();
+    const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
+    fft_in_smem<INV>(smem + row * D, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> log2D, k = i & (D - 1);
-        const size_t g = (row0 + r) * (size_t)D + k;
+        const size_t g = row0 * D + i;
         const cd v = smem[i];
-        if (REAL_OUT) static_cast<double *>(a.out[f])[g] = v.x * sc;
-        else static_cast<cd *>(a.out[f])[g] = mk(v.x * sc, v.y * sc);
+        if (REAL_OUT) static_cast<double *>(outp)[g] = v.x * sc;
+        else static_cast<cd *>(outp)[g] = mk(v.x * sc, v.y * sc);
     }
 }
 
-// One block = `per_block` (power of two) consecutive columns of one field; smem rows
-// padded to D+1 to spread the transposed accesses over the banks.
-__global__ void __launch_bounds__(256) fft_cols_kernel(FftArgs a) {
+// Column pass: block = nb adjacent columns (a strip) of one field; smem column-major with the
+// column stride padded to D + 1.
+template <bool INV>
+__global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
     extern __shared__ cd smem[];
     const int f = blockIdx.y;
     const int D = a.D, log2D = a.log2D, C = a.per_block;
     const int logC = __ffs(C) - 1;
+    const int tf = D >= 8 ? D / 8 : 1;
     const int stride = D + 1;
     const size_t col0 = (size_t)blockIdx.x * C;
-    const cd *in = static_cast<const cd *>(a.in[f]);
-    cd *out = static_cast<cd *>(a.out[f]);
+    const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int n = C << log2D;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> logC, cc = i & (C - 1);
-        smem[cc * stride + bitrev(r, log2D)] = in[(size_t)r * D + col0 + cc];
+        const int r = i >> logC, c = i & (C - 1);
+        smem[c * stride + r] = in[(size_t)r * D + col0 + c];
     }
     __syncthreads();
-    fft_stages(smem, stride, D, log2D, C, a.twiddle, a.inverse);
+    const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
+    fft_in_smem<INV>(smem + col * stride, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> logC, cc = i & (C - 1);
-        const cd v = smem[cc * stride + r];
-        out[(size_t)r * D + col0 + cc] = mk(v.x * sc, v.y * sc);
+        const int r = i >> logC, c = i & (C - 1);
+        const cd v = smem[c * stride + r];
+        out[(size_t)r * D + col0 + c] = mk(v.x * sc, v.y * sc);
     }
 }
 
@@ -357,15 +440,35 @@ static int ilog2(int x) {
     return r;
 }
 
-static const int kFftElems = 4096;   // complex elements per FFT block (64 KB of smem)
+// FFT launch shapes: threads per transform tf = max(1, D/8); a block holds nb transforms with
+// nb * tf <= 256 threads (rows) or a strip of C columns with C * tf <= 1024 and C <= 8.
+static int fft_rows_per_block(int D) {
+    const int tf = D >= 8 ? D / 8 : 1;
+    int nb = 256 / tf;
+    if (nb < 1) nb = 1;
+    if (nb > D) nb = D;
+    return nb;
+}
+static int fft_cols_per_block(int D) {
+    const int tf = D >= 8 ? D / 8 : 1;
+    int C = 1024 / tf;
+    if (C > 8) C = 8;
+    if (C < 1) C = 1;
+    if (C > D) C = D;
+    return C;
+}
 
 cudaError_t fft_setup_attributes() {
     cudaError_t e;
     const int maxsm = 200 * 1024;
-    if ((e = cudaFuncSetAttribute(fft_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(fft_rows_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(fft_rows_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    if ((e = cudaFuncSetAttribute(fft_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+#define SETA(K) if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
+    SETA((fft_rows_kernel<false, true, false>))
+    SETA((fft_rows_kernel<true, false, true>))
+    SETA((fft_rows_kernel<false, false, false>))
+    SETA((fft_rows_kernel<true, false, false>))
+    SETA(fft_cols_kernel<false>)
+    SETA(fft_cols_kernel<true>)
+#undef SETA
     return cudaSuccess;
 }
 
@@ -376,15 +479,18 @@ cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool re
     a.twiddle = tw;
     a.D = D;
     a.log2D = ilog2(D);
-    a.per_block = D >= kFftElems ? 1 : kFftElems / D;
-    if (a.per_block > D) a.per_block = D;
+    a.per_block = fft_rows_per_block(D);
     a.inverse = inverse;
     a.scale = scale;
+    const int tf = D >= 8 ? D / 8 : 1;
     dim3 grid(D / a.per_block, 3);
-    size_t sm = (size_t)a.per_block * D * sizeof(cd);
-    if (real_in && !real_out) fft_rows_kernel<true, false><<<grid, 256, sm, st>>>(a);
-    else if (!real_in && real_out) fft_rows_kernel<false, true><<<grid, 256, sm, st>>>(a);
-    else fft_rows_kernel<false, false><<<grid, 256, sm, st>>>(a);
+    const int threads = a.per_block * tf;
+    const size_t sm = (size_t)a.per_block * D * sizeof(cd);
+    if (!inverse && real_in && !real_out) fft_rows_kernel<false, true, false><<<grid, threads, sm, st>>>(a);
+    else if (inverse && !real_in && real_out) fft_rows_kernel<true, false, true><<<grid, threads, sm, st>>>(a);
+    else if (!inverse && !real_in && !real_out) fft_rows_kernel<false, false, false><<<grid, threads, sm, st>>>(a);
+    else if (inverse && !real_in && !real_out) fft_rows_kernel<true, false, false><<<grid, threads, sm, st>>>(a);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
@@ -395,15 +501,15 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     a.twiddle = tw;
     a.D = D;
     a.log2D = ilog2(D);
-    int C = D >= kFftElems ? 1 : kFftElems / D;
-    if (C > 16) C = 16;
-    if (C > D) C = D;
-    a.per_block = C;
+    a.per_block = fft_cols_per_block(D);
     a.inverse = inverse;
     a.scale = scale;
-    dim3 grid(D / C, 3);
-    size_t sm = (size_t)C * (D + 1) * sizeof(cd);
-    fft_cols_kernel<<<grid, 256, sm, st>>>(a);
+    const int tf = D >= 8 ? D / 8 : 1;
+    dim3 grid(D / a.per_block, 3);
+    const int threads = a.per_block * tf;
+    const size_t sm = (size_t)a.per_block * (D + 1) * sizeof(cd);
+    if (inverse) fft_cols_kernel<true><<<grid, threads, sm, st>>>(a);
+    else fft_cols_kernel<false><<<grid, threads, sm, st>>>(a);
     return cudaGetLastError();
 }
 

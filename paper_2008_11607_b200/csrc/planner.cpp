@@ -169,9 +169,9 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         long k = (j < D / 2) ? j : (long)j - D;
         p.ksym[(size_t)j] = (j == D / 2) ? 0.0 : (double)(2.0L * kPiL * (ld)k * (ld)tau);
     }
-    // FFT twiddles e^{-2 pi i j / D}, j = 0..D/2-1.
-    p.twiddle.assign((size_t)D, 0.0);
-    for (int j = 0; j < D / 2; ++j) {
+    // FFT twiddles e^{-2 pi i j / D}, j = 0..D-1 (full circle, long double, rounded once).
+    p.twiddle.assign(2 * (size_t)D, 0.0);
+    for (int j = 0; j < D; ++j) {
         ld th = 2.0L * kPiL * (ld)j / (ld)D;
         p.twiddle[2 * (size_t)j] = (double)std::cos(th);
         p.twiddle[2 * (size_t)j + 1] = (double)(-std::sin(th));

@@ -35,7 +35,7 @@ struct Plan {
     std::vector<double> alpha, C1, C2, gamma;
     std::vector<PoleConst> poles;
     std::vector<double> ksym;        // D tau-scaled derivative symbols, Nyquist zeroed (G2)
-    std::vector<double> twiddle;     // D/2 complex e^{-2 pi i j / D}
+    std::vector<double> twiddle;     // D complex e^{-2 pi i j / D}
 };
 
 // Validates the arguments (see rexi.h) and fills `p`. Returns 0 or a rexi_status_t code;

@@ -79,7 +79,7 @@ def test_plan_errors(R):
 
 
 # ----------------------------------------------------------------------------- S1 / S5
-@pytest.mark.parametrize("D", [4, 8, 64, 128, 256, 512])
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 64, 128, 256, 512, 1024])
 def test_forward_fft_vs_naive_dft(R, D):
     p = R.Plan(D, 0.1)
     f = inputs.white_noise(D)
@@ -91,7 +91,7 @@ def test_forward_fft_vs_naive_dft(R, D):
         assert np.linalg.norm(F[c] - O) / np.linalg.norm(O) < 1e-14
 
 
-@pytest.mark.parametrize("D", [4, 8, 64, 512])
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 64, 256, 512])
 def test_inverse_fft_vs_naive_dft(R, D):
     p = R.Plan(D, 0.1)
     A = inputs.spectral_white(D, seed=3)

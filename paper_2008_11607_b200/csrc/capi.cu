@@ -342,8 +342,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
     info->m0 = h.m0;
     info->rho = h.rho;
     info->predicted_floor = h.predicted_floor;
-    info->flops_per_pole_mode = p->variant == REXI_VARIANT_DZ ? rexi::kFlopsDZ : rexi::kFlopsUV;
-    info->fp64_ops_per_pole_mode = p->variant == REXI_VARIANT_DZ ? rexi::kOpsDZ : rexi::kOpsUV;
+    info->flops_per_pole_mode = rexi::pole_flops(p->variant, p->mpt[p->variant]);
+    info->fp64_ops_per_pole_mode = rexi::pole_ops(p->variant, p->mpt[p->variant]);
     return REXI_OK;
 }
 

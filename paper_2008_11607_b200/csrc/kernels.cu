@@ -140,19 +140,35 @@ __global__ void __launch_bounds__(1024) fft_rows_kernel(FftArgs a) {
     const int n = nb * D;
     const void *inp = f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2];
     void *outp = f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const size_t g = row0 * D + i;
-        smem[i] = REAL_IN ? mk(static_cast<const double *>(inp)[g], 0.0) : static_cast<const cd *>(inp)[g];
+    // every thread moves exactly 8 values (4 when D = 4): unrolled so all loads are in flight
+    cd tmp[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) {
+            const size_t g = row0 * D + i;
+            tmp[q] = REAL_IN ? mk(__ldg(static_cast<const double *>(inp) + g), 0.0)
+                             : static_cast<const cd *>(inp)[g];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) smem[i] = tmp[q];
     }
     __syncthreads();
     const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
     fft_in_smem<INV>(smem + row * D, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const size_t g = row0 * D + i;
-        const cd v = smem[i];
-        if (REAL_OUT) static_cast<double *>(outp)[g] = v.x * sc;
-        else static_cast<cd *>(outp)[g] = mk(v.x * sc, v.y * sc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) {
+            const size_t g = row0 * D + i;
+            const cd v = smem[i];
+            if (REAL_OUT) static_cast<double *>(outp)[g] = v.x * sc;
+            else static_cast<cd *>(outp)[g] = mk(v.x * sc, v.y * sc);
+        }
     }
 }
 
@@ -170,18 +186,29 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
     const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int n = C << log2D;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> logC, c = i & (C - 1);
-        smem[c * stride + r] = in[(size_t)r * D + col0 + c];
+    cd tmp[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) tmp[q] = in[(size_t)(i >> logC) * D + col0 + (i & (C - 1))];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) smem[(i & (C - 1)) * stride + (i >> logC)] = tmp[q];
     }
     __syncthreads();
     const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
     fft_in_smem<INV>(smem + col * stride, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int r = i >> logC, c = i & (C - 1);
-        const cd v = smem[c * stride + r];
-        out[(size_t)r * D + col0 + c] = mk(v.x * sc, v.y * sc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) {
+            const int r = i >> logC, c = i & (C - 1);
+            const cd v = smem[c * stride + r];
+            out[(size_t)r * D + col0 + c] = mk(v.x * sc, v.y * sc);
+        }
     }
 }
 
@@ -204,10 +231,7 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
 // UV variant (paper-literal eq:lswVelocities): (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (p,q),
 //   p = a + i Kx eta1, q = b + i Ky eta1; delta1, zeta1 from (u1, v1); likewise for g2.
 // fp64-pipe instructions per (pole, mode): DZ 71, UV 101 (launch.h).
-#ifndef REXI_POLE_BLOCK
-#define REXI_POLE_BLOCK 128
-#endif
-constexpr int kPoleBlock = REXI_POLE_BLOCK;
+constexpr int kPoleBlock = 128;
 constexpr int kPoleTile = 32;
 
 struct ModeState {
@@ -216,18 +240,24 @@ struct ModeState {
     cd A0, A1, A2;           // accumulators: (eta, delta, zeta) [DZ] or (eta, u, v) [UV]
 };
 
-// One pole, one mode: both shifted solves and the weighted accumulation.
+// 1/(kappa_n + K2) for one pole and one value of K2 (shared by every mode with that K2).
+__device__ __forceinline__ cd pole_den(const PoleConst &P, const double K2) {
+    const double dr = P.kr + K2;
+    const double r = rcp_pos(fma(dr, dr, P.ki2));
+    return mk(dr * r, -P.ki * r);
+}
+
+// One pole, one mode, given q = 1/(kappa + K2): both shifted solves and the weighted
+// accumulation.
 template <int VARIANT>
-__device__ __forceinline__ void pole_body(const PoleConst &P, ModeState &s, const double c) {
+__device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, const cd qd,
+                                            const double c) {
     const cd al = mk(P.ar, P.ai), s2 = mk(P.s2r, P.s2i), s1c = mk(P.s1cr, P.s1ci);
     const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
     const double hn = P.ai;
     // ---- solve 1: Helmholtz for eta1 (eq:lswEta)
     const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));
     const cd num = cfms(s2, s.m0, t);
-    const double dr = P.kr + s.K2;
-    const double r = rcp_pos(fma(dr, dr, P.ki2));
-    const cd qd = mk(dr * r, -P.ki * r);                        // 1/(kappa + K2)
     const cd eta1 = cmul(num, qd);
     if (VARIANT == 0) {
         const cd ia = mk(P.iar, P.iai);
@@ -271,30 +301,73 @@ __device__ __forceinline__ void pole_body(const PoleConst &P, ModeState &s, cons
     }
 }
 
-// grid = (mode tiles of kPoleBlock * MPT modes, pole chunks). Each thread owns MPT modes and
-// runs every pole of its chunk, PU poles per loop trip. MINB = resident blocks per SM asked
-// of ptxas (register budget 65536 / (kPoleBlock * MINB) per thread).
+// Modes of "K2 quad" q of a D x D grid (D/2 x D/2 quads, q = a * D/2 + b): four modes with the
+// same K2 = Kx^2 + Ky^2 (exactly, the symbols being odd in k and zero at 0 and Nyquist):
+//   a, b > 0:  (a, b) (a, D-b) (D-a, b) (D-a, D-b)          [row l, column k]
+//   a = 0 < b: (0, b) (0, D-b) (b, 0) (D-b, 0)              [axes]
+//   b = 0 < a: (H, a) (H, D-a) (a, H) (D-a, H), H = D/2     [Nyquist lines]
+//   a = b = 0: (0, 0) (0, H) (H, 0) (H, H)                  [K2 = 0]
+// The quads partition all D^2 modes.
+__device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) {
+    const int H = D >> 1;
+    const int a = (int)(q >> (log2D - 1)), b = (int)(q & (H - 1));
+    int l[4], k[4];
+    if (a > 0 && b > 0) {
+        l[0] = a; k[0] = b; l[1] = a; k[1] = D - b; l[2] = D - a; k[2] = b; l[3] = D - a; k[3] = D - b;
+    } else if (b > 0) {
+        l[0] = 0; k[0] = b; l[1] = 0; k[1] = D - b; l[2] = b; k[2] = 0; l[3] = D - b; k[3] = 0;
+    } else if (a > 0) {
+        l[0] = H; k[0] = a; l[1] = H; k[1] = D - a; l[2] = a; k[2] = H; l[3] = D - a; k[3] = H;
+    } else {
+        l[0] = 0; k[0] = 0; l[1] = 0; k[1] = H; l[2] = H; k[2] = 0; l[3] = H; k[3] = H;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = ((long)l[j] << log2D) + k[j];
+}
+
+// grid = (tiles, pole chunks). MPT < 4: a thread owns MPT modes m = tile0 + j * 128 + tid.
+// MPT = 4: a thread owns one K2 quad (quad_modes) and computes the pole denominator
+// 1/(kappa_n + K2) once for its four modes. Every thread runs all poles of its chunk, PU poles
+// per loop trip. MINB = resident blocks per SM asked of ptxas (register budget).
 template <int VARIANT, int MPT, int PU, int MINB>
 __global__ void __launch_bounds__(kPoleBlock, MINB)
 pole_kernel(PoleArgs a) {
+    constexpr bool QUAD = (MPT == 4);
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
-    const long tile0 = (long)blockIdx.x * (kPoleBlock * MPT);
     const int chunk = blockIdx.y;
     const long len = a.pole_end - a.pole_begin;
     const long p0 = a.pole_begin + len * chunk / a.n_chunks;
     const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
-    double c = a.tau;
-#if REXI_C_IN_REG
-    asm volatile("mov.b64 %0, %0;" : "+d"(c));   // keep c in a per-thread register
-#endif
+    const double c = a.tau;
     const double hmu = a.hmu;
+
+    long mode[MPT];
+    bool valid[MPT];
+    if (QUAD) {
+        const long q = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+        const bool ok = q < (n_modes >> 2);
+        long mq[4];
+        quad_modes(ok ? q : 0, a.D, a.log2D, mq);
+#pragma unroll
+        for (int j = 0; j < MPT; ++j) {
+            mode[j] = mq[j & 3];
+            valid[j] = ok;
+        }
+    } else {
+        const long tile0 = (long)blockIdx.x * (kPoleBlock * MPT);
+#pragma unroll
+        for (int j = 0; j < MPT; ++j) {
+            const long m = tile0 + j * kPoleBlock + threadIdx.x;
+            valid[j] = m < n_modes;
+            mode[j] = valid[j] ? m : 0;
+        }
+    }
 
     ModeState st[MPT];
 #pragma unroll
     for (int j = 0; j < MPT; ++j) {
-        const long m = tile0 + j * kPoleBlock + threadIdx.x;
-        const long mm = m < n_modes ? m : 0;
+        const long mm = mode[j];
         const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
         const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
         const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
@@ -327,32 +400,33 @@ pole_kernel(PoleArgs a) {
         int q = 0;
 #pragma unroll 1
         for (; q + PU <= cnt; q += PU) {
-#if REXI_ABLATE_LDS
-            // timing ablation only (wrong results): constants stay in registers
-            const PoleConst Pr = sp[0];
 #pragma unroll
-            for (int u = 0; u < PU; ++u)
+            for (int u = 0; u < PU; ++u) {
+                const PoleConst &P = sp[q + u];
+                if (QUAD) {
+                    const cd qd = pole_den(P, st[0].K2);
 #pragma unroll
-                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(Pr, st[j], c);
-#else
+                    for (int j = 0; j < MPT; ++j) pole_solves<VARIANT>(P, st[j], qd, c);
+                } else {
 #pragma unroll
-            for (int u = 0; u < PU; ++u)
-#pragma unroll
-                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(sp[q + u], st[j], c);
-#endif
+                    for (int j = 0; j < MPT; ++j) pole_solves<VARIANT>(P, st[j], pole_den(P, st[j].K2), c);
+                }
+            }
         }
         if (PU > 1) {
 #pragma unroll 1
-            for (; q < cnt; ++q)
+            for (; q < cnt; ++q) {
+                const PoleConst &P = sp[q];
 #pragma unroll
-                for (int j = 0; j < MPT; ++j) pole_body<VARIANT>(sp[q], st[j], c);
+                for (int j = 0; j < MPT; ++j) pole_solves<VARIANT>(P, st[j], pole_den(P, st[j].K2), c);
+            }
         }
     }
     cd *out = a.partial + (size_t)chunk * 3 * n_modes;
 #pragma unroll
     for (int j = 0; j < MPT; ++j) {
-        const long m = tile0 + j * kPoleBlock + threadIdx.x;
-        if (m < n_modes) {
+        if (valid[j]) {
+            const long m = mode[j];
             out[m] = st[j].A0;
             out[n_modes + m] = st[j].A1;
             out[2 * n_modes + m] = st[j].A2;
@@ -541,7 +615,7 @@ cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_p
 
 cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st) {
     const long mpb = kPoleBlock * mpt;
-    const long tiles = (a.n_modes + mpb - 1) / mpb;
+    const long tiles = (a.n_modes + mpb - 1) / mpb;   // MPT = 4: D^2/4 quads / 128 per block
     dim3 grid((unsigned)tiles, (unsigned)a.n_chunks);
 #define X(V, M, U, B)                                                   \
     if (variant == V && mpt == M && pu == U && minb == B) {             \

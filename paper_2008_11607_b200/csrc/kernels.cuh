@@ -44,9 +44,7 @@ __device__ __forceinline__ cd cjfms(cd a, cd b, cd c) {
 // (relative error ~ e0^3 with e0 ~ 2^-20 seed error). Not correctly rounded; <= 1 ulp.
 __device__ __forceinline__ double rcp_pos(double d) {
     double r;
-#if REXI_ABLATE_RCP
-    r = d * 1.0e-3;   // timing ablation only (wrong results)
-#elif REXI_RCP_F32_SEED
+#if REXI_RCP_F32_SEED
     // seed from the fp32 MUFU (XU pipe) instead of MUFU.RCP64H; |d| in fp32 range
     float rf;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"(__double2float_rn(d)));

@@ -21,8 +21,18 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:
 // flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each).
-// DESIGN.md "Pole kernel" lists the count line by line.
+// The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
+// by four modes. DESIGN.md "Pole kernel" lists the count line by line.
 constexpr double kFlopsDZ = 131.0, kOpsDZ = 71.0;
 constexpr double kFlopsUV = 183.0, kOpsUV = 101.0;
+constexpr double kDenFlops = 11.0, kDenOps = 7.0;
+inline double pole_flops(int variant, int mpt) {
+    const double f = variant == 0 ? kFlopsDZ : kFlopsUV;
+    return mpt == 4 ? f - kDenFlops * 0.75 : f;
+}
+inline double pole_ops(int variant, int mpt) {
+    const double f = variant == 0 ? kOpsDZ : kOpsUV;
+    return mpt == 4 ? f - kDenOps * 0.75 : f;
+}
 
 }  // namespace rexi

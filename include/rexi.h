@@ -71,9 +71,20 @@ typedef enum {
  *                   eq:lswVelocities. */
 typedef enum { REXI_VARIANT_DZ = 0, REXI_VARIANT_UV = 1 } rexi_variant_t;
 
+/* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
+ *  REXI_METHOD_REXII: the paper's REXII, two solves per term (eq:REXI_Modified_matrix,
+ *                     half-sum eq:modifiedRexiMatrixReducedSum) — the default.
+ *  REXI_METHOD_REXI:  the original REXI, eq:originalREXImatrix,
+ *                     Re sum_{n=-N}^{N} beta^Re_n (tau A + alpha_n I)^{-1} f0, one solve per
+ *                     term, evaluated as the half-sum n = 0..N with Gamma_n (the Appendix A
+ *                     table is conjugate-symmetric, so beta^Re_{-n} = conj(beta^Re_n);
+ *                     DESIGN.md reading R2). Always uses the DZ back-substitution. */
+typedef enum { REXI_METHOD_REXII = 0, REXI_METHOD_REXI = 1 } rexi_method_t;
+
 typedef struct {
     int D;                  /* grid size (power of two, 4..8192)                     */
     int variant;            /* rexi_variant_t                                         */
+    int method;             /* rexi_method_t                                          */
     double tau;             /* step size                                              */
     double tol;             /* requested tolerance (0 if M was given explicitly)      */
     double h;               /* Gaussian spacing h (eq:bm)                             */
@@ -109,10 +120,17 @@ rexi_status_t rexi_plan_info(rexi_plan_t plan, rexi_plan_info_t *info);
 /* Select the pole-kernel formulation (rexi_variant_t). EINVAL for unknown values. */
 rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
 
+/* Select the method (rexi_method_t); rebuilds and uploads the term table for the plan's
+ * (h, M) (synchronous: waits for the device). EINVAL for unknown values. */
+rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
+
 /* Pole-kernel tuning for the plan's CURRENT variant: Fourier modes per thread, poles per loop
  * trip and resident blocks per SM requested of the compiler (register budget). Supported:
- *   DZ: (1,1,8) (2,1,4) (2,1,5) (2,2,3) (3,1,3) (3,1,4) (4,1,2) (4,1,3) (4,1,4)  default (4,1,4)
- *   UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (3,1,3)
+ *   REXII DZ: (1,1,8) (2,1,4) (2,1,5) (2,2,3) (3,1,3) (3,1,4) (4,1,2) (4,1,3) (4,1,4)  default (4,1,4)
+ *   REXII UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (4,1,3)
+ *   REXI:     (1,1,8) (2,1,4) (4,1,3) (4,1,4)                                          default (4,1,4)
+ * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
+ * the pole denominator 1/(kappa_n + K^2)).
  * Per pole and mode the operation order is the same for every tuning; the number of pole
  * chunks (and so the order in which chunk partial sums are added) follows the tile count, so
  * results agree to rounding, not bit for bit. EINVAL otherwise. */
@@ -122,7 +140,8 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int p
 /* Copy the plan's term table to HOST arrays of n_poles entries each (any may be NULL):
  *   alpha[2n], C1[2n], C2[2n] (interleaved re, im) and gamma[n], for n = 0..N:
  *   alpha_n = h(mu + i n), C1_n = c1_n h mu + c2_n h n, C2_n = i c2_n
- *   (PAPER.md:270), Gamma_0 = 1, Gamma_n = 2. Synchronous. */
+ *   (PAPER.md:270), Gamma_0 = 1, Gamma_n = 2. For a REXI plan C1 holds
+ *   beta^Re_n and C2 is zero. Synchronous. */
 rexi_status_t rexi_plan_coeffs(rexi_plan_t plan, double *alpha, double *C1, double *C2,
                                double *gamma);
 
@@ -178,10 +197,13 @@ rexi_status_t rexi_timing_read(rexi_plan_t plan, double *pole_kernel_ms, long *p
  * returns L (= 24). a may be NULL to query L. */
 int rexi_appendix_a(double *mu, double *a);
 
-/* Host-only (no GPU needed): the planner's half-sum term table for (h, M) — the same
- * numbers rexi_plan_coeffs returns for a plan with that h and M. Returns n_poles = M + 25
- * (or -1 if h is not in (0, pi) or M < 12); arrays of n_poles entries may be NULL. */
-long rexi_terms_host(double h, long M, double *alpha, double *C1, double *C2, double *gamma);
+/* Host-only (no GPU needed): the planner's half-sum term table for (h, M) and a method — the
+ * same numbers rexi_plan_coeffs returns for a plan with that h, M and method. For REXII:
+ * alpha_n, C1_n, C2_n, Gamma_n; for REXI: alpha_n, beta^Re_n (in C1), 0 (in C2), Gamma_n.
+ * Returns n_poles = M + 25 (or -1 if h is not in (0, pi), M < 12 or the method is unknown);
+ * arrays of n_poles entries may be NULL. */
+long rexi_terms_host(double h, long M, int method, double *alpha, double *C1, double *C2,
+                     double *gamma);
 
 /* Host-only (no GPU needed): the term-count rule used by rexi_plan_create:
  * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0. */

@@ -53,9 +53,12 @@ struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
     int variant = REXI_VARIANT_DZ;
-    // pole-kernel tuning per variant: modes per thread, poles per loop trip, min blocks/SM
-    int mpt[2] = {4, 3}, pu[2] = {1, 1}, minb[2] = {4, 3};
-    int occ_cache[2] = {0, 0};    // resident blocks per SM of the current tuning; 0 = unknown
+    int method = REXI_METHOD_REXII;
+    // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
+    // poles per loop trip, min blocks/SM
+    int mpt[3] = {4, 4, 4}, pu[3] = {1, 1, 1}, minb[3] = {4, 3, 4};
+    int occ_cache[3] = {0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
+    int kind() const { return method == REXI_METHOD_REXI ? 2 : variant; }
     long n_modes = 0;
     int num_sms = 0;
     int max_chunks = 1;
@@ -96,7 +99,7 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range) {
     if (n_range <= 0) return 0;
-    const int v = p->variant;
+    const int v = p->kind();
     const long mpb = rexi::pole_modes_per_block(p->mpt[v]);
     const long tiles = (p->n_modes + mpb - 1) / mpb;
     int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];
@@ -181,7 +184,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    CK(rexi::launch_poles(a, p->variant, p->mpt[p->variant], p->pu[p->variant], p->minb[p->variant], st));
+    const int kd = p->kind();
+    CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     rexi::FinishArgs f;
@@ -192,11 +196,12 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     f.n_chunks = chunks;
     f.D = a.D;
     f.log2D = a.log2D;
-    f.variant = p->variant;
+    f.variant = kd;
     CK(rexi::launch_finish(f, st));
     p->launches += 2;
-    if (p->variant == REXI_VARIANT_DZ) {
+    if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
         rexi::FixupArgs x;
+        x.method = p->method;
         x.fhat = fhat;
         x.acc = acc;
         x.poles = p->d_poles;
@@ -331,6 +336,7 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
     const rexi::Plan &h = p->host;
     info->D = h.D;
     info->variant = p->variant;
+    info->method = p->method;
     info->tau = h.tau;
     info->tol = h.tol;
     info->h = h.h;
@@ -342,8 +348,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
     info->m0 = h.m0;
     info->rho = h.rho;
     info->predicted_floor = h.predicted_floor;
-    info->flops_per_pole_mode = rexi::pole_flops(p->variant, p->mpt[p->variant]);
-    info->fp64_ops_per_pole_mode = rexi::pole_ops(p->variant, p->mpt[p->variant]);
+    info->flops_per_pole_mode = rexi::pole_flops(p->kind(), p->mpt[p->kind()]);
+    info->fp64_ops_per_pole_mode = rexi::pole_ops(p->kind(), p->mpt[p->kind()]);
     return REXI_OK;
 }
 
@@ -354,10 +360,29 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     return REXI_OK;
 }
 
+rexi_status_t rexi_plan_set_method(rexi_plan_t p, int method) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (method != REXI_METHOD_REXII && method != REXI_METHOD_REXI)
+            return fail(REXI_EINVAL, "unknown method");
+        if (method == p->method) return REXI_OK;
+        rexi::Plan np;
+        std::vector<char> err;
+        const rexi::Plan &h = p->host;
+        int st = rexi::make_plan(np, h.D, h.tau, h.tol, h.h, h.M, err, method);
+        if (st != REXI_OK) return fail((rexi_status_t)st, err.empty() ? "planner" : std::string(err.data()));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
+        p->host = std::move(np);
+        p->method = method;
+        return REXI_OK;
+    });
+}
+
 rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int poles_per_iter,
                                    int min_blocks_per_sm) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    const int v = p->variant;
+    const int v = p->kind();
     if (!rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm))
         return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
     p->mpt[v] = modes_per_thread;

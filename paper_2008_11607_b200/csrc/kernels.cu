@@ -259,7 +259,15 @@ __device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, co
     const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));
     const cd num = cfms(s2, s.m0, t);
     const cd eta1 = cmul(num, qd);
-    if (VARIANT == 0) {
+    if (VARIANT == 2) {
+        // original REXI (eq:originalREXImatrix): one solve per term, acc += Gamma beta^Re g1
+        const cd ia = mk(P.iar, P.iai);
+        const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
+        const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
+        s.A0 = cfma(w1, eta1, s.A0);
+        s.A1 = cfma(w1, del1, s.A1);
+        s.A2 = cfma(w1, zet1, s.A2);
+    } else if (VARIANT == 0) {
         const cd ia = mk(P.iar, P.iai);
         const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
         const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
         s1 = mk(s1.x + x1.x, s1.y + x1.y);
         s2 = mk(s2.x + x2.x, s2.y + x2.y);
     }
-    if (a.variant == 0) {
+    if (a.variant != 1) {   // DZ accumulators (REXII-DZ and REXI): (delta, zeta) -> (u, v)
         const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
         const double kx = a.ksym[k], ky = a.ksym[l];
         const double K2 = fma(kx, kx, ky * ky);
@@ -485,6 +493,11 @@ __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
         const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
         const cd u1 = cfms(s4, vb, cmul(s3, ua));
         const cd v1 = cfma(s3, vb, cmul(s4, ua));
+        if (a.method == 1) {   // REXI: one solve per term
+            Au = cfma(w1, u1, Au);
+            Av = cfma(w1, v1, Av);
+            continue;
+        }
         const cd u2 = cjfma(s4, v1, cjfma(s3, u1, mk(0, 0)));
         const cd v2 = cjfms(s4, u1, cjfma(s3, v1, mk(0, 0)));
         Au = cfma(w2, u2, cfma(w1, u1, Au));
@@ -588,10 +601,12 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
 }
 
 // Supported (variant, modes per thread, poles per loop trip, min blocks per SM) instantiations.
+// Kernel kinds: 0 = REXII DZ, 1 = REXII UV, 2 = REXI (DZ back-substitution).
 #define REXI_POLE_CONFIGS(X)                                                             \
     X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 2, 2, 3) X(0, 3, 1, 3) X(0, 3, 1, 4)  \
     X(0, 4, 1, 2) X(0, 4, 1, 3) X(0, 4, 1, 4)                                             \
-    X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)
+    X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)  \
+    X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 3)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 

@@ -82,6 +82,7 @@ struct FinishArgs {
 };
 
 struct FixupArgs {
+    int method;            // 0: REXII, 1: REXI
     const cd *fhat;
     cd *acc;
     const PoleConst *poles;

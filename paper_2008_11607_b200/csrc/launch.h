@@ -26,12 +26,14 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 constexpr double kFlopsDZ = 131.0, kOpsDZ = 71.0;
 constexpr double kFlopsUV = 183.0, kOpsUV = 101.0;
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
-inline double pole_flops(int variant, int mpt) {
-    const double f = variant == 0 ? kFlopsDZ : kFlopsUV;
+// REXI (kind 2): solve 1 (num 6/12, den 7/11, eta1 4/6, delta1 4/8, zeta1 6/10) + 3 MACs 12/24.
+constexpr double kFlopsREXI = 71.0, kOpsREXI = 39.0;
+inline double pole_flops(int kind, int mpt) {
+    const double f = kind == 0 ? kFlopsDZ : kind == 1 ? kFlopsUV : kFlopsREXI;
     return mpt == 4 ? f - kDenFlops * 0.75 : f;
 }
-inline double pole_ops(int variant, int mpt) {
-    const double f = variant == 0 ? kOpsDZ : kOpsUV;
+inline double pole_ops(int kind, int mpt) {
+    const double f = kind == 0 ? kOpsDZ : kind == 1 ? kOpsUV : kOpsREXI;
     return mpt == 4 ? f - kDenOps * 0.75 : f;
 }
 

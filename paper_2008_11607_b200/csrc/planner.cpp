@@ -69,7 +69,13 @@ static void set_err(std::vector<char> &err, const char *msg) {
     err.assign(msg, msg + std::strlen(msg) + 1);
 }
 
-int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err) {
+int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err,
+              int method) {
+    if (method != 0 && method != 1) {
+        set_err(err, "method must be REXI_METHOD_REXII or REXI_METHOD_REXI");
+        return REXI_EINVAL;
+    }
+    p.method = method;
     if (D < 4 || D > 8192 || (D & (D - 1)) != 0) {
         set_err(err, "D must be a power of two in [4, 8192]");
         return REXI_EINVAL;
@@ -123,18 +129,24 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         // c_{1,n} = h sum_{k=L1}^{L2} Re(a_k) b_{n-k},  c_{2,n} = h sum Im(a_k) b_{n-k}
         // L1(n) = max(-L, n - M), L2(n) = min(L, n + M)
         long L1 = std::max<long>(-kL, n - M), L2 = std::min<long>(kL, n + M);
-        cld c1(0, 0), c2(0, 0);
+        cld c1(0, 0), c2(0, 0), beta(0, 0);
         for (long k = L1; k <= L2; ++k) {
             cld ak = a_coeff((int)k);
             const cld &bnk = b[(size_t)(n - k + M)];
             c1 += ak.real() * bnk;
             c2 += ak.imag() * bnk;
+            beta += ak * bnk.real();   // beta^Re_n = h sum a_k Re(b_{n-k})
         }
         c1 *= hh;
         c2 *= hh;
+        beta *= hh;
         // C_{1,n} = c_{1,n} h mu + c_{2,n} h n ; C_{2,n} = i c_{2,n}
         cld C1 = c1 * hh * mu + c2 * hh * (ld)n;
         cld C2 = cld(0, 1) * c2;
+        if (method == 1) {   // REXI: the table carries beta^Re_n in C1 and zero in C2
+            C1 = beta;
+            C2 = cld(0, 0);
+        }
         cld alpha(hh * mu, hh * (ld)n);                   // alpha_n = h(mu + i n)
         ld gam = (n == 0) ? 1.0L : 2.0L;                  // Gamma_n
         p.alpha[2 * n] = (double)alpha.real();  p.alpha[2 * n + 1] = (double)alpha.imag();
@@ -146,6 +158,13 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         cld kappa = alpha * alpha + c * c;                // kappa_n (tau-scaled)
         cld w1 = gam * C2;                                // reading G4 (division-free g3)
         cld w2 = gam * (C1 - C2 * std::conj(alpha));
+        if (method == 1) {
+            // REXI half-sum: Re sum_{n=-N}^{N} beta_n (tau A + alpha_n)^{-1} f0
+            //              = Re sum_{n=0}^{N} Gamma_n beta_n (...) f0 for real A, f0, since
+            // beta^Re_{-n} = conj(beta^Re_n) with the symmetric Appendix A table (reading R2).
+            w1 = gam * beta;
+            w2 = cld(0, 0);
+        }
         cld s2 = c / alpha, ia = 1.0L / alpha, s1c = std::conj(kappa / alpha);
         cld s3 = alpha / kappa, s4 = c / kappa;
         PoleConst &q = p.poles[(size_t)n];
@@ -197,13 +216,14 @@ extern "C" long rexi_rule_M(int D, double tau, double tol, double h) {
     return (long)std::ceil(x / h) + rexi::m0_for_tol(tol, h);
 }
 
-extern "C" long rexi_terms_host(double h, long M, double *alpha, double *C1, double *C2, double *gamma) {
+extern "C" long rexi_terms_host(double h, long M, int method, double *alpha, double *C1, double *C2,
+                                double *gamma) {
     if (!(h > 0.0 && h < M_PI) || M < 12) return -1;
     rexi::Plan p;
     std::vector<char> err;
     try {
         // D and tau do not enter the term table; D = 4, tau = 0 keep the rest cheap.
-        if (rexi::make_plan(p, 4, 0.0, 0.0, h, M, err) != REXI_OK) return -1;
+        if (rexi::make_plan(p, 4, 0.0, 0.0, h, M, err, method) != REXI_OK) return -1;
     } catch (...) {
         return -1;
     }

@@ -28,11 +28,12 @@ static_assert(sizeof(PoleConst) == 160, "PoleConst layout");
 
 struct Plan {
     int D = 0;
+    int method = 0;                  // 0: REXII (eq:REXI_Modified_matrix), 1: REXI (eq:originalREXImatrix)
     double tau = 0, tol = 0, h = 0, mu = 0;
     long M = 0, L = 24, N = 0, n_poles = 0, m0 = 11;
     double rho = 0, predicted_floor = 0;
     // term table, n = 0..N (interleaved re/im for complex entries)
-    std::vector<double> alpha, C1, C2, gamma;
+    std::vector<double> alpha, C1, C2, gamma;   // REXI plans: C1 = beta^Re_n, C2 = 0
     std::vector<PoleConst> poles;
     std::vector<double> ksym;        // D tau-scaled derivative symbols, Nyquist zeroed (G2)
     std::vector<double> twiddle;     // D complex e^{-2 pi i j / D}
@@ -40,7 +41,8 @@ struct Plan {
 
 // Validates the arguments (see rexi.h) and fills `p`. Returns 0 or a rexi_status_t code;
 // `err` receives a message.
-int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err);
+int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err,
+              int method = 0);
 
 long m0_for_tol(double tol, double h);
 

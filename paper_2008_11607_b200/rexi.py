@@ -23,6 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
 VARIANTS = {"dz": 0, "uv": 1}
+METHODS = {"rexii": 0, "rexi": 1}
 
 _vp = ctypes.c_void_p
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -30,7 +31,8 @@ _lp = ctypes.POINTER(ctypes.c_long)
 
 
 class PlanInfo(ctypes.Structure):
-    _fields_ = [("D", ctypes.c_int), ("variant", ctypes.c_int), ("tau", ctypes.c_double),
+    _fields_ = [("D", ctypes.c_int), ("variant", ctypes.c_int), ("method", ctypes.c_int),
+                ("tau", ctypes.c_double),
                 ("tol", ctypes.c_double), ("h", ctypes.c_double), ("mu", ctypes.c_double),
                 ("M", ctypes.c_long), ("L", ctypes.c_long), ("N", ctypes.c_long),
                 ("n_poles", ctypes.c_long), ("m0", ctypes.c_long), ("rho", ctypes.c_double),
@@ -44,6 +46,7 @@ EXPORTS = {
     "rexi_plan_destroy": (ctypes.c_int, [_vp]),
     "rexi_plan_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "rexi_plan_set_variant": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_plan_set_method": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -57,7 +60,7 @@ EXPORTS = {
     "rexi_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_timing_read": (ctypes.c_int, [_vp, _dp, _lp, _lp]),
     "rexi_appendix_a": (ctypes.c_int, [_dp, _dp]),
-    "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, _dp, _dp, _dp, _dp]),
+    "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, ctypes.c_int, _dp, _dp, _dp, _dp]),
     "rexi_rule_M": (ctypes.c_long, [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rexi_last_error": (ctypes.c_char_p, []),
@@ -96,14 +99,16 @@ def appendix_a():
     return mu.value, a[0::2] + 1j * a[1::2]
 
 
-def terms_host(h, M):
-    """The planner's half-sum table (alpha, C1, C2, gamma) for (h, M), computed on the host."""
-    n = _lib.rexi_terms_host(float(h), int(M), None, None, None, None)
+def terms_host(h, M, method="rexii"):
+    """The planner's half-sum table (alpha, C1, C2, gamma) for (h, M), computed on the host.
+    For method "rexi", C1 holds beta^Re_n and C2 is zero."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    n = _lib.rexi_terms_host(float(h), int(M), m, None, None, None, None)
     if n < 0:
-        raise ValueError("invalid h or M")
+        raise ValueError("invalid h, M or method")
     al, c1, c2 = (np.zeros(2 * n) for _ in range(3))
     g = np.zeros(n)
-    _lib.rexi_terms_host(float(h), int(M), _np_ptr(al), _np_ptr(c1), _np_ptr(c2), _np_ptr(g))
+    _lib.rexi_terms_host(float(h), int(M), m, _np_ptr(al), _np_ptr(c1), _np_ptr(c2), _np_ptr(g))
     z = lambda x: x[0::2] + 1j * x[1::2]
     return z(al), z(c1), z(c2), g
 
@@ -125,7 +130,7 @@ def _torch():
 class Plan:
     """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
 
-    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="dz"):
+    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="dz", method="rexii"):
         torch = _torch()
         if device is None:
             device = torch.cuda.current_device()
@@ -135,6 +140,7 @@ class Plan:
                                      float(tol if tol is not None else 0.0),
                                      float(h), int(M), self.device), "rexi_plan_create")
         self.set_variant(variant)
+        self.set_method(method)
         inf = self.info
         self.D = inf["D"]
         self.n_poles = inf["n_poles"]
@@ -169,8 +175,13 @@ class Plan:
         _check(_lib.rexi_plan_set_variant(self._h, v), "rexi_plan_set_variant")
         self.variant = v
 
+    def set_method(self, method):
+        m = METHODS[method] if isinstance(method, str) else int(method)
+        _check(_lib.rexi_plan_set_method(self._h, m), "rexi_plan_set_method")
+        self.method = m
+
     def set_tuning(self, modes_per_thread, poles_per_iter=1, min_blocks_per_sm=4):
-        """Tune the pole kernel of the current variant (see rexi_plan_set_tuning)."""
+        """Tune the pole kernel of the current variant/method (see rexi_plan_set_tuning)."""
         _check(_lib.rexi_plan_set_tuning(self._h, int(modes_per_thread), int(poles_per_iter),
                                          int(min_blocks_per_sm)), "rexi_plan_set_tuning")
 

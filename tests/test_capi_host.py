@@ -77,3 +77,15 @@ def test_terms_host_rejects_bad_args(rexi):
         rexi.terms_host(3.5, 50)
     with pytest.raises(ValueError):
         rexi.terms_host(0.5, 5)
+
+
+@pytest.mark.parametrize("h,M", [(0.2, 150), (0.5, 65), (0.2, 1000)])
+def test_planner_rexi_terms_match_oracle(rexi, h, M):
+    """NEXT-1 table: beta^Re_n of the planner vs the oracle, n = 0..N."""
+    al, beta, zero, g = rexi.terms_host(h, M, "rexi")
+    t = C.rexi_terms(h, M)
+    sel = t.n >= 0
+    assert np.abs(al - t.alpha[sel]).max() <= 1e-15 * np.abs(al).max()
+    assert np.abs(beta - t.beta_re[sel]).max() <= 2e-15 * np.abs(t.beta_re).max()
+    assert np.all(zero == 0)
+    assert g[0] == 1.0 and np.all(g[1:] == 2.0)

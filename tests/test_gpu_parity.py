@@ -309,3 +309,76 @@ def test_tuning_rejects_unsupported(R):
     p = R.Plan(16, 1.0)
     with pytest.raises(R.RexiError):
         p.set_tuning(3, 3, 3)
+
+
+
+# ----------------------------------------------------------------------------- paper rows on GPU
+from conftest import read_paper_tables  # noqa: E402
+
+_SCEN = {"wave1": inputs.wave_scenario_1, "wave2": inputs.wave_scenario_2,
+         "gaussian": inputs.gaussian_scenario}
+
+# The printed rows of tests/golden/paper_tables.txt plus the large-M rows of Tables 3, 4, 6, 7
+# (too slow for the CPU oracle on the full grid; one GPU step each here).
+EXTRA_ROWS = [
+    dict(method="REXII", scenario="wave1", tau=50.0, h=0.1, M=13341, paper=1.81e-13, cite="PAPER.md:664"),
+    dict(method="REXII", scenario="wave2", tau=50.0, h=0.5, M=56885, paper=6.53e-13, cite="PAPER.md:706"),
+    dict(method="REXII", scenario="wave2", tau=50.0, h=0.1, M=284371, paper=9.36e-13, cite="PAPER.md:707"),
+    dict(method="REXII", scenario="gaussian", tau=1.0, h=0.1, M=5698, paper=1.53e-14, cite="PAPER.md:764"),
+    dict(method="REXII", scenario="gaussian", tau=50.0, h=1.0, M=28448, paper=6.18e-13, cite="PAPER.md:787"),
+    dict(method="REXII", scenario="gaussian", tau=50.0, h=0.5, M=56885, paper=6.06e-14, cite="PAPER.md:788"),
+    dict(method="REXII", scenario="gaussian", tau=50.0, h=0.1, M=284371, paper=1.04e-13, cite="PAPER.md:789"),
+    dict(method="REXI", scenario="wave1", tau=1.0, h=0.2, M=100000, paper=3.27e-8, cite="PAPER.md:629"),
+    dict(method="REXI", scenario="gaussian", tau=1.0, h=0.2, M=1500, paper=3.78e-4, cite="PAPER.md:758"),
+    dict(method="REXI", scenario="gaussian", tau=1.0, h=0.2, M=3000, paper=3.21e-6, cite="PAPER.md:759"),
+]
+
+
+@pytest.mark.parametrize("row", read_paper_tables() + EXTRA_ROWS,
+                         ids=lambda r: f"{r['method']}-{r['scenario']}-t{r['tau']}-h{r['h']}-M{r['M']}")
+def test_gpu_reproduces_paper_rows(R, row):
+    """The CUDA path's one-step max-norm error vs the exact propagator (reading G15) on the
+    paper's 128^2 grid reproduces each printed error within a factor 2.5 (Tables 2-7)."""
+    D = 128
+    f = _SCEN[row["scenario"]](D)
+    p = R.Plan(D, row["tau"], h=row["h"], M=row["M"], method=row["method"].lower())
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    ex = lrsw.exact_step(*f, row["tau"])
+    err = max(float(np.abs(a - b).max()) for a, b in zip(got, ex))
+    assert row["paper"] / 2.5 < err < row["paper"] * 2.5, (err, row)
+
+
+@pytest.mark.parametrize("D,tau,h,M", [(16, 1.0, 0.2, 150), (32, 0.5, 0.2, 400), (8, 2.0, 0.5, 60)])
+def test_rexi_method_vs_oracle(R, D, tau, h, M):
+    """NEXT-1: the original REXI on the GPU (half-sum, reading R2) vs the oracle's full sum
+    n = -N..N of eq:originalREXImatrix with dense solves, after Re."""
+    f = inputs.white_noise(D)
+    p = R.Plan(D, tau, h=h, M=M, method="rexi")
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    ref = lrsw.rexi_step(*f, tau, h, M)
+    assert rel_l2(got, ref) < TOL
+
+
+@pytest.mark.parametrize("mpt,pu,minb", [(1, 1, 8), (2, 1, 4), (4, 1, 3), (4, 1, 4)])
+def test_rexi_method_tunings(R, mpt, pu, minb):
+    D, tau, h, M = 32, 1.0, 0.2, 300
+    f = [dev(x) for x in inputs.white_noise(D)]
+    p = R.Plan(D, tau, h=h, M=M, method="rexi")
+    base = [host(t) for t in p.apply(*f)]
+    p.set_tuning(mpt, pu, minb)
+    got = [host(t) for t in p.apply(*f)]
+    assert rel_l2(got, base) < 1e-14
+
+
+def test_set_method_roundtrip(R):
+    D = 32
+    f = [dev(x) for x in inputs.white_noise(D)]
+    p = R.Plan(D, 1.0, h=0.2, M=200)
+    a = [host(t) for t in p.apply(*f)]
+    p.set_method("rexi")
+    al, beta, zero, g = p.coeffs()
+    assert np.all(zero == 0)
+    p.set_method("rexii")
+    b = [host(t) for t in p.apply(*f)]
+    assert rel_l2(a, b) == 0.0
+    assert p.info["method"] == 0

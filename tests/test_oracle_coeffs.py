@@ -183,3 +183,24 @@ def test_M_rule_configs():
     assert C.M_lrsw(512, 1.0, 0.5, 1e-8) == 4558
     assert C.M_lrsw(64, 0.02, 0.5, 1e-12) == 22
     assert C.M_lrsw(4096, 1.0, 0.5, 1e-12) == 36407
+
+
+def test_rexi_beta_conjugate_symmetry_R2():
+    """Reading R2: with the conjugate-symmetric Appendix A table,
+    beta^Re_{-n} = conj(beta^Re_n); for a REAL matrix A and real f0 the term -n of
+    eq:originalREXImatrix is then the complex conjugate of term n, so the real part of the full
+    sum n = -N..N equals the half sum n = 0..N with Gamma_n. Checked on a random real 6x6."""
+    h, M = 0.2, 150
+    t = C.rexi_terms(h, M)
+    assert np.abs(t.beta_re - np.conj(t.beta_re[::-1])).max() < 1e-15 * np.abs(t.beta_re).max()
+    g = np.random.Generator(np.random.PCG64(3))
+    B = g.standard_normal((6, 6))
+    A = (B - B.T) * 2.0                       # real skew-symmetric, spectrum on iR
+    f = g.standard_normal(6)
+    I = np.eye(6)
+    full = sum(np.real(b * np.linalg.solve(A + a * I, f)) for b, a in zip(t.beta_re, t.alpha))
+    sel = t.n >= 0
+    gam = np.where(t.n[sel] == 0, 1.0, 2.0)
+    half = sum(gg * np.real(b * np.linalg.solve(A + a * I, f))
+               for gg, b, a in zip(gam, t.beta_re[sel], t.alpha[sel]))
+    assert np.abs(full - half).max() < 1e-12 * np.abs(full).max()

@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
 //   p = a + i Kx eta1, q = b + i Ky eta1; delta1, zeta1 from (u1, v1); likewise for g2.
 // fp64-pipe instructions per (pole, mode): DZ 71, UV 101 (launch.h).
 constexpr int kPoleBlock = 128;
-constexpr int kPoleTile = 32;
+#ifndef REXI_POLE_TILE
+#define REXI_POLE_TILE 32
+#endif
+constexpr int kPoleTile = REXI_POLE_TILE;
 
 struct ModeState {
     cd e0, B0, m0, ua, vb;   // f0 = (e0, ua, vb); B0 = h mu e0 + delta0; m0 = zeta0 - c e0

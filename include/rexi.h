@@ -137,6 +137,12 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
 rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter,
                                    int min_blocks_per_sm);
 
+/* Whole-step CUDA graphs (default on): rexi_apply / rexi_apply_partial / rexi_apply_host /
+ * rexi_run capture their kernel sequence once per (buffers, pole range, method, variant,
+ * tuning, timing) on a private stream and replay it on `stream` afterwards (up to 8 cached
+ * graphs per plan, least recently used evicted). Results are identical either way. */
+rexi_status_t rexi_plan_set_graphs(rexi_plan_t plan, int enable);
+
 /* Copy the plan's term table to HOST arrays of n_poles entries each (any may be NULL):
  *   alpha[2n], C1[2n], C2[2n] (interleaved re, im) and gamma[n], for n = 0..N:
  *   alpha_n = h(mu + i n), C1_n = c1_n h mu + c2_n h n, C2_n = i c2_n

@@ -77,9 +77,39 @@ struct rexi_plan_s {
     size_t ev_used = 0;
     long launches = 0;
     long pole_launches = 0;
+    // CUDA-graph cache of whole steps (S1..S5 for a pole range and fixed buffers)
+    struct GraphEntry {
+        const void *key[6];
+        long b, e;
+        int kind, mpt, pu, minb;
+        bool timing;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t ev_node[2] = {nullptr, nullptr};
+        long n_launches = 0, n_pole = 0;
+        unsigned long long last_use = 0;
+    };
+    bool use_graphs = true;
+    bool capturing = false;
+    cudaStream_t cap_stream = nullptr;
+    cudaEvent_t ev_cap[2] = {nullptr, nullptr};
+    std::vector<GraphEntry> graphs;
+    unsigned long long graph_clock = 0;
+
+    void clear_graphs() {
+        for (GraphEntry &g : graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
+        graphs.clear();
+    }
 
     ~rexi_plan_s() {
         DeviceGuard g(device);
+        clear_graphs();
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+        for (cudaEvent_t e : ev_cap)
+            if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
                         (void *)d_tmp, (void *)d_partial, (void *)d_stage})
             if (p) cudaFree(p);
@@ -121,15 +151,29 @@ int choose_chunks(const rexi_plan_s *p, long n_range) {
     return best;
 }
 
-rexi_status_t record(rexi_plan_s *p, cudaStream_t st, bool start) {
-    if (!p->timing) return REXI_OK;
+rexi_status_t next_event(rexi_plan_s *p, cudaEvent_t *out) {
     if (p->ev_used >= p->ev.size()) {
         cudaEvent_t e;
         CK(cudaEventCreate(&e));
         p->ev.push_back(e);
     }
-    (void)start;
-    CK(cudaEventRecord(p->ev[p->ev_used++], st));
+    *out = p->ev[p->ev_used++];
+    return REXI_OK;
+}
+
+// Bracket the pole kernel with timing events (start = true before, false after). While a step
+// is being captured into a graph, two placeholder events become event-record nodes that each
+// replay re-targets to fresh events from the pool.
+rexi_status_t record(rexi_plan_s *p, cudaStream_t st, bool start) {
+    if (!p->timing) return REXI_OK;
+    if (p->capturing) {
+        CK(cudaEventRecord(p->ev_cap[start ? 0 : 1], st));
+        return REXI_OK;
+    }
+    cudaEvent_t e;
+    rexi_status_t s = next_event(p, &e);
+    if (s != REXI_OK) return s;
+    CK(cudaEventRecord(e, st));
     return REXI_OK;
 }
 
@@ -234,6 +278,108 @@ rexi_status_t guarded(rexi_plan_t p, F &&f) {
     } catch (...) {
         return fail(REXI_EINVAL, "unexpected exception");
     }
+}
+
+rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
+                             const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+    rexi_status_t s;
+    if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
+    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+    return do_inverse(p, p->d_acc, eo, uo, vo, st);
+}
+
+// One step through a cached CUDA graph (captured on the plan's private stream the first time
+// these buffers / pole range / tuning are seen; replayed on the caller's stream afterwards).
+rexi_status_t do_step_graph(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
+                            const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+    const void *key[6] = {eta, u, v, eo, uo, vo};
+    const int kd = p->kind();
+    rexi_plan_s::GraphEntry *hit = nullptr;
+    for (auto &g : p->graphs)
+        if (std::equal(key, key + 6, g.key) && g.b == b && g.e == e && g.kind == kd &&
+            g.mpt == p->mpt[kd] && g.pu == p->pu[kd] && g.minb == p->minb[kd] && g.timing == p->timing)
+            hit = &g;
+    if (!hit) {
+        if (!p->cap_stream) {
+            CK(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&p->ev_cap[0], cudaEventDefault));
+            CK(cudaEventCreateWithFlags(&p->ev_cap[1], cudaEventDefault));
+        }
+        if (p->graphs.size() >= 8) {  // evict the least recently used entry
+            auto it = std::min_element(p->graphs.begin(), p->graphs.end(),
+                                       [](const auto &x, const auto &y) { return x.last_use < y.last_use; });
+            if (it->exec) cudaGraphExecDestroy(it->exec);
+            if (it->graph) cudaGraphDestroy(it->graph);
+            p->graphs.erase(it);
+        }
+        rexi_plan_s::GraphEntry g;
+        std::copy(key, key + 6, g.key);
+        g.b = b;
+        g.e = e;
+        g.kind = kd;
+        g.mpt = p->mpt[kd];
+        g.pu = p->pu[kd];
+        g.minb = p->minb[kd];
+        g.timing = p->timing;
+        const long l0 = p->launches, pl0 = p->pole_launches;
+        CK(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+        p->capturing = true;
+        rexi_status_t s = do_step_direct(p, b, e, eta, u, v, eo, uo, vo, p->cap_stream);
+        p->capturing = false;
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
+        if (s != REXI_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return s;
+        }
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        g.n_launches = p->launches - l0;
+        g.n_pole = p->pole_launches - pl0;
+        p->launches = l0;
+        p->pole_launches = pl0;
+        g.graph = graph;
+        ce = cudaGraphInstantiate(&g.exec, graph, 0);
+        if (ce != cudaSuccess) {
+            cudaGraphDestroy(graph);
+            return cuda_fail(ce, "cudaGraphInstantiate");
+        }
+        if (g.timing) {
+            size_t nn = 0;
+            CK(cudaGraphGetNodes(graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                CK(cudaGraphNodeGetType(nd, &t));
+                if (t != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t ev;
+                CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+                for (int i = 0; i < 2; ++i)
+                    if (ev == p->ev_cap[i]) g.ev_node[i] = nd;
+            }
+        }
+        p->graphs.push_back(g);
+        hit = &p->graphs.back();
+    }
+    hit->last_use = ++p->graph_clock;
+    if (hit->timing && hit->ev_node[0] && hit->ev_node[1]) {
+        cudaEvent_t e0, e1;
+        rexi_status_t s;
+        if ((s = next_event(p, &e0)) != REXI_OK) return s;
+        if ((s = next_event(p, &e1)) != REXI_OK) return s;
+        CK(cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[0], e0));
+        CK(cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[1], e1));
+    }
+    CK(cudaGraphLaunch(hit->exec, st));
+    p->launches += hit->n_launches;
+    p->pole_launches += hit->n_pole;
+    return REXI_OK;
+}
+
+rexi_status_t do_step(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
+                      const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+    if (p->use_graphs) return do_step_graph(p, b, e, eta, u, v, eo, uo, vo, st);
+    return do_step_direct(p, b, e, eta, u, v, eo, uo, vo, st);
 }
 
 }  // namespace
@@ -436,10 +582,15 @@ rexi_status_t rexi_apply_partial(rexi_plan_t p, long b, long e, const double *et
         if (!eta || !u || !v || !eo || !uo || !vo) return fail(REXI_EINVAL, "null pointer");
         rexi_status_t s = check_range(p, b, e);
         if (s != REXI_OK) return s;
-        cudaStream_t st = (cudaStream_t)stream;
-        if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
-        if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
-        return do_inverse(p, p->d_acc, eo, uo, vo, st);
+        return do_step(p, b, e, eta, u, v, eo, uo, vo, (cudaStream_t)stream);
+    });
+}
+
+rexi_status_t rexi_plan_set_graphs(rexi_plan_t p, int enable) {
+    return guarded(p, [&]() -> rexi_status_t {
+        p->use_graphs = enable != 0;
+        if (!p->use_graphs) p->clear_graphs();
+        return REXI_OK;
     });
 }
 
@@ -470,9 +621,8 @@ rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u,
         for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(d[i], hin[i], n * sizeof(double), cudaMemcpyHostToDevice, st));
         rexi_status_t s;
-        if ((s = do_forward(p, d[0], d[1], d[2], p->d_fhat, st)) != REXI_OK) return s;
-        if ((s = do_poles(p, 0, p->host.n_poles, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
-        if ((s = do_inverse(p, p->d_acc, d[3], d[4], d[5], st)) != REXI_OK) return s;
+        if ((s = do_step(p, 0, p->host.n_poles, d[0], d[1], d[2], d[3], d[4], d[5], st)) != REXI_OK)
+            return s;
         for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));

@@ -47,6 +47,7 @@ EXPORTS = {
     "rexi_plan_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "rexi_plan_set_variant": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_method": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_plan_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -174,6 +175,9 @@ class Plan:
         v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
         _check(_lib.rexi_plan_set_variant(self._h, v), "rexi_plan_set_variant")
         self.variant = v
+
+    def set_graphs(self, enable):
+        _check(_lib.rexi_plan_set_graphs(self._h, int(bool(enable))), "rexi_plan_set_graphs")
 
     def set_method(self, method):
         m = METHODS[method] if isinstance(method, str) else int(method)

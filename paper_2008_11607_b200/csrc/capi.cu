@@ -167,7 +167,7 @@ rexi_status_t next_event(rexi_plan_s *p, cudaEvent_t *out) {
 rexi_status_t record(rexi_plan_s *p, cudaStream_t st, bool start) {
     if (!p->timing) return REXI_OK;
     if (p->capturing) {
-        CK(cudaEventRecord(p->ev_cap[start ? 0 : 1], st));
+        CK(cudaEventRecordWithFlags(p->ev_cap[start ? 0 : 1], st, cudaEventRecordExternal));
         return REXI_OK;
     }
     cudaEvent_t e;

@@ -186,7 +186,10 @@ rexi_status_t rexi_apply_host(rexi_plan_t plan, const double *eta, const double 
                               const double *v, double *eta_out, double *u_out, double *v_out,
                               void *stream);
 
-/* S6: `steps` successive REXII steps in place on device fields (T_final = steps * tau). */
+/* S6: `steps` successive steps in place on device fields (T_final = steps * tau). For
+ * steps >= 2 the state stays in Fourier space between steps (NEXT-4): one forward FFT, then per
+ * step the pole sum and the spectral form of the real part, (X(K) + conj(X(-K)))/2 — the same
+ * operator as Re(IDFT(.)) followed by DFT, without the FFT round trip — and one inverse FFT. */
 rexi_status_t rexi_run(rexi_plan_t plan, int steps, double *eta, double *u, double *v,
                        void *stream);
 

@@ -80,6 +80,7 @@ struct rexi_plan_s {
     // CUDA-graph cache of whole steps (S1..S5 for a pole range and fixed buffers)
     struct GraphEntry {
         const void *key[6];
+        int mode;               // 0: physical step S1..S5, 1: spectral step (S2, S3, Re projection)
         long b, e;
         int kind, mpt, pu, minb;
         bool timing;
@@ -288,15 +289,26 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
     return do_inverse(p, p->d_acc, eo, uo, vo, st);
 }
 
+// One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
+rexi_status_t do_spectral_step_direct(rexi_plan_s *p, long b, long e, cudaStream_t st) {
+    rexi_status_t s;
+    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+    CK(rexi::launch_hermitian(p->d_acc, p->d_fhat, p->n_modes, p->host.D, st));
+    p->launches += 1;
+    return REXI_OK;
+}
+
 // One step through a cached CUDA graph (captured on the plan's private stream the first time
 // these buffers / pole range / tuning are seen; replayed on the caller's stream afterwards).
-rexi_status_t do_step_graph(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
-                            const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+// mode 0: physical step (S1..S5) on the given fields; mode 1: spectral step on plan buffers.
+rexi_status_t do_step_graph(rexi_plan_s *p, int mode, long b, long e, const double *eta,
+                            const double *u, const double *v, double *eo, double *uo, double *vo,
+                            cudaStream_t st) {
     const void *key[6] = {eta, u, v, eo, uo, vo};
     const int kd = p->kind();
     rexi_plan_s::GraphEntry *hit = nullptr;
     for (auto &g : p->graphs)
-        if (std::equal(key, key + 6, g.key) && g.b == b && g.e == e && g.kind == kd &&
+        if (g.mode == mode && std::equal(key, key + 6, g.key) && g.b == b && g.e == e && g.kind == kd &&
             g.mpt == p->mpt[kd] && g.pu == p->pu[kd] && g.minb == p->minb[kd] && g.timing == p->timing)
             hit = &g;
     if (!hit) {
@@ -314,6 +326,7 @@ rexi_status_t do_step_graph(rexi_plan_s *p, long b, long e, const double *eta, c
         }
         rexi_plan_s::GraphEntry g;
         std::copy(key, key + 6, g.key);
+        g.mode = mode;
         g.b = b;
         g.e = e;
         g.kind = kd;
@@ -324,7 +337,8 @@ rexi_status_t do_step_graph(rexi_plan_s *p, long b, long e, const double *eta, c
         const long l0 = p->launches, pl0 = p->pole_launches;
         CK(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
         p->capturing = true;
-        rexi_status_t s = do_step_direct(p, b, e, eta, u, v, eo, uo, vo, p->cap_stream);
+        rexi_status_t s = mode == 0 ? do_step_direct(p, b, e, eta, u, v, eo, uo, vo, p->cap_stream)
+                                    : do_spectral_step_direct(p, b, e, p->cap_stream);
         p->capturing = false;
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
@@ -378,8 +392,13 @@ rexi_status_t do_step_graph(rexi_plan_s *p, long b, long e, const double *eta, c
 
 rexi_status_t do_step(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
                       const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
-    if (p->use_graphs) return do_step_graph(p, b, e, eta, u, v, eo, uo, vo, st);
+    if (p->use_graphs) return do_step_graph(p, 0, b, e, eta, u, v, eo, uo, vo, st);
     return do_step_direct(p, b, e, eta, u, v, eo, uo, vo, st);
+}
+
+rexi_status_t do_spectral_step(rexi_plan_s *p, long b, long e, cudaStream_t st) {
+    if (p->use_graphs) return do_step_graph(p, 1, b, e, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    return do_spectral_step_direct(p, b, e, st);
 }
 
 }  // namespace
@@ -631,19 +650,33 @@ rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u,
 }
 
 rexi_status_t rexi_run(rexi_plan_t p, int steps, double *eta, double *u, double *v, void *stream) {
-    if (!p) return fail(REXI_EINVAL, "null plan");
-    if (steps < 0) return fail(REXI_EINVAL, "steps must be >= 0");
-    for (int s = 0; s < steps; ++s) {
-        rexi_status_t r = rexi_apply(p, eta, u, v, eta, u, v, stream);
-        if (r != REXI_OK) return r;
-    }
-    return REXI_OK;
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!eta || !u || !v) return fail(REXI_EINVAL, "null pointer");
+        if (steps < 0) return fail(REXI_EINVAL, "steps must be >= 0");
+        if (steps == 0) return REXI_OK;
+        cudaStream_t st = (cudaStream_t)stream;
+        const long N1 = p->host.n_poles;
+        if (steps == 1) return do_step(p, 0, N1, eta, u, v, eta, u, v, st);
+        // spectral-resident: forward once, (poles + Re projection) per step, inverse once
+        rexi_status_t s;
+        if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
+        for (int k = 0; k < steps; ++k)
+            if ((s = do_spectral_step(p, 0, N1, st)) != REXI_OK) return s;
+        return do_inverse(p, p->d_fhat, eta, u, v, st);
+    });
 }
 
 rexi_status_t rexi_timing_enable(rexi_plan_t p, int enable) {
-    if (!p) return fail(REXI_EINVAL, "null plan");
-    p->timing = enable != 0;
-    return REXI_OK;
+    return guarded(p, [&]() -> rexi_status_t {
+        p->timing = enable != 0;
+        // pre-create events so that no cudaEventCreate happens inside a timed region
+        while (p->timing && p->ev.size() < 2048) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            p->ev.push_back(e);
+        }
+        return REXI_OK;
+    });
 }
 
 rexi_status_t rexi_timing_read(rexi_plan_t p, double *ms, long *pole_launches, long *total_launches) {

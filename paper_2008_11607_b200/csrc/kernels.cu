@@ -523,6 +523,24 @@ __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
     }
 }
 
+// ============================================================================= Re projection
+// Spectral form of "take the real part in physical space": for a spectrum X of
+// a complex field, Re(IDFT(X)) = IDFT(H X) with (H X)(k, l) = (X(k, l) + conj(X(-k, -l))) / 2
+// (indices mod D; the Nyquist index is its own mirror). Used between the steps of a
+// spectral-resident multi-step run (S6) instead of an inverse + forward FFT round trip.
+__global__ void __launch_bounds__(256) hermitian_kernel(const cd *__restrict__ in, cd *__restrict__ out,
+                                                        long n_modes, int D, int log2D) {
+    const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= n_modes) return;
+    const int l = (int)(m >> log2D), k = (int)(m & (D - 1));
+    const long mm = ((long)((D - l) & (D - 1)) << log2D) + ((D - k) & (D - 1));
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        const cd x = in[f * n_modes + m], y = in[f * n_modes + mm];
+        out[f * n_modes + m] = mk(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+    }
+}
+
 // ============================================================================= launchers
 static int ilog2(int x) {
     int r = 0;
@@ -648,6 +666,11 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st) {
     const long blocks = (a.n_modes + 255) / 256;
     finish_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st) {
+    hermitian_kernel<<<(unsigned)((n_modes + 255) / 256), 256, 0, st>>>(in, out, n_modes, D, ilog2(D));
     return cudaGetLastError();
 }
 

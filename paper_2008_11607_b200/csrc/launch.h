@@ -18,6 +18,7 @@ cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_p
 cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
+cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:
 // flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each).

@@ -406,3 +406,23 @@ def test_graphs_match_direct_and_timing(R):
     c = [host(t) for t in p.apply_partial(0, 100, *f)]
     d = [host(t) for t in p.apply_partial(100, p.n_poles, *f)]
     assert rel_l2([x + y for x, y in zip(c, d)], a) < 1e-14
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_run_spectral_resident_matches_repeated_apply(R, graphs):
+    """NEXT-4: rexi_run keeps the state in Fourier space between steps (Re projection done
+    spectrally); it matches repeated physical steps to rounding."""
+    D, tau, K = 64, 0.3, 5
+    f = inputs.white_noise(D)
+    p = R.Plan(D, tau)
+    p.set_graphs(graphs)
+    t = [dev(x) for x in f]
+    p.run(K, *t)
+    q = [dev(x) for x in f]
+    for _ in range(K):
+        q = list(p.apply(*q))
+    assert rel_l2([host(x) for x in t], [host(x) for x in q]) < 1e-13
+    # energy after K steps (A skew-symmetric): conserved to tolerance
+    e0 = sum(float((x ** 2).sum()) for x in f)
+    e1 = sum(float((host(x) ** 2).sum()) for x in t)
+    assert abs(e1 - e0) / e0 < 1e-11

@@ -62,14 +62,17 @@ typedef enum {
 } rexi_status_t;
 
 /* Per-pole solve formulation of the fused pole kernel.
- * Both solve the same two shifted systems per mode and pole, Helmholtz-reduced
+ * All solve the same two shifted systems per mode and pole, Helmholtz-reduced
  * (eq:lswEta), and accumulate in registers.
- *  REXI_VARIANT_DZ: back-substitution in divergence/vorticity variables
- *                   (delta, zeta of PAPER.md:493-496); velocities recovered once
- *                   per mode from the accumulated sums (default; fewer fp64 ops).
- *  REXI_VARIANT_UV: paper-literal back-substitution of (u, v) per pole with
- *                   eq:lswVelocities. */
-typedef enum { REXI_VARIANT_DZ = 0, REXI_VARIANT_UV = 1 } rexi_variant_t;
+ *  REXI_VARIANT_DZ:  back-substitution in divergence/vorticity variables (delta, zeta of
+ *                    PAPER.md:493-496); the eta and delta pole sums are accumulated, the zeta
+ *                    pole sum is rebuilt exactly from the eta sum (zeta of each solve is affine
+ *                    in its eta: potential vorticity), velocities recovered once per mode
+ *                    (default; fewest fp64 ops).
+ *  REXI_VARIANT_UV:  paper-literal back-substitution of (u, v) per pole with
+ *                    eq:lswVelocities.
+ *  REXI_VARIANT_DZ3: as DZ but all three (eta, delta, zeta) pole sums accumulated. */
+typedef enum { REXI_VARIANT_DZ = 0, REXI_VARIANT_UV = 1, REXI_VARIANT_DZ3 = 2 } rexi_variant_t;
 
 /* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
  *  REXI_METHOD_REXII: the paper's REXII, two solves per term (eq:REXI_Modified_matrix,
@@ -126,9 +129,10 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
 
 /* Pole-kernel tuning for the plan's CURRENT variant: Fourier modes per thread, poles per loop
  * trip and resident blocks per SM requested of the compiler (register budget). Supported:
- *   REXII DZ: (1,1,8) (2,1,4) (2,1,5) (2,2,3) (3,1,3) (3,1,4) (4,1,2) (4,1,3) (4,1,4)  default (4,1,4)
- *   REXII UV: (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)                          default (4,1,3)
- *   REXI:     (1,1,8) (2,1,4) (4,1,3) (4,1,4)                                          default (4,1,4)
+ *   REXII DZ:  (1,1,8) (2,1,4) (2,1,5) (3,1,4) (4,1,3) (4,1,4)         default (4,1,4)
+ *   REXII UV:  (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)         default (4,1,3)
+ *   REXII DZ3: (1,1,8) (2,1,4) (3,1,4) (4,1,2) (4,1,4)                 default (4,1,4)
+ *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).
  * Per pole and mode the operation order is the same for every tuning; the number of pole

@@ -56,9 +56,13 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[3] = {4, 4, 4}, pu[3] = {1, 1, 1}, minb[3] = {4, 3, 4};
-    int occ_cache[3] = {0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
-    int kind() const { return method == REXI_METHOD_REXI ? 2 : variant; }
+    int mpt[4] = {4, 4, 4, 4}, pu[4] = {1, 1, 1, 1}, minb[4] = {4, 3, 4, 4};
+    int occ_cache[4] = {0, 0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
+    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3
+    int kind() const {
+        if (method == REXI_METHOD_REXI) return 2;
+        return variant == REXI_VARIANT_UV ? 1 : variant == REXI_VARIANT_DZ3 ? 3 : 0;
+    }
     long n_modes = 0;
     int num_sms = 0;
     int max_chunks = 1;
@@ -241,7 +245,14 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     f.n_chunks = chunks;
     f.D = a.D;
     f.log2D = a.log2D;
-    f.variant = kd;
+    f.kind = kd;
+    f.fhat = fhat;
+    f.tau = p->host.tau;
+    {
+        const long double sr = p->host.spre_re[(size_t)e] - p->host.spre_re[(size_t)b];
+        const long double si = p->host.spre_im[(size_t)e] - p->host.spre_im[(size_t)b];
+        f.S = cd{(double)sr, (double)si};
+    }
     CK(rexi::launch_finish(f, st));
     p->launches += 2;
     if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
@@ -520,7 +531,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
 
 rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (variant != REXI_VARIANT_DZ && variant != REXI_VARIANT_UV) return fail(REXI_EINVAL, "unknown variant");
+    if (variant != REXI_VARIANT_DZ && variant != REXI_VARIANT_UV && variant != REXI_VARIANT_DZ3)
+        return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
     return REXI_OK;
 }

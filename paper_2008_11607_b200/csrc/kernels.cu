@@ -263,14 +263,13 @@ __device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, co
     const cd num = cfms(s2, s.m0, t);
     const cd eta1 = cmul(num, qd);
     if (VARIANT == 2) {
-        // original REXI (eq:originalREXImatrix): one solve per term, acc += Gamma beta^Re g1
-        const cd ia = mk(P.iar, P.iai);
+        // original REXI (eq:originalREXImatrix): one solve per term, acc += Gamma beta^Re g1.
+        // zeta1 = m0/alpha + c eta1 is affine in eta1 (potential vorticity, see finish_kernel):
+        // its pole sum is rebuilt there, so only (eta, delta) are accumulated.
         const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
-        const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
         s.A0 = cfma(w1, eta1, s.A0);
         s.A1 = cfma(w1, del1, s.A1);
-        s.A2 = cfma(w1, zet1, s.A2);
-    } else if (VARIANT == 0) {
+    } else if (VARIANT == 0 || VARIANT == 3) {
         const cd ia = mk(P.iar, P.iai);
         const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
         const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
@@ -279,11 +278,15 @@ __device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, co
         num2 = cjfms(s2, zet1, num2);                            // - conj(c/alpha) zeta1
         const cd eta2 = cjfma(qd, num2, mk(0, 0));               // num2 * conj(q)
         const cd del2 = cjfms(al, eta2, eta1);                   // eta1 - conj(alpha) eta2
-        const cd zet2 = mk(fma(P.ia2, s.m0.x, c * eta2.x), fma(P.ia2, s.m0.y, c * eta2.y));
         // ---- accumulate w1 g1 + w2 g2
         s.A0 = cfma(w2, eta2, cfma(w1, eta1, s.A0));
         s.A1 = cfma(w2, del2, cfma(w1, del1, s.A1));
-        s.A2 = cfma(w2, zet2, cfma(w1, zet1, s.A2));
+        if (VARIANT == 3) {
+            // zeta2 = (zeta1 - c delta2)/conj(alpha) = |1/alpha|^2 m0 + c eta2; DZ (kind 0)
+            // rebuilds the zeta pole sum from the eta pole sum instead (finish_kernel)
+            const cd zet2 = mk(fma(P.ia2, s.m0.x, c * eta2.x), fma(P.ia2, s.m0.y, c * eta2.y));
+            s.A2 = cfma(w2, zet2, cfma(w1, zet1, s.A2));
+        }
     } else {
         const cd s3 = mk(P.s3r, P.s3i), s4 = mk(P.s4r, P.s4i);
         const double kx = s.Kx, ky = s.Ky;
@@ -440,27 +443,45 @@ pole_kernel(PoleArgs a) {
             const long m = mode[j];
             out[m] = st[j].A0;
             out[n_modes + m] = st[j].A1;
-            out[2 * n_modes + m] = st[j].A2;
+            if (VARIANT == 1 || VARIANT == 3) out[2 * n_modes + m] = st[j].A2;
         }
     }
 }
 
 // ============================================================================= finish
+// Sums the chunk partials in a fixed order. Kinds 0 and 2 accumulate only (eta, delta): the
+// zeta component of every solve is affine in its eta component (the third equation,
+// -c delta + alpha zeta = zeta0 with delta = alpha eta - eta0: zeta = (zeta0 - c eta0)/alpha + c eta,
+// i.e. potential vorticity zeta - c eta is carried by m0 = zeta0 - c eta0), so
+//   A_zeta = S m0 + c A_eta,  S = sum_n (w1_n / alpha_n + w2_n / |alpha_n|^2)   (exact),
+// with S summed on the host in extended precision for the pole range. Then, for the DZ kinds,
+// (u, v) are recovered from (delta, zeta).
 __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long n = a.n_modes;
     if (m >= n) return;
+    const bool pv = (a.kind == 0 || a.kind == 2);
     cd s0 = mk(0, 0), s1 = mk(0, 0), s2 = mk(0, 0);
     for (int c = 0; c < a.n_chunks; ++c) {  // fixed order: deterministic
         const cd *p = a.partial + (size_t)c * 3 * n;
-        const cd x0 = p[m], x1 = p[n + m], x2 = p[2 * n + m];
+        const cd x0 = p[m], x1 = p[n + m];
         s0 = mk(s0.x + x0.x, s0.y + x0.y);
         s1 = mk(s1.x + x1.x, s1.y + x1.y);
-        s2 = mk(s2.x + x2.x, s2.y + x2.y);
+        if (!pv) {
+            const cd x2 = p[2 * n + m];
+            s2 = mk(s2.x + x2.x, s2.y + x2.y);
+        }
     }
-    if (a.variant != 1) {   // DZ accumulators (REXII-DZ and REXI): (delta, zeta) -> (u, v)
+    if (a.kind != 1) {   // DZ accumulators: (delta, zeta) -> (u, v)
         const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
         const double kx = a.ksym[k], ky = a.ksym[l];
+        if (pv) {
+            const cd e = a.fhat[m], uu = a.fhat[n + m], vv = a.fhat[2 * n + m];
+            const double c = a.tau;
+            // m0 = zeta0 - c eta0, zeta0 = i (kx v - ky u)
+            const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
+            s2 = cfma(a.S, m0, mk(c * s0.x, c * s0.y));
+        }
         const double K2 = fma(kx, kx, ky * ky);
         if (K2 > 0.0) {
             // delta = i(kx u + ky v), zeta = i(kx v - ky u)
@@ -622,12 +643,13 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
 }
 
 // Supported (variant, modes per thread, poles per loop trip, min blocks per SM) instantiations.
-// Kernel kinds: 0 = REXII DZ, 1 = REXII UV, 2 = REXI (DZ back-substitution).
+// Kernel kinds: 0 = REXII DZ (eta, delta accumulated; zeta rebuilt), 1 = REXII UV,
+// 2 = REXI (DZ back-substitution, zeta rebuilt), 3 = REXII DZ3 (all three accumulated).
 #define REXI_POLE_CONFIGS(X)                                                             \
-    X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 2, 2, 3) X(0, 3, 1, 3) X(0, 3, 1, 4)  \
-    X(0, 4, 1, 2) X(0, 4, 1, 3) X(0, 4, 1, 4)                                             \
+    X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 3, 1, 4) X(0, 4, 1, 3) X(0, 4, 1, 4)  \
     X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)  \
-    X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 3)
+    X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 5)                               \
+    X(3, 1, 1, 8) X(3, 2, 1, 4) X(3, 3, 1, 4) X(3, 4, 1, 2) X(3, 4, 1, 4)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 

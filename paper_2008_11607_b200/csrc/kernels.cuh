@@ -74,11 +74,14 @@ struct PoleArgs {
 struct FinishArgs {
     const cd *partial;     // [n_chunks][3][D*D]
     cd *acc;               // [3][D*D]
+    const cd *fhat;        // [3][D*D] (kinds 0, 2: for m0 = zeta0 - c eta0)
     const double *ksym;
     long n_modes;
     int n_chunks;
     int D, log2D;
-    int variant;
+    int kind;              // pole-kernel kind (0 DZ, 1 UV, 2 REXI, 3 DZ3)
+    double tau;
+    cd S;                  // kinds 0, 2: sum over the pole range of w1/alpha + w2/|alpha|^2
 };
 
 struct FixupArgs {

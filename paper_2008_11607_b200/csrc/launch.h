@@ -21,21 +21,21 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:
-// flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each).
+// flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each), by kind.
+//   kind 3 (DZ3, all three accumulated): 71 ops / 131 flops (DESIGN.md 6.1 table)
+//   kind 0 (DZ): kind 3 without zeta2 (4/6) and the two zeta MACs (8/16): 59 / 109
+//   kind 1 (UV, paper-literal): 101 / 183
+//   kind 2 (REXI): solve 1 without zeta1 (num 6/12, den 7/11, eta1 4/6, delta1 4/8) + 2 MACs 8/16
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
-// by four modes. DESIGN.md "Pole kernel" lists the count line by line.
-constexpr double kFlopsDZ = 131.0, kOpsDZ = 71.0;
-constexpr double kFlopsUV = 183.0, kOpsUV = 101.0;
+// by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
-// REXI (kind 2): solve 1 (num 6/12, den 7/11, eta1 4/6, delta1 4/8, zeta1 6/10) + 3 MACs 12/24.
-constexpr double kFlopsREXI = 71.0, kOpsREXI = 39.0;
 inline double pole_flops(int kind, int mpt) {
-    const double f = kind == 0 ? kFlopsDZ : kind == 1 ? kFlopsUV : kFlopsREXI;
-    return mpt == 4 ? f - kDenFlops * 0.75 : f;
+    const double f[4] = {109.0, 183.0, 53.0, 131.0};
+    return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt) {
-    const double f = kind == 0 ? kOpsDZ : kind == 1 ? kOpsUV : kOpsREXI;
-    return mpt == 4 ? f - kDenOps * 0.75 : f;
+    const double f[4] = {59.0, 101.0, 29.0, 71.0};
+    return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }
 
 }  // namespace rexi

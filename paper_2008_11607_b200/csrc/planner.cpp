@@ -14,6 +14,7 @@ namespace rexi {
 
 using ld = long double;
 using cld = std::complex<long double>;
+using cd_pv_t = cld;
 
 // Appendix A, PAPER.md:815-851 (tab:coef_al), L = 24. Reading G1: the printed sign
 // column is the sign of the real part. a_{-l} = conj(a_l).
@@ -124,6 +125,8 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     p.C2.assign(2 * (size_t)p.n_poles, 0.0);
     p.gamma.assign((size_t)p.n_poles, 0.0);
     p.poles.assign((size_t)p.n_poles, PoleConst{});
+    p.spre_re.assign((size_t)p.n_poles + 1, 0.0L);
+    p.spre_im.assign((size_t)p.n_poles + 1, 0.0L);
     const ld c = (ld)tau;  // tau-scaled Coriolis coefficient (reading G3)
     for (long n = 0; n <= N; ++n) {
         // c_{1,n} = h sum_{k=L1}^{L2} Re(a_k) b_{n-k},  c_{2,n} = h sum Im(a_k) b_{n-k}
@@ -167,6 +170,11 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         }
         cld s2 = c / alpha, ia = 1.0L / alpha, s1c = std::conj(kappa / alpha);
         cld s3 = alpha / kappa, s4 = c / kappa;
+        {
+            const cd_pv_t sv = w1 * ia + w2 * std::norm(ia);
+            p.spre_re[(size_t)n + 1] = p.spre_re[(size_t)n] + sv.real();
+            p.spre_im[(size_t)n + 1] = p.spre_im[(size_t)n] + sv.imag();
+        }
         PoleConst &q = p.poles[(size_t)n];
         q.ar = (double)alpha.real();  q.ai = (double)alpha.imag();
         q.s2r = (double)s2.real();    q.s2i = (double)s2.imag();

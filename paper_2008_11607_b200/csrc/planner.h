@@ -35,6 +35,9 @@ struct Plan {
     // term table, n = 0..N (interleaved re/im for complex entries)
     std::vector<double> alpha, C1, C2, gamma;   // REXI plans: C1 = beta^Re_n, C2 = 0
     std::vector<PoleConst> poles;
+    // prefix sums (extended precision) of w1_n / alpha_n + w2_n / |alpha_n|^2, n = 0..N:
+    // S(b, e) = pre[e] - pre[b] rebuilds the zeta pole sum from the eta pole sum (finish_kernel)
+    std::vector<long double> spre_re, spre_im;
     std::vector<double> ksym;        // D tau-scaled derivative symbols, Nyquist zeroed (G2)
     std::vector<double> twiddle;     // D complex e^{-2 pi i j / D}
 };

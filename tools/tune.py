@@ -13,10 +13,10 @@ D, tau, tol = {"c1": (64, 0.02, 1e-12), "c2": (512, 1.0, 1e-8), "c3": (1024, 0.1
                "c4": (4096, 1.0, 1e-12)}[cfg]
 f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
 res = []
-TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (2, 2, 3), (3, 1, 3), (3, 1, 4), (4, 1, 2),
-                  (4, 1, 3), (4, 1, 4)],
-           "uv": [(1, 1, 6), (2, 1, 3), (2, 1, 4), (3, 1, 3), (4, 1, 2), (4, 1, 3)]}
-for variant in ("dz", "uv"):
+TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (3, 1, 4), (4, 1, 3), (4, 1, 4)],
+           "uv": [(1, 1, 6), (2, 1, 3), (2, 1, 4), (3, 1, 3), (4, 1, 2), (4, 1, 3)],
+           "dz3": [(1, 1, 8), (2, 1, 4), (3, 1, 4), (4, 1, 2), (4, 1, 4)]}
+for variant in ("dz", "uv", "dz3"):
     for mpt, pu, minb in TUNINGS[variant]:
         p = rexi.Plan(D, tau, tol=tol, variant=variant)
         p.set_tuning(mpt, pu, minb)

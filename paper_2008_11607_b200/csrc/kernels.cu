@@ -243,6 +243,11 @@ struct ModeState {
     cd A0, A1, A2;           // accumulators: (eta, delta, zeta) [DZ] or (eta, u, v) [UV]
 };
 
+template <int VARIANT>
+__device__ __forceinline__ void pole_solves_in(const PoleConst &P, ModeState &s, const cd e0in,
+                                               const cd B0in, const cd m0in, const cd qd,
+                                               const double c);
+
 // 1/(kappa_n + K2) for one pole and one value of K2 (shared by every mode with that K2).
 __device__ __forceinline__ cd pole_den(const PoleConst &P, const double K2) {
     const double dr = P.kr + K2;
@@ -255,24 +260,31 @@ __device__ __forceinline__ cd pole_den(const PoleConst &P, const double K2) {
 template <int VARIANT>
 __device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, const cd qd,
                                             const double c) {
+    pole_solves_in<VARIANT>(P, s, s.e0, s.B0, s.m0, qd, c);
+}
+
+template <int VARIANT>
+__device__ __forceinline__ void pole_solves_in(const PoleConst &P, ModeState &s, const cd e0in,
+                                               const cd B0in, const cd m0in, const cd qd,
+                                               const double c) {
     const cd al = mk(P.ar, P.ai), s2 = mk(P.s2r, P.s2i), s1c = mk(P.s1cr, P.s1ci);
     const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
     const double hn = P.ai;
     // ---- solve 1: Helmholtz for eta1 (eq:lswEta)
-    const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));
-    const cd num = cfms(s2, s.m0, t);
+    const cd t = mk(fma(-hn, e0in.y, B0in.x), fma(hn, e0in.x, B0in.y));
+    const cd num = cfms(s2, m0in, t);
     const cd eta1 = cmul(num, qd);
     if (VARIANT == 2) {
         // original REXI (eq:originalREXImatrix): one solve per term, acc += Gamma beta^Re g1.
         // zeta1 = m0/alpha + c eta1 is affine in eta1 (potential vorticity, see finish_kernel):
         // its pole sum is rebuilt there, so only (eta, delta) are accumulated.
-        const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
+        const cd del1 = cfma(al, eta1, mk(-e0in.x, -e0in.y));
         s.A0 = cfma(w1, eta1, s.A0);
         s.A1 = cfma(w1, del1, s.A1);
     } else if (VARIANT == 0 || VARIANT == 3) {
         const cd ia = mk(P.iar, P.iai);
-        const cd del1 = cfma(al, eta1, mk(-s.e0.x, -s.e0.y));
-        const cd zet1 = cfma(ia, s.m0, mk(c * eta1.x, c * eta1.y));
+        const cd del1 = cfma(al, eta1, mk(-e0in.x, -e0in.y));
+        const cd zet1 = cfma(ia, m0in, mk(c * eta1.x, c * eta1.y));
         // ---- solve 2
         cd num2 = cfma(s1c, eta1, mk(-del1.x, -del1.y));
         num2 = cjfms(s2, zet1, num2);                            // - conj(c/alpha) zeta1
@@ -284,7 +296,7 @@ __device__ __forceinline__ void pole_solves(const PoleConst &P, ModeState &s, co
         if (VARIANT == 3) {
             // zeta2 = (zeta1 - c delta2)/conj(alpha) = |1/alpha|^2 m0 + c eta2; DZ (kind 0)
             // rebuilds the zeta pole sum from the eta pole sum instead (finish_kernel)
-            const cd zet2 = mk(fma(P.ia2, s.m0.x, c * eta2.x), fma(P.ia2, s.m0.y, c * eta2.y));
+            const cd zet2 = mk(fma(P.ia2, m0in.x, c * eta2.x), fma(P.ia2, m0in.y, c * eta2.y));
             s.A2 = cfma(w2, zet2, cfma(w1, zet1, s.A2));
         }
     } else {

@@ -71,8 +71,17 @@ typedef enum {
  *                    (default; fewest fp64 ops).
  *  REXI_VARIANT_UV:  paper-literal back-substitution of (u, v) per pole with
  *                    eq:lswVelocities.
- *  REXI_VARIANT_DZ3: as DZ but all three (eta, delta, zeta) pole sums accumulated. */
-typedef enum { REXI_VARIANT_DZ = 0, REXI_VARIANT_UV = 1, REXI_VARIANT_DZ3 = 2 } rexi_variant_t;
+ *  REXI_VARIANT_DZ3: as DZ but all three (eta, delta, zeta) pole sums accumulated.
+ *  REXI_VARIANT_PF:  partial fractions (allowed equivalent):
+ *                    (conj(a) - B)^-1 (a + B)^-1 = [(a + B)^-1 + (conj(a) - B)^-1] / (2 h mu),
+ *                    i.e. two independent Helmholtz solves of f0 per pole, same back-substitution
+ *                    and zeta rebuild as DZ. */
+typedef enum {
+    REXI_VARIANT_DZ = 0,
+    REXI_VARIANT_UV = 1,
+    REXI_VARIANT_DZ3 = 2,
+    REXI_VARIANT_PF = 3
+} rexi_variant_t;
 
 /* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
  *  REXI_METHOD_REXII: the paper's REXII, two solves per term (eq:REXI_Modified_matrix,
@@ -132,6 +141,7 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
  *   REXII DZ:  (1,1,8) (2,1,4) (2,1,5) (3,1,4) (4,1,3) (4,1,4)         default (4,1,4)
  *   REXII UV:  (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)         default (4,1,3)
  *   REXII DZ3: (1,1,8) (2,1,4) (3,1,4) (4,1,2) (4,1,4)                 default (4,1,4)
+ *   REXII PF:  (1,1,8) (2,1,4) (4,1,3) (4,1,4)                         default (4,1,4)
  *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).

@@ -56,12 +56,17 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[4] = {4, 4, 4, 4}, pu[4] = {1, 1, 1, 1}, minb[4] = {4, 3, 4, 4};
-    int occ_cache[4] = {0, 0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
-    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3
+    int mpt[5] = {4, 4, 4, 4, 4}, pu[5] = {1, 1, 1, 1, 1}, minb[5] = {4, 3, 4, 4, 4};
+    int occ_cache[5] = {0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
+    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF
     int kind() const {
         if (method == REXI_METHOD_REXI) return 2;
-        return variant == REXI_VARIANT_UV ? 1 : variant == REXI_VARIANT_DZ3 ? 3 : 0;
+        switch (variant) {
+            case REXI_VARIANT_UV: return 1;
+            case REXI_VARIANT_DZ3: return 3;
+            case REXI_VARIANT_PF: return 4;
+            default: return 0;
+        }
     }
     long n_modes = 0;
     int num_sms = 0;
@@ -531,8 +536,7 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
 
 rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (variant != REXI_VARIANT_DZ && variant != REXI_VARIANT_UV && variant != REXI_VARIANT_DZ3)
-        return fail(REXI_EINVAL, "unknown variant");
+    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PF) return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
     return REXI_OK;
 }

@@ -239,6 +239,7 @@ constexpr int kPoleTile = REXI_POLE_TILE;
 
 struct ModeState {
     cd e0, B0, m0, ua, vb;   // f0 = (e0, ua, vb); B0 = h mu e0 + delta0; m0 = zeta0 - c e0
+    cd Bt0;                  // h mu e0 - delta0 (PF kind)
     double K2, Kx, Ky;
     cd A0, A1, A2;           // accumulators: (eta, delta, zeta) [DZ] or (eta, u, v) [UV]
 };
@@ -274,7 +275,22 @@ __device__ __forceinline__ void pole_solves_in(const PoleConst &P, ModeState &s,
     const cd t = mk(fma(-hn, e0in.y, B0in.x), fma(hn, e0in.x, B0in.y));
     const cd num = cfms(s2, m0in, t);
     const cd eta1 = cmul(num, qd);
-    if (VARIANT == 2) {
+    if (VARIANT == 4) {
+        // Partial fractions (SURVEY.md 8(d) "allowed algebraic equivalents"):
+        //   (conj(alpha) - B)^{-1} (alpha + B)^{-1} = [(alpha + B)^{-1} + (conj(alpha) - B)^{-1}] / (2 h mu)
+        // so w1 g1 + w2 g2 = W1 g1 + W2 gt with gt = (conj(alpha) I - tau A)^{-1} f0: two independent
+        // Helmholtz solves of the same right-hand side. For gt (same reduction, alpha -> conj(alpha),
+        // B -> -B): eta_t (conj(kappa) + K2) = conj(alpha) e0 - delta0 - (c/conj(alpha)) m0,
+        // delta_t = e0 - conj(alpha) eta_t; zeta rebuilt from eta in finish_kernel (as kind 0).
+        const cd tt = mk(fma(hn, e0in.y, s.Bt0.x), fma(-hn, e0in.x, s.Bt0.y));   // Bt0 - i hn e0
+        const cd numt = cjfms(s2, m0in, tt);                                      // - conj(c/alpha) m0
+        const cd etat = cjfma(qd, numt, mk(0, 0));                                // conj(q) numt
+        const cd del1 = cfma(al, eta1, mk(-e0in.x, -e0in.y));
+        const cd delt = cjfms(al, etat, e0in);                                    // e0 - conj(alpha) eta_t
+        const cd W1 = mk(P.W1r, P.W1i), W2 = mk(P.W2r, P.W2i);
+        s.A0 = cfma(W2, etat, cfma(W1, eta1, s.A0));
+        s.A1 = cfma(W2, delt, cfma(W1, del1, s.A1));
+    } else if (VARIANT == 2) {
         // original REXI (eq:originalREXImatrix): one solve per term, acc += Gamma beta^Re g1.
         // zeta1 = m0/alpha + c eta1 is affine in eta1 (potential vorticity, see finish_kernel):
         // its pole sum is rebuilt there, so only (eta, delta) are accumulated.
@@ -407,6 +423,7 @@ pole_kernel(PoleArgs a) {
         const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
         const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
         s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+        s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
         s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
         s.K2 = fma(kx, kx, ky * ky);
         s.A0 = mk(0, 0);
@@ -420,7 +437,8 @@ pole_kernel(PoleArgs a) {
         {
             const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
             double2 *dst = reinterpret_cast<double2 *>(sp);
-            for (int i = threadIdx.x; i < cnt * 10; i += kPoleBlock) dst[i] = src[i];
+            constexpr int kPer = (int)(sizeof(PoleConst) / sizeof(double2));
+            for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
         }
         __syncthreads();
         int q = 0;
@@ -455,7 +473,7 @@ pole_kernel(PoleArgs a) {
             const long m = mode[j];
             out[m] = st[j].A0;
             out[n_modes + m] = st[j].A1;
-            if (VARIANT == 1 || VARIANT == 3) out[2 * n_modes + m] = st[j].A2;
+            if (VARIANT == 1 || VARIANT == 3) out[2 * n_modes + m] = st[j].A2;   // else rebuilt
         }
     }
 }
@@ -472,7 +490,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long n = a.n_modes;
     if (m >= n) return;
-    const bool pv = (a.kind == 0 || a.kind == 2);
+    const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4);
     cd s0 = mk(0, 0), s1 = mk(0, 0), s2 = mk(0, 0);
     for (int c = 0; c < a.n_chunks; ++c) {  // fixed order: deterministic
         const cd *p = a.partial + (size_t)c * 3 * n;
@@ -656,12 +674,14 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
 
 // Supported (variant, modes per thread, poles per loop trip, min blocks per SM) instantiations.
 // Kernel kinds: 0 = REXII DZ (eta, delta accumulated; zeta rebuilt), 1 = REXII UV,
-// 2 = REXI (DZ back-substitution, zeta rebuilt), 3 = REXII DZ3 (all three accumulated).
+// 2 = REXI (DZ back-substitution, zeta rebuilt), 3 = REXII DZ3 (all three accumulated),
+// 4 = REXII PF (partial fractions: two independent solves of f0; zeta rebuilt).
 #define REXI_POLE_CONFIGS(X)                                                             \
     X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 3, 1, 4) X(0, 4, 1, 3) X(0, 4, 1, 4)  \
     X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)  \
     X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 5)                               \
-    X(3, 1, 1, 8) X(3, 2, 1, 4) X(3, 3, 1, 4) X(3, 4, 1, 2) X(3, 4, 1, 4)
+    X(3, 1, 1, 8) X(3, 2, 1, 4) X(3, 3, 1, 4) X(3, 4, 1, 2) X(3, 4, 1, 4)                 \
+    X(4, 1, 1, 8) X(4, 2, 1, 4) X(4, 4, 1, 3) X(4, 4, 1, 4)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 

@@ -186,6 +186,14 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         q.w2r = (double)w2.real();    q.w2i = (double)w2.imag();
         q.s3r = (double)s3.real();    q.s3i = (double)s3.imag();
         q.s4r = (double)s4.real();    q.s4i = (double)s4.imag();
+        {
+            // (conj(alpha) - B)^{-1} (alpha + B)^{-1} = [(alpha + B)^{-1} + (conj(alpha) - B)^{-1}]
+            // / (alpha + conj(alpha)), alpha + conj(alpha) = 2 h mu (partial fractions)
+            const cld W2 = w2 / (2.0L * alpha.real());
+            const cld W1 = w1 + W2;
+            q.W1r = (double)W1.real();  q.W1i = (double)W1.imag();
+            q.W2r = (double)W2.real();  q.W2i = (double)W2.imag();
+        }
         q.ia2 = (double)std::norm(ia);
     }
 

@@ -8,7 +8,7 @@
 
 namespace rexi {
 
-// Per-pole constants of the pole kernel (device layout, 20 doubles = 160 B).
+// Per-pole constants of the pole kernel (device layout, 24 doubles = 192 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
 // the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
 struct alignas(16) PoleConst {
@@ -23,8 +23,10 @@ struct alignas(16) PoleConst {
     double s3r, s3i;    // alpha / kappa   (eq:lswVelocities, UV variant)
     double s4r, s4i;    // c / kappa
     double ia2;         // |1/alpha|^2
+    double W1r, W1i;    // partial-fraction weights (PF kind): w1 + w2 / (2 h mu)
+    double W2r, W2i;    //                                      w2 / (2 h mu)
 };
-static_assert(sizeof(PoleConst) == 160, "PoleConst layout");
+static_assert(sizeof(PoleConst) == 192, "PoleConst layout");
 
 struct Plan {
     int D = 0;

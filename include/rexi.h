@@ -75,12 +75,16 @@ typedef enum {
  *  REXI_VARIANT_PF:  partial fractions (allowed equivalent):
  *                    (conj(a) - B)^-1 (a + B)^-1 = [(a + B)^-1 + (conj(a) - B)^-1] / (2 h mu),
  *                    i.e. two independent Helmholtz solves of f0 per pole, same back-substitution
- *                    and zeta rebuild as DZ. */
+ *                    and zeta rebuild as DZ.
+ *  REXI_VARIANT_PFH: PF with the delta back-substitution (delta = alpha eta - eta0, the first row
+ *                    of each system) folded into the accumulation weights: per pole only the two
+ *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode. */
 typedef enum {
     REXI_VARIANT_DZ = 0,
     REXI_VARIANT_UV = 1,
     REXI_VARIANT_DZ3 = 2,
-    REXI_VARIANT_PF = 3
+    REXI_VARIANT_PF = 3,
+    REXI_VARIANT_PFH = 4
 } rexi_variant_t;
 
 /* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
@@ -141,7 +145,8 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
  *   REXII DZ:  (1,1,8) (2,1,4) (2,1,5) (3,1,4) (4,1,3) (4,1,4)         default (4,1,4)
  *   REXII UV:  (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)         default (4,1,3)
  *   REXII DZ3: (1,1,8) (2,1,4) (3,1,4) (4,1,2) (4,1,4)                 default (4,1,4)
- *   REXII PF:  (1,1,8) (2,1,4) (4,1,3) (4,1,4)                         default (4,1,4)
+ *   REXII PF:  (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
+ *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
  *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).

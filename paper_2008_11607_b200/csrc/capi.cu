@@ -56,15 +56,16 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[5] = {4, 4, 4, 4, 4}, pu[5] = {1, 1, 1, 1, 1}, minb[5] = {4, 3, 4, 4, 4};
-    int occ_cache[5] = {0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning; 0 = unknown
-    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF
+    int mpt[6] = {4, 4, 4, 4, 4, 4}, pu[6] = {1, 1, 1, 1, 1, 1}, minb[6] = {4, 3, 4, 4, 3, 3};
+    int occ_cache[6] = {0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
+    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH
     int kind() const {
         if (method == REXI_METHOD_REXI) return 2;
         switch (variant) {
             case REXI_VARIANT_UV: return 1;
             case REXI_VARIANT_DZ3: return 3;
             case REXI_VARIANT_PF: return 4;
+            case REXI_VARIANT_PFH: return 5;
             default: return 0;
         }
     }
@@ -257,6 +258,9 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         const long double sr = p->host.spre_re[(size_t)e] - p->host.spre_re[(size_t)b];
         const long double si = p->host.spre_im[(size_t)e] - p->host.spre_im[(size_t)b];
         f.S = cd{(double)sr, (double)si};
+        const long double wr = p->host.wpre_re[(size_t)e] - p->host.wpre_re[(size_t)b];
+        const long double wi = p->host.wpre_im[(size_t)e] - p->host.wpre_im[(size_t)b];
+        f.Sd = cd{(double)wr, (double)wi};
     }
     CK(rexi::launch_finish(f, st));
     p->launches += 2;
@@ -536,7 +540,7 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
 
 rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PF) return fail(REXI_EINVAL, "unknown variant");
+    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PFH) return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
     return REXI_OK;
 }

@@ -275,7 +275,18 @@ __device__ __forceinline__ void pole_solves_in(const PoleConst &P, ModeState &s,
     const cd t = mk(fma(-hn, e0in.y, B0in.x), fma(hn, e0in.x, B0in.y));
     const cd num = cfms(s2, m0in, t);
     const cd eta1 = cmul(num, qd);
-    if (VARIANT == 4) {
+    if (VARIANT == 5) {
+        // PFH: as PF, with the delta back-substitution folded into the weights:
+        //   W1 delta1 + W2 delta_t = (W1 alpha) eta1 - (W2 conj(alpha)) eta_t - w1 e0,
+        // the -w1 e0 term summed over the pole range in finish_kernel.
+        const cd tt = mk(fma(hn, e0in.y, s.Bt0.x), fma(-hn, e0in.x, s.Bt0.y));   // Bt0 - i hn e0
+        const cd numt = cjfms(s2, m0in, tt);
+        const cd etat = cjfma(qd, numt, mk(0, 0));
+        const cd W1 = mk(P.W1r, P.W1i), W2 = mk(P.W2r, P.W2i);
+        const cd P1 = mk(P.P1r, P.P1i), P2 = mk(P.P2r, P.P2i);
+        s.A0 = cfma(W2, etat, cfma(W1, eta1, s.A0));
+        s.A1 = cfma(P2, etat, cfma(P1, eta1, s.A1));
+    } else if (VARIANT == 4) {
         // Partial fractions (SURVEY.md 8(d) "allowed algebraic equivalents"):
         //   (conj(alpha) - B)^{-1} (alpha + B)^{-1} = [(alpha + B)^{-1} + (conj(alpha) - B)^{-1}] / (2 h mu)
         // so w1 g1 + w2 g2 = W1 g1 + W2 gt with gt = (conj(alpha) I - tau A)^{-1} f0: two independent
@@ -490,7 +501,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long n = a.n_modes;
     if (m >= n) return;
-    const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4);
+    const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4 || a.kind == 5);
     cd s0 = mk(0, 0), s1 = mk(0, 0), s2 = mk(0, 0);
     for (int c = 0; c < a.n_chunks; ++c) {  // fixed order: deterministic
         const cd *p = a.partial + (size_t)c * 3 * n;
@@ -507,6 +518,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
         const double kx = a.ksym[k], ky = a.ksym[l];
         if (pv) {
             const cd e = a.fhat[m], uu = a.fhat[n + m], vv = a.fhat[2 * n + m];
+            if (a.kind == 5) s1 = cfms(a.Sd, e, s1);   // delta sum: + sum(W2 - W1) e0 = - sum(w1) e0
             const double c = a.tau;
             // m0 = zeta0 - c eta0, zeta0 = i (kx v - ky u)
             const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
@@ -675,13 +687,15 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
 // Supported (variant, modes per thread, poles per loop trip, min blocks per SM) instantiations.
 // Kernel kinds: 0 = REXII DZ (eta, delta accumulated; zeta rebuilt), 1 = REXII UV,
 // 2 = REXI (DZ back-substitution, zeta rebuilt), 3 = REXII DZ3 (all three accumulated),
-// 4 = REXII PF (partial fractions: two independent solves of f0; zeta rebuilt).
+// 4 = REXII PF (partial fractions: two independent solves of f0; zeta rebuilt),
+// 5 = REXII PFH (PF with the delta back-substitution folded into the weights).
 #define REXI_POLE_CONFIGS(X)                                                             \
     X(0, 1, 1, 8) X(0, 2, 1, 4) X(0, 2, 1, 5) X(0, 3, 1, 4) X(0, 4, 1, 3) X(0, 4, 1, 4)  \
     X(1, 1, 1, 6) X(1, 2, 1, 3) X(1, 2, 1, 4) X(1, 3, 1, 3) X(1, 4, 1, 2) X(1, 4, 1, 3)  \
     X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 5)                               \
     X(3, 1, 1, 8) X(3, 2, 1, 4) X(3, 3, 1, 4) X(3, 4, 1, 2) X(3, 4, 1, 4)                 \
-    X(4, 1, 1, 8) X(4, 2, 1, 4) X(4, 4, 1, 3) X(4, 4, 1, 4)
+    X(4, 1, 1, 8) X(4, 2, 1, 3) X(4, 2, 1, 4) X(4, 3, 1, 4) X(4, 4, 1, 3) X(4, 4, 1, 4)  \
+    X(5, 1, 1, 8) X(5, 2, 1, 3) X(5, 2, 1, 4) X(5, 3, 1, 4) X(5, 4, 1, 3) X(5, 4, 1, 4)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 

@@ -81,7 +81,8 @@ struct FinishArgs {
     int D, log2D;
     int kind;              // pole-kernel kind (0 DZ, 1 UV, 2 REXI, 3 DZ3)
     double tau;
-    cd S;                  // kinds 0, 2: sum over the pole range of w1/alpha + w2/|alpha|^2
+    cd S;                  // zeta rebuild: sum over the pole range of w1/alpha + w2/|alpha|^2
+    cd Sd;                 // kind 5: sum over the pole range of w1
 };
 
 struct FixupArgs {

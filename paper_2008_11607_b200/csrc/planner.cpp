@@ -127,6 +127,8 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     p.poles.assign((size_t)p.n_poles, PoleConst{});
     p.spre_re.assign((size_t)p.n_poles + 1, 0.0L);
     p.spre_im.assign((size_t)p.n_poles + 1, 0.0L);
+    p.wpre_re.assign((size_t)p.n_poles + 1, 0.0L);
+    p.wpre_im.assign((size_t)p.n_poles + 1, 0.0L);
     const ld c = (ld)tau;  // tau-scaled Coriolis coefficient (reading G3)
     for (long n = 0; n <= N; ++n) {
         // c_{1,n} = h sum_{k=L1}^{L2} Re(a_k) b_{n-k},  c_{2,n} = h sum Im(a_k) b_{n-k}
@@ -174,6 +176,8 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             const cd_pv_t sv = w1 * ia + w2 * std::norm(ia);
             p.spre_re[(size_t)n + 1] = p.spre_re[(size_t)n] + sv.real();
             p.spre_im[(size_t)n + 1] = p.spre_im[(size_t)n] + sv.imag();
+            p.wpre_re[(size_t)n + 1] = p.wpre_re[(size_t)n] + w1.real();
+            p.wpre_im[(size_t)n + 1] = p.wpre_im[(size_t)n] + w1.imag();
         }
         PoleConst &q = p.poles[(size_t)n];
         q.ar = (double)alpha.real();  q.ai = (double)alpha.imag();
@@ -193,6 +197,9 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             const cld W1 = w1 + W2;
             q.W1r = (double)W1.real();  q.W1i = (double)W1.imag();
             q.W2r = (double)W2.real();  q.W2i = (double)W2.imag();
+            const cld P1 = W1 * alpha, P2 = -W2 * std::conj(alpha);
+            q.P1r = (double)P1.real();  q.P1i = (double)P1.imag();
+            q.P2r = (double)P2.real();  q.P2i = (double)P2.imag();
         }
         q.ia2 = (double)std::norm(ia);
     }

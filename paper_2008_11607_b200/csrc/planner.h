@@ -8,7 +8,7 @@
 
 namespace rexi {
 
-// Per-pole constants of the pole kernel (device layout, 24 doubles = 192 B).
+// Per-pole constants of the pole kernel (device layout, 28 doubles = 224 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
 // the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
 struct alignas(16) PoleConst {
@@ -23,10 +23,12 @@ struct alignas(16) PoleConst {
     double s3r, s3i;    // alpha / kappa   (eq:lswVelocities, UV variant)
     double s4r, s4i;    // c / kappa
     double ia2;         // |1/alpha|^2
-    double W1r, W1i;    // partial-fraction weights (PF kind): w1 + w2 / (2 h mu)
-    double W2r, W2i;    //                                      w2 / (2 h mu)
+    double W1r, W1i;    // partial-fraction weights (PF kinds): w1 + w2 / (2 h mu)
+    double W2r, W2i;    //                                       w2 / (2 h mu)
+    double P1r, P1i;    // PFH: W1 alpha          (delta1 = alpha eta1 - e0 folded into the weights)
+    double P2r, P2i;    // PFH: -W2 conj(alpha)   (delta_t = e0 - conj(alpha) eta_t)
 };
-static_assert(sizeof(PoleConst) == 192, "PoleConst layout");
+static_assert(sizeof(PoleConst) == 224, "PoleConst layout");
 
 struct Plan {
     int D = 0;
@@ -40,6 +42,8 @@ struct Plan {
     // prefix sums (extended precision) of w1_n / alpha_n + w2_n / |alpha_n|^2, n = 0..N:
     // S(b, e) = pre[e] - pre[b] rebuilds the zeta pole sum from the eta pole sum (finish_kernel)
     std::vector<long double> spre_re, spre_im;
+    // prefix sums of w1_n: the e0 term of the delta pole sum in the PFH kind
+    std::vector<long double> wpre_re, wpre_im;
     std::vector<double> ksym;        // D tau-scaled derivative symbols, Nyquist zeroed (G2)
     std::vector<double> twiddle;     // D complex e^{-2 pi i j / D}
 };

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
-VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3}
+VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4}
 METHODS = {"rexii": 0, "rexi": 1}
 
 _vp = ctypes.c_void_p

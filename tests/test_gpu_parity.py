@@ -139,7 +139,7 @@ def _pole_parity(R, D, tau, tol, variant, modes=None, begin=0, end=None, seed=5)
     return err, float(pm.max())
 
 
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh"])
 @pytest.mark.parametrize("D,tau,tol", [(4, 0.5, 1e-12), (8, 1.0, 1e-12), (64, 0.02, 1e-12),
                                        (64, 1.0, 1e-12), (32, 5.0, 1e-8)])
 def test_pole_kernel_full_grid(R, variant, D, tau, tol):
@@ -148,7 +148,7 @@ def test_pole_kernel_full_grid(R, variant, D, tau, tol):
     assert pm < 1e-11, pm
 
 
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh"])
 def test_pole_kernel_ranges(R, variant):
     D, tau = 64, 1.0
     for (b, e) in [(0, 1), (1, 2), (0, 37), (100, 333), (500, 604)]:
@@ -164,7 +164,7 @@ def test_pole_kernel_empty_range_is_zero(R):
     assert float(acc.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh"])
 def test_pole_kernel_c2_full_size_sampled(R, variant):
     """BASELINE configs[1] (512^2, tau = 1, tol 1e-8, 4583 poles) in the launch configuration
     bench.py times; 2048 sampled modes incl. K = 0, Nyquist row/column and the corner."""
@@ -174,7 +174,7 @@ def test_pole_kernel_c2_full_size_sampled(R, variant):
     assert pm < 1e-11, pm
 
 
-@pytest.mark.parametrize("variant", ["dz", "dz3", "pf"])
+@pytest.mark.parametrize("variant", ["dz", "dz3", "pf", "pfh"])
 def test_pole_kernel_c4_size_sampled(R, variant):
     """4096^2 grid, tau = 1, tol 1e-12 (configs[3]): all 36432 poles, 512 sampled modes.
     (A pole SUB-range is a harder target: its terms cancel less, and the independent fp64
@@ -186,7 +186,7 @@ def test_pole_kernel_c4_size_sampled(R, variant):
 
 
 # ----------------------------------------------------------------------------- S1..S5
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh"])
 @pytest.mark.parametrize("D,tau,tol,scen", [(64, 0.02, 1e-12, "gauss"), (64, 0.02, 1e-12, "white"),
                                             (128, 1.0, 1e-12, "gauss"), (32, 3.0, 1e-10, "white"),
                                             (8, 0.7, 1e-12, "white")])
@@ -261,9 +261,9 @@ def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]
     res = {}
-    for v in ("dz", "uv", "dz3", "pf"):
+    for v in ("dz", "uv", "dz3", "pf", "pfh"):
         res[v] = [host(t) for t in R.Plan(D, 2.0, variant=v).apply(*f)]
-    for v in ("uv", "dz3", "pf"):
+    for v in ("uv", "dz3", "pf", "pfh"):
         assert rel_l2(res["dz"], res[v]) < TOL
 
 
@@ -284,7 +284,10 @@ TUNINGS = [("dz", 1, 1, 8), ("dz", 2, 1, 4), ("dz", 2, 1, 5), ("dz", 3, 1, 4), (
            ("uv", 1, 1, 6), ("uv", 2, 1, 3), ("uv", 2, 1, 4), ("uv", 3, 1, 3), ("uv", 4, 1, 2),
            ("uv", 4, 1, 3),
            ("dz3", 1, 1, 8), ("dz3", 2, 1, 4), ("dz3", 3, 1, 4), ("dz3", 4, 1, 2), ("dz3", 4, 1, 4),
-           ("pf", 1, 1, 8), ("pf", 2, 1, 4), ("pf", 4, 1, 3), ("pf", 4, 1, 4)]
+           ("pf", 1, 1, 8), ("pf", 2, 1, 3), ("pf", 2, 1, 4), ("pf", 3, 1, 4), ("pf", 4, 1, 3),
+           ("pf", 4, 1, 4),
+           ("pfh", 1, 1, 8), ("pfh", 2, 1, 3), ("pfh", 2, 1, 4), ("pfh", 3, 1, 4), ("pfh", 4, 1, 3),
+           ("pfh", 4, 1, 4)]
 
 
 @pytest.mark.parametrize("variant,mpt,pu,minb", TUNINGS)

@@ -61,24 +61,24 @@ typedef enum {
     REXI_ERANGE = 4  /* bad pole range                                     */
 } rexi_status_t;
 
-/* Per-pole solve formulation of the fused pole kernel.
- * All solve the same two shifted systems per mode and pole, Helmholtz-reduced
- * (eq:lswEta), and accumulate in registers.
- *  REXI_VARIANT_DZ:  back-substitution in divergence/vorticity variables (delta, zeta of
- *                    PAPER.md:493-496); the eta and delta pole sums are accumulated, the zeta
- *                    pole sum is rebuilt exactly from the eta sum (zeta of each solve is affine
- *                    in its eta: potential vorticity), velocities recovered once per mode
- *                    (default; fewest fp64 ops).
- *  REXI_VARIANT_UV:  paper-literal back-substitution of (u, v) per pole with
- *                    eq:lswVelocities.
- *  REXI_VARIANT_DZ3: as DZ but all three (eta, delta, zeta) pole sums accumulated.
- *  REXI_VARIANT_PF:  partial fractions (allowed equivalent):
- *                    (conj(a) - B)^-1 (a + B)^-1 = [(a + B)^-1 + (conj(a) - B)^-1] / (2 h mu),
- *                    i.e. two independent Helmholtz solves of f0 per pole, same back-substitution
- *                    and zeta rebuild as DZ.
+/* Per-pole solve formulation of the fused pole kernel ("the variant ladder").
+ * Every variant solves, per Fourier mode and pole, the shifted systems of PAPER.md:429-434 by
+ * the Helmholtz reduction (eq:lswEta) and accumulates in registers; they
+ * differ only in exact algebraic rearrangements of the per-pole back-substitution:
+ *  REXI_VARIANT_UV:  paper-literal: (u, v) per pole by eq:lswVelocities,
+ *                    delta, zeta of g1 from (u1, v1) (Alg. 1), then g2.
+ *  REXI_VARIANT_DZ3: back-substitution in divergence/vorticity variables (delta, zeta of
+ *                    PAPER.md:493-496); all three (eta, delta, zeta) pole sums accumulated;
+ *                    velocities recovered once per mode from the sums.
+ *  REXI_VARIANT_DZ:  as DZ3, but the zeta pole sum is rebuilt exactly from the eta pole sum
+ *                    (zeta of each solve is affine in its eta: potential vorticity).
+ *  REXI_VARIANT_PF:  as DZ, with the partial-fraction split of the two resolvents (SURVEY.md 8(d),
+ *                    allowed equivalent): (conj(a) - B)^-1 (a + B)^-1 =
+ *                    [(a + B)^-1 + (conj(a) - B)^-1] / (2 h mu) — two independent solves of f0.
  *  REXI_VARIANT_PFH: PF with the delta back-substitution (delta = alpha eta - eta0, the first row
- *                    of each system) folded into the accumulation weights: per pole only the two
- *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode. */
+ *                    of each system) folded into the accumulation weights: per pole the two
+ *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode
+ *                    (default; fewest fp64 ops). */
 typedef enum {
     REXI_VARIANT_DZ = 0,
     REXI_VARIANT_UV = 1,

@@ -52,7 +52,7 @@ struct DeviceGuard {
 struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
-    int variant = REXI_VARIANT_DZ;
+    int variant = REXI_VARIANT_PFH;
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM

@@ -131,7 +131,7 @@ def _torch():
 class Plan:
     """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
 
-    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="dz", method="rexii"):
+    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfh", method="rexii"):
         torch = _torch()
         if device is None:
             device = torch.cuda.current_device()

@@ -146,7 +146,8 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
  *   REXII UV:  (1,1,6) (2,1,3) (2,1,4) (3,1,3) (4,1,2) (4,1,3)         default (4,1,3)
  *   REXII DZ3: (1,1,8) (2,1,4) (3,1,4) (4,1,2) (4,1,4)                 default (4,1,4)
  *   REXII PF:  (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
- *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
+ *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4) (1,2,6) (2,2,3) (2,2,4) (4,2,2)
+ *                                                                      default (4,2,2)
  *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).

@@ -56,7 +56,7 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[6] = {4, 4, 4, 4, 4, 4}, pu[6] = {1, 1, 1, 1, 1, 1}, minb[6] = {4, 3, 4, 4, 3, 3};
+    int mpt[6] = {4, 4, 4, 4, 4, 4}, pu[6] = {1, 1, 1, 1, 1, 2}, minb[6] = {4, 3, 4, 4, 3, 2};
     int occ_cache[6] = {0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH
     int kind() const {

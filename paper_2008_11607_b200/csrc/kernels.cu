@@ -76,6 +76,11 @@ __device__ __forceinline__ void dftR(cd *v) {
     else dft2<INV>(v);
 }
 
+// Padded shared-memory index: one pad slot per 8 values, so the stride-8 writes of the first
+// Stockham pass (and the stride-N/8 reads) spread over the banks.
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int padded_len(int N) { return N + (N >> 3); }
+
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
 template <int R, bool INV>
@@ -92,7 +97,7 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
             const int step = k * (N / (Ns * R));  // twiddle index step: r * k * N / (Ns R)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                cd x = s[j + r * nbf];
+                cd x = s[pidx(j + r * nbf)];
                 if (r > 0 && Ns > 1) {
                     const double2 w2 = __ldg(reinterpret_cast<const double2 *>(tw) + ((r * step) & (N - 1)));
                     const cd w = mk(w2.x, INV ? -w2.y : w2.y);
@@ -111,7 +116,7 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
             const int k = j & (Ns - 1);
             const int d = (j - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) s[d + r * Ns] = v[b * R + r];
+            for (int r = 0; r < R; ++r) s[pidx(d + r * Ns)] = v[b * R + r];
         }
     }
     __syncthreads();
@@ -151,21 +156,22 @@ __global__ void __launch_bounds__(1024) fft_rows_kernel(FftArgs a) {
                              : static_cast<const cd *>(inp)[g];
         }
     }
+    const int PL = padded_len(D);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) smem[i] = tmp[q];
+        if (i < n) smem[(i >> log2D) * PL + pidx(i & (D - 1))] = tmp[q];
     }
     __syncthreads();
     const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
-    fft_in_smem<INV>(smem + row * D, D, log2D, t, tf, a.twiddle);
+    fft_in_smem<INV>(smem + row * PL, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
         if (i < n) {
             const size_t g = row0 * D + i;
-            const cd v = smem[i];
+            const cd v = smem[(i >> log2D) * PL + pidx(i & (D - 1))];
             if (REAL_OUT) static_cast<double *>(outp)[g] = v.x * sc;
             else static_cast<cd *>(outp)[g] = mk(v.x * sc, v.y * sc);
         }
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
     const int D = a.D, log2D = a.log2D, C = a.per_block;
     const int logC = __ffs(C) - 1;
     const int tf = D >= 8 ? D / 8 : 1;
-    const int stride = D + 1;
+    const int stride = padded_len(D) + 1;
     const size_t col0 = (size_t)blockIdx.x * C;
     const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) smem[(i & (C - 1)) * stride + (i >> logC)] = tmp[q];
+        if (i < n) smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
     }
     __syncthreads();
     const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
         const int i = threadIdx.x + q * blockDim.x;
         if (i < n) {
             const int r = i >> logC, c = i & (C - 1);
-            const cd v = smem[c * stride + r];
+            const cd v = smem[c * stride + pidx(r)];
             out[(size_t)r * D + col0 + c] = mk(v.x * sc, v.y * sc);
         }
     }
@@ -622,7 +628,7 @@ static int fft_rows_per_block(int D) {
 }
 static int fft_cols_per_block(int D) {
     const int tf = D >= 8 ? D / 8 : 1;
-    int C = 1024 / tf;
+    int C = 512 / tf;   // <= 512 threads and ~74 KB of smem per block: 3 blocks per SM
     if (C > 8) C = 8;
     if (C < 1) C = 1;
     if (C > D) C = D;
@@ -656,7 +662,7 @@ cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool re
     const int tf = D >= 8 ? D / 8 : 1;
     dim3 grid(D / a.per_block, 3);
     const int threads = a.per_block * tf;
-    const size_t sm = (size_t)a.per_block * D * sizeof(cd);
+    const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
     if (!inverse && real_in && !real_out) fft_rows_kernel<false, true, false><<<grid, threads, sm, st>>>(a);
     else if (inverse && !real_in && real_out) fft_rows_kernel<true, false, true><<<grid, threads, sm, st>>>(a);
     else if (!inverse && !real_in && !real_out) fft_rows_kernel<false, false, false><<<grid, threads, sm, st>>>(a);
@@ -678,7 +684,7 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     const int tf = D >= 8 ? D / 8 : 1;
     dim3 grid(D / a.per_block, 3);
     const int threads = a.per_block * tf;
-    const size_t sm = (size_t)a.per_block * (D + 1) * sizeof(cd);
+    const size_t sm = (size_t)a.per_block * (padded_len(D) + 1) * sizeof(cd);
     if (inverse) fft_cols_kernel<true><<<grid, threads, sm, st>>>(a);
     else fft_cols_kernel<false><<<grid, threads, sm, st>>>(a);
     return cudaGetLastError();
@@ -695,7 +701,8 @@ cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const c
     X(2, 1, 1, 8) X(2, 2, 1, 4) X(2, 4, 1, 4) X(2, 4, 1, 5)                               \
     X(3, 1, 1, 8) X(3, 2, 1, 4) X(3, 3, 1, 4) X(3, 4, 1, 2) X(3, 4, 1, 4)                 \
     X(4, 1, 1, 8) X(4, 2, 1, 3) X(4, 2, 1, 4) X(4, 3, 1, 4) X(4, 4, 1, 3) X(4, 4, 1, 4)  \
-    X(5, 1, 1, 8) X(5, 2, 1, 3) X(5, 2, 1, 4) X(5, 3, 1, 4) X(5, 4, 1, 3) X(5, 4, 1, 4)
+    X(5, 1, 1, 8) X(5, 2, 1, 3) X(5, 2, 1, 4) X(5, 3, 1, 4) X(5, 4, 1, 3) X(5, 4, 1, 4)  \
+    X(5, 1, 2, 6) X(5, 2, 2, 3) X(5, 2, 2, 4) X(5, 4, 2, 2)
 
 int pole_modes_per_block(int mpt) { return kPoleBlock * mpt; }
 

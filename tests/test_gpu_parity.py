@@ -287,7 +287,7 @@ TUNINGS = [("dz", 1, 1, 8), ("dz", 2, 1, 4), ("dz", 2, 1, 5), ("dz", 3, 1, 4), (
            ("pf", 1, 1, 8), ("pf", 2, 1, 3), ("pf", 2, 1, 4), ("pf", 3, 1, 4), ("pf", 4, 1, 3),
            ("pf", 4, 1, 4),
            ("pfh", 1, 1, 8), ("pfh", 2, 1, 3), ("pfh", 2, 1, 4), ("pfh", 3, 1, 4), ("pfh", 4, 1, 3),
-           ("pfh", 4, 1, 4)]
+           ("pfh", 4, 1, 4), ("pfh", 1, 2, 6), ("pfh", 2, 2, 3), ("pfh", 2, 2, 4), ("pfh", 4, 2, 2)]
 
 
 @pytest.mark.parametrize("variant,mpt,pu,minb", TUNINGS)

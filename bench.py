@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--variant", default="pfh", choices=["pfh", "pf", "dz", "dz3", "uv"])
+    ap.add_argument("--variant", default="pfhr", choices=["pfhr", "pfh", "pf", "dz", "dz3", "uv"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()

@@ -77,14 +77,19 @@ typedef enum {
  *                    [(a + B)^-1 + (conj(a) - B)^-1] / (2 h mu) — two independent solves of f0.
  *  REXI_VARIANT_PFH: PF with the delta back-substitution (delta = alpha eta - eta0, the first row
  *                    of each system) folded into the accumulation weights: per pole the two
- *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode
- *                    (default; fewest fp64 ops). */
+ *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode.
+ *  REXI_VARIANT_PFHR: PFH on "R2C" mode pairs (allowed equivalent): the fields
+ *                    are real, so the spectrum is Hermitian and the solves at -K follow from those
+ *                    at K; the pair {K, -K} accumulates directly the Hermitian part that survives
+ *                    Re(IDFT(.)) (default; used by rexi_apply / apply_partial / apply_host / run;
+ *                    rexi_poles, whose input need not be Hermitian, runs PFH). */
 typedef enum {
     REXI_VARIANT_DZ = 0,
     REXI_VARIANT_UV = 1,
     REXI_VARIANT_DZ3 = 2,
     REXI_VARIANT_PF = 3,
-    REXI_VARIANT_PFH = 4
+    REXI_VARIANT_PFH = 4,
+    REXI_VARIANT_PFHR = 5
 } rexi_variant_t;
 
 /* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
@@ -148,6 +153,8 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
  *   REXII PF:  (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
  *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4) (1,2,6) (2,2,3) (2,2,4) (4,2,2)
  *                                                                      default (4,2,2)
+ *   REXII PFHR: modes_per_thread 4 (one K2 quad = two R2C pairs) with (poles_per_iter,
+ *               min_blocks) in (1,4) (1,5) (1,6) (2,3) (2,4)            default (4,1,5)
  *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).

@@ -52,13 +52,14 @@ struct DeviceGuard {
 struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
-    int variant = REXI_VARIANT_PFH;
+    int variant = REXI_VARIANT_PFHR;
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[6] = {4, 4, 4, 4, 4, 4}, pu[6] = {1, 1, 1, 1, 1, 2}, minb[6] = {4, 3, 4, 4, 3, 2};
-    int occ_cache[6] = {0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
-    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 4}, pu[7] = {1, 1, 1, 1, 1, 2, 1}, minb[7] = {4, 3, 4, 4, 3, 2, 5};
+    int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
+    // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
+    // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
     int kind() const {
         if (method == REXI_METHOD_REXI) return 2;
         switch (variant) {
@@ -66,6 +67,7 @@ struct rexi_plan_s {
             case REXI_VARIANT_DZ3: return 3;
             case REXI_VARIANT_PF: return 4;
             case REXI_VARIANT_PFH: return 5;
+            case REXI_VARIANT_PFHR: return 6;
             default: return 0;
         }
     }
@@ -138,13 +140,16 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // Number of pole chunks (grid.y) for a pole range: minimise the tail of the last wave of
 // blocks (grid sized in multiples of SMs x resident blocks), at most max_chunks, at least
 // 4 poles per chunk.
-int choose_chunks(const rexi_plan_s *p, long n_range) {
+int choose_chunks(const rexi_plan_s *p, long n_range, int v) {
     if (n_range <= 0) return 0;
-    const int v = p->kind();
-    const long mpb = rexi::pole_modes_per_block(p->mpt[v]);
+    const long mpb = v == 6 ? 4L * 128 : rexi::pole_modes_per_block(p->mpt[v]);
     const long tiles = (p->n_modes + mpb - 1) / mpb;
     int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];
-    if (occ <= 0 && rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ) != cudaSuccess) occ = 1;
+    if (occ <= 0) {
+        cudaError_t e = v == 6 ? rexi::pole_r2c_occupancy(p->pu[v], p->minb[v], &occ)
+                               : rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ);
+        if (e != cudaSuccess) occ = 1;
+    }
     const long conc = (long)p->num_sms * std::max(1, occ);
     const long max_c = std::max(1L, std::min<long>(p->max_chunks, n_range / 4));
     int best = 1;
@@ -216,13 +221,18 @@ rexi_status_t do_inverse(rexi_plan_s *p, const cd *acc, double *eta, double *u, 
     return REXI_OK;
 }
 
-rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, cudaStream_t st) {
+// real_input: fhat is the spectrum of real fields (Hermitian), so the R2C pair kernel may be
+// used; rexi_poles (arbitrary complex spectra) passes false.
+rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, cudaStream_t st,
+                       bool real_input) {
     const long n = p->n_modes;
     if (e <= b) {
         CK(cudaMemsetAsync(acc, 0, sizeof(cd) * 3 * (size_t)n, st));
         return REXI_OK;
     }
-    const int chunks = choose_chunks(p, e - b);
+    int kd = p->kind();
+    if (kd == 6 && !real_input) kd = 5;
+    const int chunks = choose_chunks(p, e - b, kd);
     rexi::PoleArgs a;
     a.fhat = fhat;
     a.partial = p->d_partial;
@@ -239,8 +249,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    const int kd = p->kind();
-    CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
+    if (kd == 6) CK(rexi::launch_poles_r2c(a, p->pu[kd], p->minb[kd], st));
+    else CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     rexi::FinishArgs f;
@@ -267,6 +277,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
         rexi::FixupArgs x;
         x.method = p->method;
+        x.write_eta = kd == 6;
+        x.S = f.S;
         x.fhat = fhat;
         x.acc = acc;
         x.poles = p->d_poles;
@@ -305,14 +317,14 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
                              const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
     rexi_status_t s;
     if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
-    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
     return do_inverse(p, p->d_acc, eo, uo, vo, st);
 }
 
 // One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
 rexi_status_t do_spectral_step_direct(rexi_plan_s *p, long b, long e, cudaStream_t st) {
     rexi_status_t s;
-    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st)) != REXI_OK) return s;
+    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
     CK(rexi::launch_hermitian(p->d_acc, p->d_fhat, p->n_modes, p->host.D, st));
     p->launches += 1;
     return REXI_OK;
@@ -540,7 +552,7 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
 
 rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PFH) return fail(REXI_EINVAL, "unknown variant");
+    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PFHR) return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
     return REXI_OK;
 }
@@ -568,8 +580,9 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int pole
                                    int min_blocks_per_sm) {
     if (!p) return fail(REXI_EINVAL, "null plan");
     const int v = p->kind();
-    if (!rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm))
-        return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
+    const bool ok = v == 6 ? (modes_per_thread == 4 && rexi::pole_r2c_supported(poles_per_iter, min_blocks_per_sm))
+                           : rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm);
+    if (!ok) return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
     p->mpt[v] = modes_per_thread;
     p->pu[v] = poles_per_iter;
     p->minb[v] = min_blocks_per_sm;
@@ -603,7 +616,7 @@ rexi_status_t rexi_poles(rexi_plan_t p, long b, long e, const double *fhat, doub
         rexi_status_t s = check_range(p, b, e);
         if (s != REXI_OK) return s;
         return do_poles(p, b, e, reinterpret_cast<const cd *>(fhat), reinterpret_cast<cd *>(acc),
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, false);
     });
 }
 

@@ -384,6 +384,106 @@ __device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) 
     for (int j = 0; j < 4; ++j) m[j] = ((long)l[j] << log2D) + k[j];
 }
 
+// ----------------------------------------------------------------------------- R2C pairs
+// Real physical input => Hermitian spectrum, f0(-K) = conj(f0(K)) (symbols odd in K, G2). For
+// the pair {K, -K} with representative K (the smaller linear index) and the PFH weights, the
+// solves at -K follow from those at K (B0 = Bt0 + 2 d0, d0 = delta0):
+//   eta1(-K)  = conj(eta_t(K) + conj(q) 2 d0),   eta_t(-K) = conj(eta1(K) - q 2 d0),
+// so the Hermitian part that survives the final Re(IDFT(.)),
+//   H(A)(K) = (A(K) + conj(A(-K))) / 2 = [Re sum_{n=-N}^{N} over the pair, "R2C" of SURVEY 8(d)],
+// is accumulated directly per pole:
+//   H_eta   += X1 eta1 + X2 eta_t + (conj(W1 q) - conj(W2) q) d0
+//   H_delta' += Y1 eta1 + Y2 eta_t + (conj(P1 q) - conj(P2) q) d0
+// (X, Y: half-weights from the planner). Each thread owns one K2 quad = two pairs; the
+// corner quad (four self-mirror K = 0 modes) is left to fixup_k0_kernel.
+struct PairState {
+    cd e0, B0, Bt0, m0, d0;  // data of the representative mode
+    cd H0, H1;               // Hermitian accumulators: eta, delta' (before the e0 term)
+};
+
+template <int PU, int MINB>
+__global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
+    __shared__ PoleConst sp[kPoleTile];
+    const long n_modes = a.n_modes;
+    const int chunk = blockIdx.y;
+    const long len = a.pole_end - a.pole_begin;
+    const long p0 = a.pole_begin + len * chunk / a.n_chunks;
+    const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
+    const double c = a.tau;
+    const double hmu = a.hmu;
+    const long q = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+    const bool ok = q > 0 && q < (n_modes >> 2);   // quad 0 = the four K = 0 corners
+    long mq[4];
+    quad_modes(ok ? q : 1, a.D, a.log2D, mq);
+    // representatives: interior quads pair (0,3) and (1,2); axis / Nyquist quads (0,1), (2,3)
+    const int H = a.D >> 1;
+    const int qa = (int)((ok ? q : 1) >> (a.log2D - 1)), qb = (int)((ok ? q : 1) & (H - 1));
+    const long rep[2] = {mq[0], (qa > 0 && qb > 0) ? mq[1] : mq[2]};
+    PairState st[2];
+    double K2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const long mm = rep[j];
+        const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
+        const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
+        const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
+        const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
+        const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
+        PairState &s = st[j];
+        s.e0 = e;
+        s.d0 = d;
+        s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+        s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
+        s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+        s.H0 = mk(0, 0);
+        s.H1 = mk(0, 0);
+        K2 = fma(kx, kx, ky * ky);
+    }
+
+    for (long pt = p0; pt < p1; pt += kPoleTile) {
+        const int cnt = (int)min((long)kPoleTile, p1 - pt);
+        __syncthreads();
+        {
+            const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
+            double2 *dst = reinterpret_cast<double2 *>(sp);
+            constexpr int kPer = (int)(sizeof(PoleConst) / sizeof(double2));
+            for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
+        }
+        __syncthreads();
+#pragma unroll PU
+        for (int qq = 0; qq < cnt; ++qq) {
+            const PoleConst &P = sp[qq];
+            const cd qd = pole_den(P, K2);
+            const cd s2 = mk(P.s2r, P.s2i);
+            const double hn = P.ai;
+            // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, per quad)
+            const cd W1q = cmul(mk(P.W1r, P.W1i), qd), P1q = cmul(mk(P.P1r, P.P1i), qd);
+            const cd sig = cjfms(mk(P.W2r, P.W2i), qd, mk(W1q.x, -W1q.y));
+            const cd tau = cjfms(mk(P.P2r, P.P2i), qd, mk(P1q.x, -P1q.y));
+            const cd X1 = mk(P.X1r, P.X1i), X2 = mk(P.X2r, P.X2i);
+            const cd Y1 = mk(P.Y1r, P.Y1i), Y2 = mk(P.Y2r, P.Y2i);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                PairState &s = st[j];
+                const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
+                const cd eta1 = cmul(cfms(s2, s.m0, t), qd);
+                const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
+                const cd etat = cjfma(qd, cjfms(s2, s.m0, tt), mk(0, 0));
+                s.H0 = cfma(sig, s.d0, cfma(X2, etat, cfma(X1, eta1, s.H0)));
+                s.H1 = cfma(tau, s.d0, cfma(Y2, etat, cfma(Y1, eta1, s.H1)));
+            }
+        }
+    }
+    if (ok) {
+        cd *out = a.partial + (size_t)chunk * 3 * n_modes;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            out[rep[j]] = st[j].H0;
+            out[n_modes + rep[j]] = st[j].H1;
+        }
+    }
+}
+
 // grid = (tiles, pole chunks). MPT < 4: a thread owns MPT modes m = tile0 + j * 128 + tid.
 // MPT = 4: a thread owns one K2 quad (quad_modes) and computes the pole denominator
 // 1/(kappa_n + K2) once for its four modes. Every thread runs all poles of its chunk, PU poles
@@ -507,6 +607,41 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long n = a.n_modes;
     if (m >= n) return;
+    if (a.kind == 6) {   // R2C pairs: Hermitian accumulators at the representative mode
+        const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
+        const long mm = ((long)((a.D - l) & (a.D - 1)) << a.log2D) + ((a.D - k) & (a.D - 1));
+        if (mm == m) return;                        // self-mirror K = 0 corner: fixup_k0_kernel
+        const long r = m < mm ? m : mm;             // representative of {K, -K}
+        cd h0 = mk(0, 0), h1 = mk(0, 0);
+        for (int c = 0; c < a.n_chunks; ++c) {
+            const cd *p = a.partial + (size_t)c * 3 * n;
+            const cd x0 = p[r], x1 = p[n + r];
+            h0 = mk(h0.x + x0.x, h0.y + x0.y);
+            h1 = mk(h1.x + x1.x, h1.y + x1.y);
+        }
+        const int rl = (int)(r >> a.log2D), rk = (int)(r & (a.D - 1));
+        const double kx = a.ksym[rk], ky = a.ksym[rl];
+        const cd e = a.fhat[r], uu = a.fhat[n + r], vv = a.fhat[2 * n + r];
+        const double c = a.tau;
+        // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
+        h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
+        const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
+        cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
+        const double K2 = fma(kx, kx, ky * ky);
+        const double inv = 1.0 / K2;   // K2 > 0: only the corners have K2 = 0
+        const cd t = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
+        const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
+        cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
+        if (r != m) {   // mirror mode: the Hermitian spectrum at -K is the conjugate
+            h0.y = -h0.y;
+            U.y = -U.y;
+            V.y = -V.y;
+        }
+        a.acc[m] = h0;
+        a.acc[n + m] = U;
+        a.acc[2 * n + m] = V;
+        return;
+    }
     const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4 || a.kind == 5);
     cd s0 = mk(0, 0), s1 = mk(0, 0), s2 = mk(0, 0);
     for (int c = 0; c < a.n_chunks; ++c) {  // fixed order: deterministic
@@ -589,6 +724,9 @@ __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
     if (threadIdx.x == 0) {
         a.acc[n + m] = red[0][0];
         a.acc[2 * n + m] = red[1][0];
+        // R2C kind: the pole kernel skips the corners; at K = 0, eta1 = e0/alpha and
+        // eta2 = eta1/conj(alpha), so sum(w1 eta1 + w2 eta2) = S e0 with the finish-kernel S.
+        if (a.write_eta) a.acc[m] = cmul(a.S, a.fhat[m]);
     }
 }
 
@@ -735,6 +873,28 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
     }
     REXI_POLE_CONFIGS(X)
 #undef X
+    return cudaErrorInvalidValue;
+}
+
+bool pole_r2c_supported(int pu, int minb) {
+    return (pu == 1 && (minb == 4 || minb == 5 || minb == 6)) || (pu == 2 && (minb == 3 || minb == 4));
+}
+
+cudaError_t pole_r2c_occupancy(int pu, int minb, int *blocks_per_sm) {
+#define OCC(U, B) if (pu == U && minb == B) \
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2c<U, B>, kPoleBlock, 0);
+    OCC(1, 4) OCC(1, 5) OCC(1, 6) OCC(2, 3) OCC(2, 4)
+#undef OCC
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_poles_r2c(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
+    const long quads = a.n_modes >> 2;
+    dim3 grid((unsigned)((quads + kPoleBlock - 1) / kPoleBlock), (unsigned)a.n_chunks);
+#define LAUNCH(U, B) if (pu == U && minb == B) { \
+    pole_kernel_r2c<U, B><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
+    LAUNCH(1, 4) LAUNCH(1, 5) LAUNCH(1, 6) LAUNCH(2, 3) LAUNCH(2, 4)
+#undef LAUNCH
     return cudaErrorInvalidValue;
 }
 

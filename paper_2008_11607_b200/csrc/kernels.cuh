@@ -87,6 +87,8 @@ struct FinishArgs {
 
 struct FixupArgs {
     int method;            // 0: REXII, 1: REXI
+    int write_eta;         // R2C kind: also write eta = S e0 at the corners
+    cd S;
     const cd *fhat;
     cd *acc;
     const PoleConst *poles;

@@ -8,7 +8,7 @@
 
 namespace rexi {
 
-// Per-pole constants of the pole kernel (device layout, 28 doubles = 224 B).
+// Per-pole constants of the pole kernel (device layout, 36 doubles = 288 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
 // the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
 struct alignas(16) PoleConst {
@@ -27,8 +27,12 @@ struct alignas(16) PoleConst {
     double W2r, W2i;    //                                       w2 / (2 h mu)
     double P1r, P1i;    // PFH: W1 alpha          (delta1 = alpha eta1 - e0 folded into the weights)
     double P2r, P2i;    // PFH: -W2 conj(alpha)   (delta_t = e0 - conj(alpha) eta_t)
+    double X1r, X1i;    // R2C pairs: (W1 + conj W2)/2
+    double X2r, X2i;    //            (W2 + conj W1)/2
+    double Y1r, Y1i;    //            (P1 + conj P2)/2
+    double Y2r, Y2i;    //            (P2 + conj P1)/2
 };
-static_assert(sizeof(PoleConst) == 224, "PoleConst layout");
+static_assert(sizeof(PoleConst) == 288, "PoleConst layout");
 
 struct Plan {
     int D = 0;

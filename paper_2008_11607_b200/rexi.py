@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
-VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4}
+VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4, "pfhr": 5}
 METHODS = {"rexii": 0, "rexi": 1}
 
 _vp = ctypes.c_void_p
@@ -131,7 +131,7 @@ def _torch():
 class Plan:
     """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
 
-    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfh", method="rexii"):
+    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfhr", method="rexii"):
         torch = _torch()
         if device is None:
             device = torch.cuda.current_device()

@@ -186,7 +186,7 @@ def test_pole_kernel_c4_size_sampled(R, variant):
 
 
 # ----------------------------------------------------------------------------- S1..S5
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh", "pfhr"])
 @pytest.mark.parametrize("D,tau,tol,scen", [(64, 0.02, 1e-12, "gauss"), (64, 0.02, 1e-12, "white"),
                                             (128, 1.0, 1e-12, "gauss"), (32, 3.0, 1e-10, "white"),
                                             (8, 0.7, 1e-12, "white")])
@@ -261,9 +261,9 @@ def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]
     res = {}
-    for v in ("dz", "uv", "dz3", "pf", "pfh"):
+    for v in ("dz", "uv", "dz3", "pf", "pfh", "pfhr"):
         res[v] = [host(t) for t in R.Plan(D, 2.0, variant=v).apply(*f)]
-    for v in ("uv", "dz3", "pf", "pfh"):
+    for v in ("uv", "dz3", "pf", "pfh", "pfhr"):
         assert rel_l2(res["dz"], res[v]) < TOL
 
 
@@ -432,3 +432,31 @@ def test_run_spectral_resident_matches_repeated_apply(R, graphs):
     e0 = sum(float((x ** 2).sum()) for x in f)
     e1 = sum(float((host(x) ** 2).sum()) for x in t)
     assert abs(e1 - e0) / e0 < 1e-11
+
+
+
+@pytest.mark.parametrize("pu,minb", [(1, 4), (1, 5), (1, 6), (2, 3), (2, 4)])
+@pytest.mark.parametrize("D", [4, 8, 32, 64])
+def test_pfhr_tunings_vs_oracle(R, pu, minb, D):
+    """R2C-pair kernel (real input): every tuning vs the oracle step, grids with every quad type
+    (corner, axis, Nyquist, interior) and ragged tiles."""
+    tau = 0.9
+    f = inputs.white_noise(D)
+    p = R.Plan(D, tau, variant="pfhr")
+    p.set_tuning(4, pu, minb)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    info = p.info
+    ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])
+    assert rel_l2(got, ref) < TOL
+
+
+def test_pfhr_c2_full_size_properties(R):
+    """The default (PFHR) at the bench configuration: vs DZ3 (all per-pole components formed)
+    and vs the exact propagator."""
+    D = 512
+    f = inputs.gaussian_scenario(D)
+    t = [dev(x) for x in f]
+    a = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant="pfhr").apply(*t)]
+    b = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant="dz3").apply(*t)]
+    assert rel_l2(a, b) < TOL
+    assert rel_l2(a, lrsw.exact_step(*f, 1.0)) < 1e-8

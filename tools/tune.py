@@ -18,12 +18,14 @@ TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (3, 1, 4), (4, 1, 3), (4, 1, 
            "dz3": [(1, 1, 8), (2, 1, 4), (3, 1, 4), (4, 1, 2), (4, 1, 4)],
            "pf": [(1, 1, 8), (2, 1, 3), (2, 1, 4), (3, 1, 4), (4, 1, 3), (4, 1, 4)],
            "pfh": [(1, 1, 8), (2, 1, 3), (2, 1, 4), (3, 1, 4), (4, 1, 3), (4, 1, 4), (1, 2, 6),
-                   (2, 2, 3), (2, 2, 4), (4, 2, 2)]}
-for variant in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dz", "uv", "dz3", "pf", "pfh"):
+                   (2, 2, 3), (2, 2, 4), (4, 2, 2)],
+           "pfhr": [(4, 1, 4), (4, 1, 5), (4, 1, 6), (4, 2, 3), (4, 2, 4)]}
+for variant in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dz", "uv", "dz3", "pf", "pfh", "pfhr"):
     for mpt, pu, minb in TUNINGS[variant]:
         p = rexi.Plan(D, tau, tol=tol, variant=variant)
         p.set_tuning(mpt, pu, minb)
         F = p.forward(*f)
+        out = p.apply(*f)
         acc = p.poles(F)
         torch.cuda.synchronize()
         p.timing_enable(True)
@@ -32,7 +34,10 @@ for variant in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dz", "uv", "dz
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(reps):
-            p.poles(F, acc=acc)
+            if variant == "pfhr":        # the R2C kernel runs on the real-input (apply) path
+                p.apply(*f, out=out)
+            else:
+                p.poles(F, acc=acc)
         ev1.record()
         torch.cuda.synchronize()
         ms, pl, tl = p.timing_read()

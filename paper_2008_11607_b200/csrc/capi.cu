@@ -106,6 +106,9 @@ struct rexi_plan_s {
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
     cudaEvent_t ev_cap[2] = {nullptr, nullptr};
+    // side stream for the K = 0 fix-up, which runs concurrently with the pole kernel (R2C kind)
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<GraphEntry> graphs;
     unsigned long long graph_clock = 0;
 
@@ -121,6 +124,9 @@ struct rexi_plan_s {
         DeviceGuard g(device);
         clear_graphs();
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (aux_stream) cudaStreamDestroy(aux_stream);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
@@ -248,6 +254,35 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.tau = p->host.tau;
     a.hmu = p->host.poles[0].ar;
     rexi_status_t s;
+    const bool fork = (kd == 6);
+    if (fork) {
+        // K = 0 corners on a side stream, concurrently with the pole kernel (disjoint outputs)
+        if (!p->aux_stream) {
+            CK(cudaStreamCreateWithFlags(&p->aux_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+        }
+        rexi::FixupArgs x;
+        x.method = p->method;
+        x.write_eta = 1;
+        {
+            const long double sr = p->host.spre_re[(size_t)e] - p->host.spre_re[(size_t)b];
+            const long double si = p->host.spre_im[(size_t)e] - p->host.spre_im[(size_t)b];
+            x.S = cd{(double)sr, (double)si};
+        }
+        x.fhat = fhat;
+        x.acc = acc;
+        x.poles = p->d_poles;
+        x.pole_begin = b;
+        x.pole_end = e;
+        x.n_modes = n;
+        x.D = p->host.D;
+        CK(cudaEventRecord(p->ev_fork, st));
+        CK(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
+        CK(rexi::launch_fixup_k0(x, p->aux_stream));
+        CK(cudaEventRecord(p->ev_join, p->aux_stream));
+        p->launches += 1;
+    }
     if ((s = record(p, st, true)) != REXI_OK) return s;
     if (kd == 6) CK(rexi::launch_poles_r2c(a, p->pu[kd], p->minb[kd], st));
     else CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
@@ -274,10 +309,12 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     }
     CK(rexi::launch_finish(f, st));
     p->launches += 2;
-    if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
+    if (fork) {
+        CK(cudaStreamWaitEvent(st, p->ev_join, 0));
+    } else if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
         rexi::FixupArgs x;
         x.method = p->method;
-        x.write_eta = kd == 6;
+        x.write_eta = 0;
         x.S = f.S;
         x.fhat = fhat;
         x.acc = acc;

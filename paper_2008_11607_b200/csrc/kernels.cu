@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
 // Modes with Kx = Ky = 0: (0,0), (0,D/2), (D/2,0), (D/2,D/2). There tau A only couples u, v
 // through Coriolis: (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (a,b) (eq:lswVelocities with
 // grad eta = 0) and (u2,v2) = conj(kappa)^-1 [[conj alpha, c],[-c, conj alpha]] (u1,v1).
-constexpr int kFixBlock = 256;
+constexpr int kFixBlock = 1024;
 __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
     __shared__ cd red[2][kFixBlock];
     const int D = a.D, H = D / 2;
@@ -695,9 +695,9 @@ __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
     const cd ua = a.fhat[n + m], vb = a.fhat[2 * n + m];
     cd Au = mk(0, 0), Av = mk(0, 0);
     for (long p = a.pole_begin + threadIdx.x; p < a.pole_end; p += kFixBlock) {
-        const PoleConst P = a.poles[p];
-        const cd s3 = mk(P.s3r, P.s3i), s4 = mk(P.s4r, P.s4i);
-        const cd w1 = mk(P.w1r, P.w1i), w2 = mk(P.w2r, P.w2i);
+        const PoleConst *P = a.poles + p;
+        const cd s3 = mk(__ldg(&P->s3r), __ldg(&P->s3i)), s4 = mk(__ldg(&P->s4r), __ldg(&P->s4i));
+        const cd w1 = mk(__ldg(&P->w1r), __ldg(&P->w1i)), w2 = mk(__ldg(&P->w2r), __ldg(&P->w2i));
         const cd u1 = cfms(s4, vb, cmul(s3, ua));
         const cd v1 = cfma(s3, vb, cmul(s4, ua));
         if (a.method == 1) {   // REXI: one solve per term

@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="pfhr", choices=["pfhr", "pfh", "pf", "dz", "dz3", "uv"])
+    ap.add_argument("--h", default="0.5", help="Gaussian spacing h, or 'auto' (NEXT-2 h_for_tol)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -220,7 +221,8 @@ def main():
     from paper_2008_11607_b200.distributed import apply_distributed, pole_partition
 
     D, tau, tol, scen, cidx = CONFIGS[args.config]
-    plan = rexi.Plan(D, tau, tol=tol, h=0.5, device=local, variant=args.variant)
+    h_arg = "auto" if args.h == "auto" else float(args.h)
+    plan = rexi.Plan(D, tau, tol=tol, h=h_arg, device=local, variant=args.variant)
     info = plan.info
     n_poles = info["n_poles"]
     pb, pe = pole_partition(n_poles, world, rank)
@@ -330,8 +332,8 @@ def main():
             "steps_per_s": args.steps / (ms_total / 1e3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: LRSW {D}x{D}, tau={tau}, tol={tol}, h=0.5, "
-                                   f"M={info['M']}, {n_poles} poles, {scen} scenario "
+            "config": {"workload": f"{args.config}: LRSW {D}x{D}, tau={tau}, tol={tol}, "
+                                   f"h={info['h']:.4g}, M={info['M']}, {n_poles} poles, {scen} scenario "
                                    f"(BASELINE configs[{cidx}])",
                        "variant": args.variant, "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"poles split over {world} GPU(s)"},

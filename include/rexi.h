@@ -50,6 +50,7 @@ extern "C" {
 #endif
 
 #define REXI_ABI_VERSION 1
+#define REXI_H_AUTO (-1.0)
 
 typedef struct rexi_plan_s *rexi_plan_t; /* opaque; owns device workspace + pole table */
 
@@ -127,7 +128,8 @@ typedef struct {
  *  tol:    in (0, 1): sets m0 = ceil(2 sqrt(h^2 - ln(sqrt(4 pi) tol)) - 1) (reading G9,
  *          from Appendix B). tol <= 0 means the paper's m0 = 11
  *          (eq:Mformula).
- *  h:      in (0, pi); h <= 0 selects 0.5.
+ *  h:      in (0, pi); h <= 0 selects 0.5; h == REXI_H_AUTO selects
+ *          rexi_h_for_tol(tol) (NEXT-2: fewer poles at loose tolerances).
  *  M:      > 0: use this M (must be >= 12); <= 0: M from the rule
  *          tau rho(A) <= (M - m0) h (eq:matrixAccuracyBound).
  *  device: CUDA device ordinal.
@@ -240,6 +242,11 @@ int rexi_appendix_a(double *mu, double *a);
  * arrays of n_poles entries may be NULL. */
 long rexi_terms_host(double h, long M, int method, double *alpha, double *C1, double *C2,
                      double *gamma);
+
+/* Host-only (no GPU needed): the h optimiser of REXI_H_AUTO (NEXT-2, readings G8/G9): the largest
+ * h with aliasing floor e^{-4 pi (pi - h)} <= tol / 10, clamped to [0.5, 2]; 0.5 if tol is not
+ * in (0, 1). */
+double rexi_h_for_tol(double tol);
 
 /* Host-only (no GPU needed): the term-count rule used by rexi_plan_create:
  * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0. */

@@ -278,6 +278,14 @@ def m0_for_tol(tol, h):
     return int(math.ceil(2.0 * math.sqrt(h * h - math.log(math.sqrt(4.0 * math.pi) * tol)) - 1.0))
 
 
+def h_for_tol(tol):
+    """NEXT-2 h optimiser (readings G8, G9): largest h with e^{-4 pi (pi - h)} <= tol/10,
+    clamped to [0.5, 2]."""
+    if not (0.0 < tol < 1.0):
+        return 0.5
+    return min(2.0, max(0.5, math.pi - math.log(10.0 / tol) / (4.0 * math.pi)))
+
+
 def M_rule(x_max, h, m0=11):
     """eq:Mformula / eq:matrixAccuracyBound: smallest M with x_max <= (M - m0) h."""
     return int(math.ceil(x_max / h)) + m0

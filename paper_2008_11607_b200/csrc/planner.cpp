@@ -66,6 +66,17 @@ long m0_for_tol(double tol, double h) {
     return (long)std::ceil(v);
 }
 
+// NEXT-2 h optimiser (reading G9): the largest h whose aliasing floor
+// e^{-4 pi (pi - h)} (reading G8) stays a factor 10 below tol, clamped to [0.5, 2]:
+// fewer poles (M ~ tau rho / h) at the same tolerance.
+double h_for_tol(double tol) {
+    if (!(tol > 0.0 && tol < 1.0)) return 0.5;
+    double h = M_PI - std::log(10.0 / tol) / (4.0 * M_PI);
+    if (h < 0.5) h = 0.5;
+    if (h > 2.0) h = 2.0;
+    return h;
+}
+
 static void set_err(std::vector<char> &err, const char *msg) {
     err.assign(msg, msg + std::strlen(msg) + 1);
 }
@@ -82,6 +93,7 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
         return REXI_EINVAL;
     }
     if (!std::isfinite(tau)) { set_err(err, "tau must be finite"); return REXI_EINVAL; }
+    if (h == REXI_H_AUTO) h = h_for_tol(tol);
     if (!(h > 0.0)) h = 0.5;
     if (!(h < M_PI)) { set_err(err, "h must lie in (0, pi) (PAPER.md:98)"); return REXI_EINVAL; }
     if (!(tol < 1.0) || std::isnan(tol)) { set_err(err, "tol must lie in (0, 1) (or <= 0 for m0 = 11)"); return REXI_EINVAL; }
@@ -263,3 +275,5 @@ extern "C" long rexi_terms_host(double h, long M, int method, double *alpha, dou
     if (gamma) std::memcpy(gamma, p.gamma.data(), n * sizeof(double));
     return p.n_poles;
 }
+
+extern "C" double rexi_h_for_tol(double tol) { return rexi::h_for_tol(tol); }

@@ -58,5 +58,6 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
               int method = 0);
 
 long m0_for_tol(double tol, double h);
+double h_for_tol(double tol);
 
 }  // namespace rexi

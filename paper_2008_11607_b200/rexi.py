@@ -62,6 +62,7 @@ EXPORTS = {
     "rexi_timing_read": (ctypes.c_int, [_vp, _dp, _lp, _lp]),
     "rexi_appendix_a": (ctypes.c_int, [_dp, _dp]),
     "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, ctypes.c_int, _dp, _dp, _dp, _dp]),
+    "rexi_h_for_tol": (ctypes.c_double, [ctypes.c_double]),
     "rexi_rule_M": (ctypes.c_long, [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rexi_last_error": (ctypes.c_char_p, []),
@@ -118,6 +119,13 @@ def rule_M(D, tau, tol, h=0.5):
     return int(_lib.rexi_rule_M(int(D), float(tau), float(tol), float(h)))
 
 
+H_AUTO = -1.0
+
+
+def h_for_tol(tol):
+    return float(_lib.rexi_h_for_tol(float(tol)))
+
+
 def abi_version():
     return _lib.rexi_abi_version()
 
@@ -132,6 +140,11 @@ class Plan:
     """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
 
     def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfhr", method="rexii"):
+        """h = "auto" (or H_AUTO) selects h_for_tol(tol) (NEXT-2)."""
+        if isinstance(h, str):
+            if h != "auto":
+                raise ValueError("h must be a number or 'auto'")
+            h = H_AUTO
         torch = _torch()
         if device is None:
             device = torch.cuda.current_device()

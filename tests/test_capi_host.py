@@ -89,3 +89,8 @@ def test_planner_rexi_terms_match_oracle(rexi, h, M):
     assert np.abs(beta - t.beta_re[sel]).max() <= 2e-15 * np.abs(t.beta_re).max()
     assert np.all(zero == 0)
     assert g[0] == 1.0 and np.all(g[1:] == 2.0)
+
+
+@pytest.mark.parametrize("tol", [0.0, 1e-3, 1e-6, 1e-8, 1e-12, 1e-15])
+def test_h_for_tol_matches_oracle(rexi, tol):
+    assert rexi.h_for_tol(tol) == C.h_for_tol(tol)

@@ -460,3 +460,22 @@ def test_pfhr_c2_full_size_properties(R):
     b = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant="dz3").apply(*t)]
     assert rel_l2(a, b) < TOL
     assert rel_l2(a, lrsw.exact_step(*f, 1.0)) < 1e-8
+
+
+def test_h_auto_c2(R):
+    """NEXT-2: h chosen from tol (h_for_tol) at the bench configuration: ~3x fewer poles and
+    still within tol of the exact propagator; parity with the oracle at a small size."""
+    D = 512
+    f = inputs.gaussian_scenario(D)
+    p = R.Plan(D, 1.0, tol=1e-8, h="auto")
+    info = p.info
+    assert info["h"] > 1.4 and p.n_poles < 1600
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    assert rel_l2(got, lrsw.exact_step(*f, 1.0)) < 1e-8
+    D = 32
+    g = inputs.white_noise(D)
+    q = R.Plan(D, 2.0, tol=1e-8, h="auto")
+    got = [host(t) for t in q.apply(*(dev(x) for x in g))]
+    ref = lrsw.rexii_step(*g, 2.0, q.info["h"], q.info["M"])
+    assert rel_l2(got, ref) < TOL
+    assert rel_l2(got, lrsw.exact_step(*g, 2.0)) < 1e-8

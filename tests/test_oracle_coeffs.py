@@ -204,3 +204,17 @@ def test_rexi_beta_conjugate_symmetry_R2():
     half = sum(gg * np.real(b * np.linalg.solve(A + a * I, f))
                for gg, b, a in zip(gam, t.beta_re[sel], t.alpha[sel]))
     assert np.abs(full - half).max() < 1e-12 * np.abs(full).max()
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-6, 1e-8, 1e-10, 1e-12])
+def test_h_for_tol_meets_tol_scalar(tol):
+    """NEXT-2 h optimiser (readings G8, G9): with h = h_for_tol(tol) and M from the rule, the
+    scalar REXII meets tol over the whole admissible range (and uses ~h/0.5 x fewer terms)."""
+    h = C.h_for_tol(tol)
+    xmax = 60.0
+    M = C.M_rule(xmax, h, C.m0_for_tol(tol, h))
+    x = np.linspace(-xmax, xmax, 1201)
+    err = np.abs(C.rexii_scalar(x, h, M) - np.exp(1j * x)).max()
+    assert err < tol
+    if tol >= 1e-8:
+        assert h > 1.4 and M < 0.5 * C.M_rule(xmax, 0.5, C.m0_for_tol(tol, 0.5))

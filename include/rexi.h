@@ -147,6 +147,11 @@ rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
  * (h, M) (synchronous: waits for the device). EINVAL for unknown values. */
 rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
 
+/* Replace the plan's rational approximation of the Gaussian (default: Appendix A) by
+ * (L, mu, a[2(L+1)]) — e.g. a rexi_fit_gaussian refit — keeping h and M (N = M + L).
+ * Rebuilds and uploads the term table (synchronous). EINVAL for bad tables. */
+rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const double *a);
+
 /* Pole-kernel tuning for the plan's CURRENT variant: Fourier modes per thread, poles per loop
  * trip and resident blocks per SM requested of the compiler (register budget). Supported:
  *   REXII DZ:  (1,1,8) (2,1,4) (2,1,5) (3,1,4) (4,1,3) (4,1,4)         default (4,1,4)
@@ -242,6 +247,18 @@ int rexi_appendix_a(double *mu, double *a);
  * arrays of n_poles entries may be NULL. */
 long rexi_terms_host(double h, long M, int method, double *alpha, double *C1, double *C2,
                      double *gamma);
+
+/* Host-only (no GPU needed), NEXT-2: the paper's least-squares fit of the Gaussian psi_1 by the
+ * symmetric rational function R (eq:A(x,mu); eq:minl2approx)
+ * on K points of the Leja sequence on [0, xmax] started at x_1 = 0 (reading G18),
+ * solved by Householder QR in extended precision. mu = NaN scans mu in [-7, -3] for the
+ * smallest defect ("mu is determined such that a high accuracy is obtained").
+ * Outputs a_out[2(L+1)] = (Re a_l, Im a_l), l = 0..L (a_0 real), *mu_out and *defect =
+ * max |R - psi_1| on [-200, 200] (the REXI sums evaluate R far into its tail; xmax = 100,
+ * K = 200 keep the tail below ~1e-15). Returns 0, or -1 for bad arguments (L in 1..64,
+ * K >= 2L+1). */
+int rexi_fit_gaussian(int L, double mu, int K, double xmax, double *a_out, double *mu_out,
+                      double *defect);
 
 /* Host-only (no GPU needed): the h optimiser of REXI_H_AUTO (NEXT-2, readings G8/G9): the largest
  * h with aliasing floor e^{-4 pi (pi - h)} <= tol / 10, clamped to [0.5, 2]; 0.5 if tol is not

@@ -136,6 +136,52 @@ def R_real_form(x, mu=None, a=None):
     return out
 
 
+def leja_points(K, xmax, ncand=30001):
+    """Reading G18: the Leja sequence on [0, xmax] from x_1 = 0 ("the same strategy
+    that is used for ... interpolation with Leja points"): x_{k+1} maximises prod_j |x - x_j|
+    over a uniform candidate grid."""
+    cand = np.linspace(0.0, xmax, ncand)
+    pts = [0.0]
+    logp = np.log(np.abs(cand) + 1e-300)
+    used = np.zeros(ncand, dtype=bool)
+    used[0] = True
+    for _ in range(1, K):
+        score = np.where(used, -np.inf, logp)
+        i = int(np.argmax(score))
+        used[i] = True
+        pts.append(cand[i])
+        logp = logp + np.log(np.abs(cand - cand[i]) + 1e-300)
+    return np.array(pts)
+
+
+def design_matrix(x, mu, L):
+    """G(x, mu, L) of PAPER.md:155-162: columns for y = [a0, Re a_1..Re a_L, Im a_1..Im a_L]
+    of the real form eq:A(x,mu)."""
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    x2 = x * x
+    cols = [mu / (x2 + mu * mu)]
+    dens = [x2 * x2 + 2.0 * (mu * mu - l * l) * x2 + (mu * mu + l * l) ** 2 for l in range(1, L + 1)]
+    for l in range(1, L + 1):
+        cols.append(2.0 * mu * (mu * mu + l * l + x2) / dens[l - 1])
+    for l in range(1, L + 1):
+        cols.append(2.0 * l * (mu * mu + l * l - x2) / dens[l - 1])
+    return np.stack(cols, axis=-1)
+
+
+def fit_rational_gaussian(L=24, mu=-5.133333333333333, K=200, xmax=100.0):
+    """NEXT-2: eq:minl2approx — least squares of psi_1 - R on K Leja points
+    on [0, xmax] (reading G18; xmax = 100 so the tail of R, which the REXI sums evaluate, stays
+    small). Returns a[0..2L] with a[L + l] = a_l, a_{-l} = conj(a_l)."""
+    x = leja_points(K, xmax)
+    y, *_ = np.linalg.lstsq(design_matrix(x, mu, L), psi(1.0, x), rcond=None)
+    a = np.zeros(2 * L + 1, dtype=np.complex128)
+    a[L] = y[0]
+    for l in range(1, L + 1):
+        a[L + l] = y[l] + 1j * y[L + l]
+        a[L - l] = np.conj(a[L + l])
+    return a
+
+
 # ---------------------------------------------------------------------------
 # Step 3 — single-sum coefficient tables
 # ---------------------------------------------------------------------------
@@ -181,10 +227,18 @@ def _windowed(h, M, L, wk_re, wk_im, bre, bim, N):
     return hh * out_re, hh * out_im
 
 
-def rexii_terms(h, M):
-    """The REXII term table (eq:modifiedRexi, eq:REXI_Modified_matrix), N = M + L."""
-    mu_ld, a_re, a_im = appendix_a(LD)
-    L = L_APPENDIX_A
+def rexii_terms(h, M, mu=None, a=None):
+    """The REXII term table (eq:modifiedRexi, eq:REXI_Modified_matrix), N = M + L.
+    Default table: Appendix A; or (mu, a[0..2L]) with a[L + l] = a_l (e.g. a NEXT-2 refit)."""
+    if mu is None:
+        mu_ld, a_re, a_im = appendix_a(LD)
+        L = L_APPENDIX_A
+    else:
+        a = np.asarray(a, dtype=np.complex128)
+        L = (len(a) - 1) // 2
+        mu_ld = LD(mu)
+        a_re = a.real.astype(LD)
+        a_im = a.imag.astype(LD)
     N = M + L
     bre, bim = b_coeffs_ld(h, M)
     zero = np.zeros_like(a_re)

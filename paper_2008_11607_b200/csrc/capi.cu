@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <complex>
 #include <cstring>
 #include <new>
 #include <string>
@@ -602,13 +603,46 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t p, int method) {
         rexi::Plan np;
         std::vector<char> err;
         const rexi::Plan &h = p->host;
-        int st = rexi::make_plan(np, h.D, h.tau, h.tol, h.h, h.M, err, method);
+        int st = rexi::make_plan(np, h.D, h.tau, h.tol, h.h, h.M, err, method, &h.table);
         if (st != REXI_OK) return fail((rexi_status_t)st, err.empty() ? "planner" : std::string(err.data()));
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         p->host = std::move(np);
         p->method = method;
+        return REXI_OK;
+    });
+}
+
+rexi_status_t rexi_plan_set_table(rexi_plan_t p, int L, double mu, const double *a) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (L < 1 || L > 64 || !a || !std::isfinite(mu)) return fail(REXI_EINVAL, "bad coefficient table");
+        rexi::GaussTable t;
+        t.L = L;
+        t.mu = mu;
+        t.a.resize((size_t)L + 1);
+        for (int l = 0; l <= L; ++l) t.a[(size_t)l] = std::complex<long double>(a[2 * l], a[2 * l + 1]);
+        rexi::Plan np;
+        std::vector<char> err;
+        const rexi::Plan &h = p->host;
+        // M is kept (the term count of the plan); N = M + L follows the new L
+        int st = rexi::make_plan(np, h.D, h.tau, h.tol, h.h, h.M, err, p->method, &t);
+        if (st != REXI_OK) return fail((rexi_status_t)st, err.empty() ? "planner" : std::string(err.data()));
+        CK(cudaDeviceSynchronize());
+        p->clear_graphs();
+        if (np.n_poles != h.n_poles) {
+            rexi::PoleConst *d = nullptr;
+            cudaError_t e = cudaMalloc((void **)&d, sizeof(rexi::PoleConst) * (size_t)np.n_poles);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(REXI_ENOMEM, "cudaMalloc (pole table) failed");
+            }
+            cudaFree(p->d_poles);
+            p->d_poles = d;
+        }
+        CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
+        p->host = std::move(np);
         return REXI_OK;
     });
 }

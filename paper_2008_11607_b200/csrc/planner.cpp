@@ -51,10 +51,19 @@ static const long double kPiL = 3.141592653589793238462643383279502884L;
 
 static ld parse(const char *s) { return std::strtold(s, nullptr); }
 
+GaussTable appendix_a_table() {
+    GaussTable t;
+    t.L = kL;
+    t.mu = parse(kMu);
+    t.a.resize((size_t)kL + 1);
+    for (int l = 0; l <= kL; ++l) t.a[(size_t)l] = cld(parse(kA[l][0]), parse(kA[l][1]));
+    return t;
+}
+
 // a_l for l = -L..L (conjugate-symmetric extension)
-static cld a_coeff(int l) {
-    int al = l < 0 ? -l : l;
-    cld a(parse(kA[al][0]), parse(kA[al][1]));
+static cld a_coeff(const GaussTable &t, int l) {
+    const int al = l < 0 ? -l : l;
+    const cld a = t.a[(size_t)al];
     return l < 0 ? std::conj(a) : a;
 }
 
@@ -82,7 +91,14 @@ static void set_err(std::vector<char> &err, const char *msg) {
 }
 
 int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err,
-              int method) {
+              int method, const GaussTable *table) {
+    p.table = table ? *table : appendix_a_table();
+    const GaussTable &T = p.table;
+    const int kLt = T.L;
+    if (kLt < 1 || (int)T.a.size() != kLt + 1) {
+        set_err(err, "bad coefficient table");
+        return REXI_EINVAL;
+    }
     if (method != 0 && method != 1) {
         set_err(err, "method must be REXI_METHOD_REXII or REXI_METHOD_REXI");
         return REXI_EINVAL;
@@ -111,11 +127,11 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     if (M < 12) { set_err(err, "M must be >= 12 (eq:Mformula needs M - 11 >= 1)"); return REXI_EINVAL; }
     if (M > 50000000L) { set_err(err, "M too large"); return REXI_EINVAL; }
     p.M = M;
-    p.L = kL;
-    p.N = M + kL;
+    p.L = kLt;
+    p.N = M + kLt;
     p.n_poles = p.N + 1;
     const ld hh = (ld)h;
-    const ld mu = parse(kMu);
+    const ld mu = T.mu;
     p.mu = (double)mu;
     {
         ld alias = std::exp(-4.0L * kPiL * (kPiL - hh));                 // reading G8
@@ -145,10 +161,10 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     for (long n = 0; n <= N; ++n) {
         // c_{1,n} = h sum_{k=L1}^{L2} Re(a_k) b_{n-k},  c_{2,n} = h sum Im(a_k) b_{n-k}
         // L1(n) = max(-L, n - M), L2(n) = min(L, n + M)
-        long L1 = std::max<long>(-kL, n - M), L2 = std::min<long>(kL, n + M);
+        long L1 = std::max<long>(-kLt, n - M), L2 = std::min<long>(kLt, n + M);
         cld c1(0, 0), c2(0, 0), beta(0, 0);
         for (long k = L1; k <= L2; ++k) {
-            cld ak = a_coeff((int)k);
+            cld ak = a_coeff(T, (int)k);
             const cld &bnk = b[(size_t)(n - k + M)];
             c1 += ak.real() * bnk;
             c2 += ak.imag() * bnk;

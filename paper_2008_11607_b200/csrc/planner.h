@@ -4,9 +4,19 @@
 // arXiv:2008.11607 and the per-pole constants consumed by the fused pole kernel.
 #pragma once
 
+#include <complex>
 #include <vector>
 
 namespace rexi {
+
+// The rational approximation R(x) of psi_1 (eq:ratapproxgaus): mu and a_0..a_L
+// (a_{-l} = conj(a_l)); Appendix A by default, or a NEXT-2 refit.
+struct GaussTable {
+    int L = 24;
+    long double mu = 0;
+    std::vector<std::complex<long double>> a;   // a_0..a_L
+};
+GaussTable appendix_a_table();
 
 // Per-pole constants of the pole kernel (device layout, 36 doubles = 288 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
@@ -35,6 +45,7 @@ struct alignas(16) PoleConst {
 static_assert(sizeof(PoleConst) == 288, "PoleConst layout");
 
 struct Plan {
+    GaussTable table;
     int D = 0;
     int method = 0;                  // 0: REXII (eq:REXI_Modified_matrix), 1: REXI (eq:originalREXImatrix)
     double tau = 0, tol = 0, h = 0, mu = 0;
@@ -55,7 +66,7 @@ struct Plan {
 // Validates the arguments (see rexi.h) and fills `p`. Returns 0 or a rexi_status_t code;
 // `err` receives a message.
 int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err,
-              int method = 0);
+              int method = 0, const GaussTable *table = nullptr);
 
 long m0_for_tol(double tol, double h);
 double h_for_tol(double tol);

@@ -63,6 +63,9 @@ EXPORTS = {
     "rexi_appendix_a": (ctypes.c_int, [_dp, _dp]),
     "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, ctypes.c_int, _dp, _dp, _dp, _dp]),
     "rexi_h_for_tol": (ctypes.c_double, [ctypes.c_double]),
+    "rexi_fit_gaussian": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                         _dp, _dp, _dp]),
+    "rexi_plan_set_table": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _dp]),
     "rexi_rule_M": (ctypes.c_long, [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rexi_last_error": (ctypes.c_char_p, []),
@@ -124,6 +127,18 @@ H_AUTO = -1.0
 
 def h_for_tol(tol):
     return float(_lib.rexi_h_for_tol(float(tol)))
+
+
+def fit_gaussian(L=24, mu=-5.133333333333333, K=200, xmax=100.0):
+    """NEXT-2 refit (rexi_fit_gaussian): returns (mu, a[0..L] complex, defect); mu=None scans."""
+    a = np.zeros(2 * (L + 1))
+    mu_out = ctypes.c_double()
+    d = ctypes.c_double()
+    r = _lib.rexi_fit_gaussian(int(L), float("nan") if mu is None else float(mu), int(K), float(xmax),
+                               _np_ptr(a), ctypes.byref(mu_out), ctypes.byref(d))
+    if r != 0:
+        raise ValueError("bad fit arguments")
+    return mu_out.value, a[0::2] + 1j * a[1::2], d.value
 
 
 def abi_version():
@@ -191,6 +206,13 @@ class Plan:
 
     def set_graphs(self, enable):
         _check(_lib.rexi_plan_set_graphs(self._h, int(bool(enable))), "rexi_plan_set_graphs")
+
+    def set_table(self, mu, a):
+        """Use (mu, a_0..a_L) instead of Appendix A (rexi_plan_set_table)."""
+        a = np.asarray(a, dtype=np.complex128)
+        buf = np.ascontiguousarray(np.stack([a.real, a.imag], axis=-1).ravel())
+        _check(_lib.rexi_plan_set_table(self._h, len(a) - 1, float(mu), _np_ptr(buf)), "rexi_plan_set_table")
+        self.n_poles = self.info["n_poles"]
 
     def set_method(self, method):
         m = METHODS[method] if isinstance(method, str) else int(method)

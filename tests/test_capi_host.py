@@ -94,3 +94,33 @@ def test_planner_rexi_terms_match_oracle(rexi, h, M):
 @pytest.mark.parametrize("tol", [0.0, 1e-3, 1e-6, 1e-8, 1e-12, 1e-15])
 def test_h_for_tol_matches_oracle(rexi, tol):
     assert rexi.h_for_tol(tol) == C.h_for_tol(tol)
+
+
+def test_planner_refit_meets_paper_bound(rexi):
+    """NEXT-2: the planner's extended-precision refit, evaluated by the oracle in 30-digit
+    arithmetic, meets the paper's stated fit error (< 8e-15), and its REXII
+    reproduces e^{ix} at the Fig. 1 threshold M = ceil(x/h) + 11."""
+    mpmath = pytest.importorskip("mpmath")
+    mu, a, defect = rexi.fit_gaussian(24, -5.133333333333333)
+    assert defect < 8e-15
+    mpmath.mp.dps = 30
+    full = [complex(np.conj(v)) for v in a[:0:-1]] + [complex(v) for v in a]
+    worst = 0.0
+    for x in np.linspace(0.0, 30.0, 601):
+        xm = mpmath.mpf(float(x))
+        s_ = mpmath.mpc(0)
+        for j, l in enumerate(range(-24, 25)):
+            s_ += mpmath.mpc(full[j].real, full[j].imag) / (mpmath.mpc(0, 1) * xm + mpmath.mpf(mu) + mpmath.mpc(0, l))
+        worst = max(worst, float(abs(s_.real - mpmath.exp(-xm * xm / 4) / mpmath.sqrt(4 * mpmath.pi))))
+    assert worst < 8e-15
+    # scalar REXII with the refit table (oracle evaluator, closed-form reference)
+    h, X = 0.5, 30.0
+    M = C.M_rule(X, h)
+    t = C.rexii_terms(h, M, mu=mu, a=np.array(full))
+    assert abs(C.rexii_scalar(X, h, M, t)[0] - np.exp(1j * X)) < 1e-13
+
+
+def test_planner_refit_mu_scan(rexi):
+    mu, a, defect = rexi.fit_gaussian(24, None)
+    mu0, a0, d0 = rexi.fit_gaussian(24, -5.133333333333333)
+    assert -7.0 <= mu <= -3.0 and defect <= d0 * 1.5

@@ -479,3 +479,24 @@ def test_h_auto_c2(R):
     ref = lrsw.rexii_step(*g, 2.0, q.info["h"], q.info["M"])
     assert rel_l2(got, ref) < TOL
     assert rel_l2(got, lrsw.exact_step(*g, 2.0)) < 1e-8
+
+
+def test_refit_table_on_gpu(R):
+    """NEXT-2: a plan using the planner's least-squares refit of the Gaussian (instead of
+    Appendix A) reaches the same accuracy against the exact propagator; a smaller L (fewer
+    terms, N = M + L) works too."""
+    D, tau = 64, 1.0
+    f = inputs.white_noise(D)
+    t = [dev(x) for x in f]
+    ex = lrsw.exact_step(*f, tau)
+    p = R.Plan(D, tau, tol=1e-12)
+    base = [host(x) for x in p.apply(*t)]
+    mu, a, defect = R.fit_gaussian(24)
+    p.set_table(mu, a)
+    got = [host(x) for x in p.apply(*t)]
+    assert rel_l2(got, ex) < 1e-12 and rel_l2(base, ex) < 1e-12
+    mu20, a20, d20 = R.fit_gaussian(20, mu)
+    p.set_table(mu20, a20)
+    assert p.n_poles == p.info["M"] + 21
+    got20 = [host(x) for x in p.apply(*t)]
+    assert rel_l2(got20, ex) < max(1e-10, 100 * d20)

@@ -218,3 +218,27 @@ def test_h_for_tol_meets_tol_scalar(tol):
     assert err < tol
     if tol >= 1e-8:
         assert h > 1.4 and M < 0.5 * C.M_rule(xmax, 0.5, C.m0_for_tol(tol, 0.5))
+
+
+def test_oracle_refit_procedure_G18():
+    """NEXT-2: the paper's l2 fit on Leja points (reading G18), done in fp64 (numpy lstsq; the
+    system is ill-conditioned, so fp64 costs ~1 digit against the extended-precision planner fit,
+    which meets the paper's "< 8e-15", test_capi_host.py): small defect on the core, small tail,
+    and its REXII reproduces e^{ix} at the Fig. 1 threshold."""
+    mu = float(C.MU_APPENDIX_A)
+    a = C.fit_rational_gaussian(24, mu)
+    x = np.linspace(-30, 30, 20001)
+    assert np.abs(C.R_complex_form(x, mu, a) - C.psi(1.0, x)).max() < 1e-13
+    xt = np.linspace(30, 1000, 20001)
+    assert np.abs(C.R_complex_form(xt, mu, a)).max() < 5e-14
+    assert a[24].imag == 0.0
+    _, a0, _ = C.appendix_a()
+    assert np.abs(a - a0).max() < 1e-2      # same mu and L: close to the printed table
+    h, X = 0.5, 30.0
+    M = C.M_rule(X, h)
+    t = C.rexii_terms(h, M, mu=mu, a=a)
+    assert abs(C.rexii_scalar(X, h, M, t)[0] - np.exp(1j * X)) < 3e-13
+    # fitting only the core [0, 30] leaves a tail that ruins the REXI sum (why xmax = 100)
+    b = C.fit_rational_gaussian(24, mu, K=100, xmax=30.0)
+    tb = C.rexii_terms(h, M, mu=mu, a=b)
+    assert abs(C.rexii_scalar(X, h, M, tb)[0] - np.exp(1j * X)) > 1e-11

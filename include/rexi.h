@@ -269,6 +269,29 @@ double rexi_h_for_tol(double tol);
  * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0. */
 long rexi_rule_M(int D, double tau, double tol, double h);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3: the scalar forms applied to a diagonalised operator A = V E V^{-1} with purely
+ * imaginary eigenvalues (eq:AisVEV..eq:REXI_VEV_DECOMP), e.g. a circulant
+ * finite-difference matrix diagonalised by the DFT (the test matrices A_1, A_2 of PAPER.md:381-388).
+ * A scalar plan holds the full-sum term table n = -N..N for (h, M) (Appendix A).
+ * rexi_scalar_apply computes, for j < n (device arrays; x real, in/out complex interleaved):
+ *     out_j = phase * r(i x_j) * in_j
+ *   REXI_SCALAR_REXII:  r = eq:modifiedRexi
+ *   REXI_SCALAR_REXI:   r = eq:originalRexi: per eigenvalue this is REXIE
+ *                       (eq:REXIE) when V is real
+ *   REXI_SCALAR_REXI_M: r = sum_n beta^Re_n / (i x + alpha_n): the eigen-coordinates of
+ *                       eq:originalREXImatrix for a real A, whose Re the caller takes on the vector
+ * Remark 1's shift is x_j -> x_j - nu/i and phase = e^{tau nu}. One block of
+ * 256 threads per eigenvalue (each term a complex shifted solve 1/(alpha_n + i x_j)). */
+typedef struct rexi_scalar_plan_s *rexi_scalar_plan_t;
+typedef enum { REXI_SCALAR_REXII = 0, REXI_SCALAR_REXI = 1, REXI_SCALAR_REXI_M = 2 } rexi_scalar_method_t;
+rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M, int device);
+rexi_status_t rexi_scalar_plan_destroy(rexi_scalar_plan_t plan);
+long rexi_scalar_plan_terms(rexi_scalar_plan_t plan);
+rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t plan, int method, long n, const double *x,
+                                const double *in, double *out, double phase_re, double phase_im,
+                                void *stream);
+
 const char *rexi_status_string(rexi_status_t status);
 const char *rexi_last_error(void);
 int rexi_abi_version(void);

@@ -255,6 +255,42 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     return REXI_OK;
 }
 
+int make_scalar_terms(std::vector<ScalarTerm> &out, double h, long M, std::vector<char> &err,
+                      const GaussTable *table) {
+    if (!(h > 0.0 && h < M_PI)) { set_err(err, "h must lie in (0, pi) (PAPER.md:98)"); return REXI_EINVAL; }
+    if (M < 12 || M > 50000000L) { set_err(err, "M must be in [12, 5e7]"); return REXI_EINVAL; }
+    const GaussTable T = table ? *table : appendix_a_table();
+    const int L = T.L;
+    const long N = M + L;
+    const ld hh = (ld)h, mu = T.mu, eh2 = std::exp(hh * hh);
+    std::vector<cld> b((size_t)(2 * M + 1));
+    for (long m = -M; m <= M; ++m) {
+        const ld ph = (ld)m * hh;
+        b[(size_t)(m + M)] = cld(eh2 * std::cos(ph), -eh2 * std::sin(ph));   // eq:bm
+    }
+    out.assign((size_t)(2 * N + 1), ScalarTerm{});
+    for (long n = -N; n <= N; ++n) {
+        const long L1 = std::max<long>(-L, n - M), L2 = std::min<long>(L, n + M);
+        cld c1(0, 0), c2(0, 0), bR(0, 0), bI(0, 0);
+        for (long k = L1; k <= L2; ++k) {
+            const cld ak = a_coeff(T, (int)k), bnk = b[(size_t)(n - k + M)];
+            c1 += ak.real() * bnk;
+            c2 += ak.imag() * bnk;
+            bR += ak * bnk.real();
+            bI += ak * bnk.imag();
+        }
+        c1 *= hh; c2 *= hh; bR *= hh; bI *= hh;
+        const cld C1 = c1 * hh * mu + c2 * hh * (ld)n;
+        ScalarTerm &t = out[(size_t)(n + N)];
+        t.ar = (double)(hh * mu);   t.ai = (double)(hh * (ld)n);
+        t.C1r = (double)C1.real();  t.C1i = (double)C1.imag();
+        t.c2r = (double)c2.real();  t.c2i = (double)c2.imag();
+        t.bRr = (double)bR.real();  t.bRi = (double)bR.imag();
+        t.bIr = (double)bI.real();  t.bIi = (double)bI.imag();
+    }
+    return REXI_OK;
+}
+
 }  // namespace rexi
 
 extern "C" int rexi_appendix_a(double *mu, double *a) {

@@ -68,6 +68,18 @@ struct Plan {
 int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vector<char> &err,
               int method = 0, const GaussTable *table = nullptr);
 
+// Full-sum term table n = -N..N for the scalar forms (NEXT-3): eq:modifiedRexi and
+// eq:originalRexi.
+struct ScalarTerm {
+    double ar, ai;      // alpha_n = h(mu + i n)
+    double C1r, C1i;    // c_{1,n} h mu + c_{2,n} h n
+    double c2r, c2i;    // c_{2,n}
+    double bRr, bRi;    // beta^Re_n
+    double bIr, bIi;    // beta^Im_n
+};
+int make_scalar_terms(std::vector<ScalarTerm> &out, double h, long M, std::vector<char> &err,
+                      const GaussTable *table = nullptr);
+
 long m0_for_tol(double tol, double h);
 double h_for_tol(double tol);
 

@@ -1,0 +1,162 @@
+// scalar.cu — NEXT-3: the rational approximations applied to a diagonalised operator.
+//
+// For A = V E V^{-1} with purely imaginary eigenvalues (eq:AisVEV..eq:REXI_VEV_DECOMP,
+// PAPER.md:232-259) every scalar form is evaluated per eigenvalue i x_j and multiplied into
+// the eigen-coordinates in_j of the vector: out_j = phase * r(i x_j) * in_j, with
+//   REXII  (eq:modifiedRexi):
+//       r = sum_{n=-N}^{N} (c_{1,n} h mu + c_{2,n}(x + h n)) / ((alpha_{-n} - i x)(alpha_n + i x)),
+//   REXI   (eq:originalRexi; REXIE, eq:REXIE, when V is real):
+//       r = sum_n Re(beta^Re_n / (i x + alpha_n)) + i Re(beta^Im_n / (i x + alpha_n)),
+//   REXI-M (the per-eigenvalue sum of eq:originalREXImatrix for a real A, before its Re):
+//       r = sum_n beta^Re_n / (i x + alpha_n)  (the caller takes Re of the vector afterwards).
+// A spectral shift (Remark 1) is the caller's x_j - nu and phase e^{tau nu}.
+// One block per eigenvalue, threads stride over the 2N+1 terms (each a complex shifted
+// "solve" 1/(alpha + i x)), fixed-order tree reduction.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/rexi.h"
+#include "kernels.cuh"
+#include "planner.h"
+
+using rexi::cd;
+using rexi::cmul;
+using rexi::mk;
+
+namespace {
+
+constexpr int kScalarBlock = 256;
+
+template <int METHOD>
+__global__ void __launch_bounds__(kScalarBlock) scalar_kernel(const rexi::ScalarTerm *__restrict__ t,
+                                                              long nt, const double *__restrict__ x,
+                                                              const cd *__restrict__ in, cd *out,
+                                                              cd phase) {
+    __shared__ cd red[kScalarBlock];
+    const long j = blockIdx.x;
+    const double xj = x[j];
+    cd acc = mk(0, 0);
+    for (long i = threadIdx.x; i < nt; i += kScalarBlock) {
+        const rexi::ScalarTerm T = t[i];
+        // d = alpha_n + i x ; 1/d = conj(d)/|d|^2
+        const cd d = mk(T.ar, T.ai + xj);
+        const double r = 1.0 / fma(d.x, d.x, d.y * d.y);
+        const cd q = mk(d.x * r, -d.y * r);
+        if (METHOD == REXI_SCALAR_REXII) {
+            // (alpha_{-n} - i x)(alpha_n + i x) = |alpha_n + i x|^2 for real x
+            const cd num = mk(fma(T.c2r, xj, T.C1r), fma(T.c2i, xj, T.C1i));
+            acc = mk(fma(num.x, r, acc.x), fma(num.y, r, acc.y));
+        } else if (METHOD == REXI_SCALAR_REXI) {
+            const cd a = cmul(mk(T.bRr, T.bRi), q), b = cmul(mk(T.bIr, T.bIi), q);
+            acc = mk(acc.x + a.x, acc.y + b.x);
+        } else {
+            const cd a = cmul(mk(T.bRr, T.bRi), q);
+            acc = mk(acc.x + a.x, acc.y + a.y);
+        }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kScalarBlock / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            red[threadIdx.x] = mk(red[threadIdx.x].x + red[threadIdx.x + s].x,
+                                  red[threadIdx.x].y + red[threadIdx.x + s].y);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = cmul(phase, cmul(red[0], in[j]));
+}
+
+}  // namespace
+
+struct rexi_scalar_plan_s {
+    int device = 0;
+    double h = 0;
+    long M = 0, N = 0;
+    rexi::ScalarTerm *d_terms = nullptr;
+    ~rexi_scalar_plan_s() {
+        if (d_terms) cudaFree(d_terms);
+    }
+};
+
+extern "C" {
+
+rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M, int device) {
+    if (!out) return REXI_EINVAL;
+    *out = nullptr;
+    std::vector<rexi::ScalarTerm> terms;
+    std::vector<char> err;
+    int st;
+    try {
+        st = rexi::make_scalar_terms(terms, h, M, err);
+    } catch (...) {
+        return REXI_ENOMEM;
+    }
+    if (st != REXI_OK) return (rexi_status_t)st;
+    rexi_scalar_plan_s *p = new (std::nothrow) rexi_scalar_plan_s();
+    if (!p) return REXI_ENOMEM;
+    p->device = device;
+    p->h = h;
+    p->M = M;
+    p->N = (long)(terms.size() - 1) / 2;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete p;
+        return REXI_ECUDA;
+    }
+    cudaError_t e = cudaMalloc((void **)&p->d_terms, sizeof(rexi::ScalarTerm) * terms.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_terms, terms.data(), sizeof(rexi::ScalarTerm) * terms.size(),
+                       cudaMemcpyHostToDevice);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        delete p;
+        return e == cudaErrorMemoryAllocation ? REXI_ENOMEM : REXI_ECUDA;
+    }
+    *out = p;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_scalar_plan_destroy(rexi_scalar_plan_t p) {
+    if (!p) return REXI_EINVAL;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(p->device);
+    delete p;
+    cudaSetDevice(prev);
+    return REXI_OK;
+}
+
+long rexi_scalar_plan_terms(rexi_scalar_plan_t p) { return p ? 2 * p->N + 1 : -1; }
+
+rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t p, int method, long n, const double *x,
+                                const double *in, double *out, double phase_re, double phase_im,
+                                void *stream) {
+    if (!p || n < 0 || (n > 0 && (!x || !in || !out))) return REXI_EINVAL;
+    if (method != REXI_SCALAR_REXII && method != REXI_SCALAR_REXI && method != REXI_SCALAR_REXI_M)
+        return REXI_EINVAL;
+    if (n == 0) return REXI_OK;
+    if (n > 0x7fffffffL) return REXI_EINVAL;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(p->device) != cudaSuccess) return REXI_ECUDA;
+    const long nt = 2 * p->N + 1;
+    const cd ph = cd{phase_re, phase_im};
+    const cd *cin = reinterpret_cast<const cd *>(in);
+    cd *cout = reinterpret_cast<cd *>(out);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (method == REXI_SCALAR_REXII)
+        scalar_kernel<REXI_SCALAR_REXII><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, cin, cout, ph);
+    else if (method == REXI_SCALAR_REXI)
+        scalar_kernel<REXI_SCALAR_REXI><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, cin, cout, ph);
+    else
+        scalar_kernel<REXI_SCALAR_REXI_M><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, cin, cout, ph);
+    cudaError_t e = cudaGetLastError();
+    cudaSetDevice(prev);
+    return e == cudaSuccess ? REXI_OK : REXI_ECUDA;
+}
+
+}  // extern "C"

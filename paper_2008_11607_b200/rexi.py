@@ -67,6 +67,12 @@ EXPORTS = {
                                          _dp, _dp, _dp]),
     "rexi_plan_set_table": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_double, _dp]),
     "rexi_rule_M": (ctypes.c_long, [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
+    "rexi_scalar_plan_create": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_double, ctypes.c_long,
+                                               ctypes.c_int]),
+    "rexi_scalar_plan_destroy": (ctypes.c_int, [_vp]),
+    "rexi_scalar_plan_terms": (ctypes.c_long, [_vp]),
+    "rexi_scalar_apply": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_long, _vp, _vp, _vp, ctypes.c_double,
+                                         ctypes.c_double, _vp]),
     "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rexi_last_error": (ctypes.c_char_p, []),
     "rexi_abi_version": (ctypes.c_int, []),
@@ -335,3 +341,42 @@ class Plan:
         _check(_lib.rexi_timing_read(self._h, ctypes.byref(ms), ctypes.byref(pl), ctypes.byref(tl)),
                "rexi_timing_read")
         return ms.value, pl.value, tl.value
+
+
+SCALAR_METHODS = {"rexii": 0, "rexi": 1, "rexi_m": 2}
+
+
+class ScalarPlan:
+    """NEXT-3: the scalar forms per eigenvalue of a diagonalised operator (rexi_scalar_apply)."""
+
+    def __init__(self, h, M, device=None):
+        torch = _torch()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._h = _vp()
+        _check(_lib.rexi_scalar_plan_create(ctypes.byref(self._h), float(h), int(M), self.device),
+               "rexi_scalar_plan_create")
+        self.n_terms = _lib.rexi_scalar_plan_terms(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.rexi_scalar_plan_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def apply(self, x, vec, method="rexii", phase=1.0 + 0.0j, out=None):
+        """out_j = phase * r(i x_j) * vec_j for float64 x and complex128 vec (CUDA tensors)."""
+        torch = _torch()
+        if x.dtype != torch.float64 or vec.dtype != torch.complex128 or x.shape != vec.shape \
+                or not (x.is_cuda and vec.is_cuda) or not (x.is_contiguous() and vec.is_contiguous()):
+            raise ValueError("x: contiguous float64, vec: contiguous complex128, same shape, CUDA")
+        out = torch.empty_like(vec) if out is None else out
+        stream = _vp(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(_lib.rexi_scalar_apply(self._h, SCALAR_METHODS[method], int(x.numel()), _vp(x.data_ptr()),
+                                      _vp(vec.data_ptr()), _vp(out.data_ptr()), float(complex(phase).real),
+                                      float(complex(phase).imag), stream), "rexi_scalar_apply")
+        return out

@@ -500,3 +500,58 @@ def test_refit_table_on_gpu(R):
     assert p.n_poles == p.info["M"] + 21
     got20 = [host(x) for x in p.apply(*t)]
     assert rel_l2(got20, ex) < max(1e-10, 100 * d20)
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_tau_zero_and_negative(R):
+    """tau = 0 gives the identity (to the approximation's r(0) error); a step of -tau undoes a
+    step of +tau (e^{-tau A} e^{tau A} = I; REXII is valid for both signs, eq:modifiedRexi)."""
+    D = 64
+    f = inputs.white_noise(D)
+    t = [dev(x) for x in f]
+    p0 = R.Plan(D, 0.0)
+    assert rel_l2([host(x) for x in p0.apply(*t)], f) < 1e-13
+    pp, pm = R.Plan(D, 0.7), R.Plan(D, -0.7)
+    back = pm.apply(*pp.apply(*t))
+    assert rel_l2([host(x) for x in back], f) < 1e-12
+    # and -tau matches the oracle too
+    ref = lrsw.rexii_step(*f, -0.7, pm.info["h"], pm.info["M"])
+    assert rel_l2([host(x) for x in pm.apply(*t)], ref) < TOL
+
+
+def test_zero_input_and_single_mode(R):
+    """Linear map: zero in, zero out; a single Fourier mode stays a single mode (per-mode solves,
+    PAPER.md:497), matching the exact propagator."""
+    D = 32
+    p = R.Plan(D, 1.0)
+    z = [dev(np.zeros((D, D))) for _ in range(3)]
+    assert max(float(x.abs().max()) for x in p.apply(*z)) == 0.0
+    X, Y = inputs.grid(D)
+    f = (np.sin(6 * np.pi * X) * np.cos(4 * np.pi * Y), np.zeros((D, D)), np.zeros((D, D)))
+    got = [host(x) for x in p.apply(*(dev(x) for x in f))]
+    assert rel_l2(got, lrsw.exact_step(*f, 1.0)) < 1e-12
+    Fg = np.fft.fft2(got[0])
+    Fg[np.abs(Fg) < 1e-9 * np.abs(Fg).max()] = 0
+    assert set(zip(*np.nonzero(Fg))) <= {(l % D, k % D) for l in (2, -2) for k in (3, -3)}
+
+
+def test_max_grid_8192_small_tau(R):
+    """Largest supported grid (D = 8192, 67M modes, 3.2 GB per spectral array): a short step
+    conserves energy and the mean of eta; the forward FFT matches the DFT on sampled entries."""
+    import torch
+    D = 8192
+    p = R.Plan(D, 0.002, tol=1e-10)
+    g = np.random.Generator(np.random.PCG64(4))
+    X = g.standard_normal((D, D))
+    t = [torch.from_numpy(X).cuda(), torch.zeros((D, D), dtype=torch.float64, device="cuda"),
+         torch.zeros((D, D), dtype=torch.float64, device="cuda")]
+    F0 = host(p.forward(*t)[0])
+    x = np.arange(D)
+    for (l, k) in [(0, 0), (1, 4095), (4096, 4096), (8191, 3)]:
+        ph = np.exp(-2j * np.pi * ((k * x[None, :] + l * x[:, None]) % D) / D)
+        assert abs(F0[l, k] - (X * ph).sum() / D ** 2) < 1e-15
+    out = p.apply(*t)
+    e0 = float((t[0] ** 2).sum())
+    e1 = sum(float((o ** 2).sum()) for o in out)
+    assert abs(e1 - e0) / e0 < 1e-10
+    assert abs(float(out[0].mean()) - float(t[0].mean())) < 1e-13

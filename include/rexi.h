@@ -131,7 +131,7 @@ typedef struct {
  *  h:      in (0, pi); h <= 0 selects 0.5; h == REXI_H_AUTO selects
  *          rexi_h_for_tol(tol) (NEXT-2: fewer poles at loose tolerances).
  *  M:      > 0: use this M (must be >= 12); <= 0: M from the rule
- *          tau rho(A) <= (M - m0) h (eq:matrixAccuracyBound).
+ *          tau rho(A) <= (M - m0) h (eq:matrixAccuracyBound), at least 12.
  *  device: CUDA device ordinal.
  * Allocates the pole table and all workspace on `device`; synchronous.
  * Errors: EINVAL (arguments), ENOMEM, ECUDA. *out is NULL on error. */
@@ -266,7 +266,8 @@ int rexi_fit_gaussian(int L, double mu, int K, double xmax, double *a_out, doubl
 double rexi_h_for_tol(double tol);
 
 /* Host-only (no GPU needed): the term-count rule used by rexi_plan_create:
- * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0. */
+ * m0(tol, h) (tol <= 0: 11) and M = ceil(|tau| sqrt(2) pi D / h) + m0 (rexi_plan_create raises
+ * a result below 12 to 12). */
 long rexi_rule_M(int D, double tau, double tol, double h);
 
 /* ---------------------------------------------------------------------------------------

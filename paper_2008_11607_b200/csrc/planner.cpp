@@ -123,6 +123,7 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     if (M <= 0) {
         double x = std::fabs(tau) * p.rho;                 // eq:matrixAccuracyBound
         M = (long)std::ceil(x / h) + p.m0;
+        if (M < 12) M = 12;   // tiny |tau| rho: at least M - 11 >= 1 (eq:Mformula)
     }
     if (M < 12) { set_err(err, "M must be >= 12 (eq:Mformula needs M - 11 >= 1)"); return REXI_EINVAL; }
     if (M > 50000000L) { set_err(err, "M too large"); return REXI_EINVAL; }

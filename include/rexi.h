@@ -144,7 +144,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t plan, rexi_plan_info_t *info);
 rexi_status_t rexi_plan_set_variant(rexi_plan_t plan, int variant);
 
 /* Select the method (rexi_method_t); rebuilds and uploads the term table for the plan's
- * (h, M) (synchronous: waits for the device). EINVAL for unknown values. */
+ * (h, M) (synchronous: waits for the device). EINVAL for unknown values, and for REXI on a
+ * tau = 0 plan. (A REXII plan with tau = 0 always runs the UV variant: all symbols vanish.) */
 rexi_status_t rexi_plan_set_method(rexi_plan_t plan, int method);
 
 /* Replace the plan's rational approximation of the Gaussian (default: Appendix A) by

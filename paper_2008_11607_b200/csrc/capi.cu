@@ -63,6 +63,8 @@ struct rexi_plan_s {
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
     int kind() const {
         if (method == REXI_METHOD_REXI) return 2;
+        // tau = 0: every symbol vanishes, (delta, zeta) carry no velocity anywhere -> UV route
+        if (host.tau == 0.0) return 1;
         switch (variant) {
             case REXI_VARIANT_UV: return 1;
             case REXI_VARIANT_DZ3: return 3;
@@ -599,6 +601,8 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t p, int method) {
     return guarded(p, [&]() -> rexi_status_t {
         if (method != REXI_METHOD_REXII && method != REXI_METHOD_REXI)
             return fail(REXI_EINVAL, "unknown method");
+        if (method == REXI_METHOD_REXI && p->host.tau == 0.0)
+            return fail(REXI_EINVAL, "REXI method needs tau != 0 (its kernel back-substitutes in delta, zeta)");
         if (method == p->method) return REXI_OK;
         rexi::Plan np;
         std::vector<char> err;

@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", default="pfhr", choices=["pfhr", "pfh", "pf", "dz", "dz3", "uv"])
     ap.add_argument("--h", default="0.5", help="Gaussian spacing h, or 'auto' (NEXT-2 h_for_tol)")
+    ap.add_argument("--tuning", default=None,
+                    help="pole kernel tuning 'modes_per_thread,poles_per_iter,min_blocks' (default: plan's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -223,6 +225,8 @@ def main():
     D, tau, tol, scen, cidx = CONFIGS[args.config]
     h_arg = "auto" if args.h == "auto" else float(args.h)
     plan = rexi.Plan(D, tau, tol=tol, h=h_arg, device=local, variant=args.variant)
+    if args.tuning:
+        plan.set_tuning(*[int(x) for x in args.tuning.split(",")])
     info = plan.info
     n_poles = info["n_poles"]
     pb, pe = pole_partition(n_poles, world, rank)
@@ -335,7 +339,7 @@ def main():
             "config": {"workload": f"{args.config}: LRSW {D}x{D}, tau={tau}, tol={tol}, "
                                    f"h={info['h']:.4g}, M={info['M']}, {n_poles} poles, {scen} scenario "
                                    f"(BASELINE configs[{cidx}])",
-                       "variant": args.variant, "l2": "flushed between timed steps (256 MB write)",
+                       "variant": args.variant, "tuning": args.tuning or "default", "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"poles split over {world} GPU(s)"},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,

@@ -401,7 +401,7 @@ struct PairState {
     cd H0, H1;               // Hermitian accumulators: eta, delta' (before the e0 term)
 };
 
-template <int PU, int MINB>
+template <int PU, int MINB, int NQ>
 __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
@@ -411,33 +411,43 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
     const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
     const double c = a.tau;
     const double hmu = a.hmu;
-    const long q = (long)blockIdx.x * kPoleBlock + threadIdx.x;
-    const bool ok = q > 0 && q < (n_modes >> 2);   // quad 0 = the four K = 0 corners
-    long mq[4];
-    quad_modes(ok ? q : 1, a.D, a.log2D, mq);
-    // representatives: interior quads pair (0,3) and (1,2); axis / Nyquist quads (0,1), (2,3)
     const int H = a.D >> 1;
-    const int qa = (int)((ok ? q : 1) >> (a.log2D - 1)), qb = (int)((ok ? q : 1) & (H - 1));
-    const long rep[2] = {mq[0], (qa > 0 && qb > 0) ? mq[1] : mq[2]};
-    PairState st[2];
-    double K2 = 0.0;
+    // NQ K2 quads per thread (quad q = blockIdx.x * 128 NQ + g * 128 + tid); quad 0 = the four
+    // K = 0 corners, left to the fix-up kernel
+    long rep[2 * NQ];
+    bool ok[NQ];
+    double K2[NQ];
+    PairState st[2 * NQ];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const long mm = rep[j];
-        const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
-        const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
-        const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
-        const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
-        const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
-        PairState &s = st[j];
-        s.e0 = e;
-        s.d0 = d;
-        s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
-        s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
-        s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
-        s.H0 = mk(0, 0);
-        s.H1 = mk(0, 0);
-        K2 = fma(kx, kx, ky * ky);
+    for (int g = 0; g < NQ; ++g) {
+        const long q = (long)blockIdx.x * (kPoleBlock * NQ) + g * kPoleBlock + threadIdx.x;
+        ok[g] = q > 0 && q < (n_modes >> 2);
+        const long qs = ok[g] ? q : 1;
+        long mq[4];
+        quad_modes(qs, a.D, a.log2D, mq);
+        // representatives: interior quads pair (0,3) and (1,2); axis / Nyquist quads (0,1), (2,3)
+        const int qa = (int)(qs >> (a.log2D - 1)), qb = (int)(qs & (H - 1));
+        rep[2 * g] = mq[0];
+        rep[2 * g + 1] = (qa > 0 && qb > 0) ? mq[1] : mq[2];
+        K2[g] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const long mm = rep[2 * g + j];
+            const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
+            const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
+            const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
+            const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
+            const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
+            PairState &s = st[2 * g + j];
+            s.e0 = e;
+            s.d0 = d;
+            s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+            s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
+            s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+            s.H0 = mk(0, 0);
+            s.H1 = mk(0, 0);
+            K2[g] = fma(kx, kx, ky * ky);
+        }
     }
 
     for (long pt = p0; pt < p1; pt += kPoleTile) {
@@ -453,33 +463,39 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
 #pragma unroll PU
         for (int qq = 0; qq < cnt; ++qq) {
             const PoleConst &P = sp[qq];
-            const cd qd = pole_den(P, K2);
             const cd s2 = mk(P.s2r, P.s2i);
             const double hn = P.ai;
-            // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, per quad)
-            const cd W1q = cmul(mk(P.W1r, P.W1i), qd), P1q = cmul(mk(P.P1r, P.P1i), qd);
-            const cd sig = cjfms(mk(P.W2r, P.W2i), qd, mk(W1q.x, -W1q.y));
-            const cd tau = cjfms(mk(P.P2r, P.P2i), qd, mk(P1q.x, -P1q.y));
             const cd X1 = mk(P.X1r, P.X1i), X2 = mk(P.X2r, P.X2i);
             const cd Y1 = mk(P.Y1r, P.Y1i), Y2 = mk(P.Y2r, P.Y2i);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                PairState &s = st[j];
-                const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
-                const cd eta1 = cmul(cfms(s2, s.m0, t), qd);
-                const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
-                const cd etat = cjfma(qd, cjfms(s2, s.m0, tt), mk(0, 0));
-                s.H0 = cfma(sig, s.d0, cfma(X2, etat, cfma(X1, eta1, s.H0)));
-                s.H1 = cfma(tau, s.d0, cfma(Y2, etat, cfma(Y1, eta1, s.H1)));
+            for (int g = 0; g < NQ; ++g) {
+                const cd qd = pole_den(P, K2[g]);
+                // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, quad)
+                const cd W1q = cmul(mk(P.W1r, P.W1i), qd), P1q = cmul(mk(P.P1r, P.P1i), qd);
+                const cd sig = cjfms(mk(P.W2r, P.W2i), qd, mk(W1q.x, -W1q.y));
+                const cd tau = cjfms(mk(P.P2r, P.P2i), qd, mk(P1q.x, -P1q.y));
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    PairState &s = st[2 * g + j];
+                    const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
+                    const cd eta1 = cmul(cfms(s2, s.m0, t), qd);
+                    const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
+                    const cd etat = cjfma(qd, cjfms(s2, s.m0, tt), mk(0, 0));
+                    s.H0 = cfma(sig, s.d0, cfma(X2, etat, cfma(X1, eta1, s.H0)));
+                    s.H1 = cfma(tau, s.d0, cfma(Y2, etat, cfma(Y1, eta1, s.H1)));
+                }
             }
         }
     }
-    if (ok) {
-        cd *out = a.partial + (size_t)chunk * 3 * n_modes;
+    cd *out = a.partial + (size_t)chunk * 3 * n_modes;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            out[rep[j]] = st[j].H0;
-            out[n_modes + rep[j]] = st[j].H1;
+    for (int g = 0; g < NQ; ++g) {
+        if (ok[g]) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                out[rep[2 * g + j]] = st[2 * g + j].H0;
+                out[n_modes + rep[2 * g + j]] = st[2 * g + j].H1;
+            }
         }
     }
 }
@@ -876,25 +892,33 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
     return cudaErrorInvalidValue;
 }
 
-bool pole_r2c_supported(int pu, int minb) {
-    return (pu == 1 && (minb == 4 || minb == 5 || minb == 6)) || (pu == 2 && (minb == 3 || minb == 4));
+// R2C pair kernel instantiations: (quads per thread NQ, poles per loop trip PU, min blocks).
+#define REXI_R2C_CONFIGS(X) \
+    X(1, 1, 4) X(1, 1, 5) X(1, 1, 6) X(1, 2, 3) X(1, 2, 4) X(2, 1, 2) X(2, 1, 3) X(2, 2, 2)
+
+bool pole_r2c_supported(int nq, int pu, int minb) {
+#define X(Q, U, B) if (nq == Q && pu == U && minb == B) return true;
+    REXI_R2C_CONFIGS(X)
+#undef X
+    return false;
 }
 
-cudaError_t pole_r2c_occupancy(int pu, int minb, int *blocks_per_sm) {
-#define OCC(U, B) if (pu == U && minb == B) \
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2c<U, B>, kPoleBlock, 0);
-    OCC(1, 4) OCC(1, 5) OCC(1, 6) OCC(2, 3) OCC(2, 4)
-#undef OCC
+cudaError_t pole_r2c_occupancy(int nq, int pu, int minb, int *blocks_per_sm) {
+#define X(Q, U, B) if (nq == Q && pu == U && minb == B) \
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2c<U, B, Q>, kPoleBlock, 0);
+    REXI_R2C_CONFIGS(X)
+#undef X
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_poles_r2c(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
+cudaError_t launch_poles_r2c(const PoleArgs &a, int nq, int pu, int minb, cudaStream_t st) {
     const long quads = a.n_modes >> 2;
-    dim3 grid((unsigned)((quads + kPoleBlock - 1) / kPoleBlock), (unsigned)a.n_chunks);
-#define LAUNCH(U, B) if (pu == U && minb == B) { \
-    pole_kernel_r2c<U, B><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
-    LAUNCH(1, 4) LAUNCH(1, 5) LAUNCH(1, 6) LAUNCH(2, 3) LAUNCH(2, 4)
-#undef LAUNCH
+    const long per_block = (long)kPoleBlock * nq;
+    dim3 grid((unsigned)((quads + per_block - 1) / per_block), (unsigned)a.n_chunks);
+#define X(Q, U, B) if (nq == Q && pu == U && minb == B) { \
+    pole_kernel_r2c<U, B, Q><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
+    REXI_R2C_CONFIGS(X)
+#undef X
     return cudaErrorInvalidValue;
 }
 

@@ -17,9 +17,9 @@ bool pole_config_supported(int variant, int mpt, int pu, int minb);
 cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_per_sm);
 cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st);
-bool pole_r2c_supported(int pu, int minb);
-cudaError_t pole_r2c_occupancy(int pu, int minb, int *blocks_per_sm);
-cudaError_t launch_poles_r2c(const PoleArgs &a, int pu, int minb, cudaStream_t st);
+bool pole_r2c_supported(int nq, int pu, int minb);
+cudaError_t pole_r2c_occupancy(int nq, int pu, int minb, int *blocks_per_sm);
+cudaError_t launch_poles_r2c(const PoleArgs &a, int nq, int pu, int minb, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 

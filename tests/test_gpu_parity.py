@@ -435,15 +435,16 @@ def test_run_spectral_resident_matches_repeated_apply(R, graphs):
 
 
 
-@pytest.mark.parametrize("pu,minb", [(1, 4), (1, 5), (1, 6), (2, 3), (2, 4)])
+@pytest.mark.parametrize("mpt,pu,minb", [(4, 1, 4), (4, 1, 5), (4, 1, 6), (4, 2, 3), (4, 2, 4),
+                                         (8, 1, 2), (8, 1, 3), (8, 2, 2)])
 @pytest.mark.parametrize("D", [4, 8, 32, 64])
-def test_pfhr_tunings_vs_oracle(R, pu, minb, D):
+def test_pfhr_tunings_vs_oracle(R, mpt, pu, minb, D):
     """R2C-pair kernel (real input): every tuning vs the oracle step, grids with every quad type
     (corner, axis, Nyquist, interior) and ragged tiles."""
     tau = 0.9
     f = inputs.white_noise(D)
     p = R.Plan(D, tau, variant="pfhr")
-    p.set_tuning(4, pu, minb)
+    p.set_tuning(mpt, pu, minb)
     got = [host(t) for t in p.apply(*(dev(x) for x in f))]
     info = p.info
     ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])

@@ -57,7 +57,7 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 2}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 3}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
     int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
@@ -206,26 +206,24 @@ rexi_status_t do_forward(rexi_plan_s *p, const double *eta, const double *u, con
                          cd *fhat, cudaStream_t st) {
     const long n = p->n_modes;
     const int D = p->host.D;
-    const void *in[3] = {eta, u, v};
-    void *mid[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
-    const void *mid_c[3] = {mid[0], mid[1], mid[2]};
-    void *out[3] = {fhat, fhat + n, fhat + 2 * n};
-    CK(rexi::launch_fft_rows(in, mid, true, false, p->d_tw, D, 0, 1.0, st));
-    CK(rexi::launch_fft_cols(mid_c, out, p->d_tw, D, 0, 1.0 / ((double)D * (double)D), st));
+    const double *in[3] = {eta, u, v};
+    cd *half[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
+    cd *out[3] = {fhat, fhat + n, fhat + 2 * n};
+    CK(rexi::launch_fft_forward(in, half, out, p->d_tw, D, 1.0 / ((double)D * (double)D), st));
     p->launches += 2;
     return REXI_OK;
 }
 
+// hermitian: acc is known to be a Hermitian spectrum (the R2C accumulator, or a spectrum after
+// the Re projection), so the inverse skips the symmetrisation loads.
 rexi_status_t do_inverse(rexi_plan_s *p, const cd *acc, double *eta, double *u, double *v,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool hermitian = false) {
     const long n = p->n_modes;
     const int D = p->host.D;
-    const void *in[3] = {acc, acc + n, acc + 2 * n};
-    void *mid[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
-    const void *mid_c[3] = {mid[0], mid[1], mid[2]};
-    void *out[3] = {eta, u, v};
-    CK(rexi::launch_fft_cols(in, mid, p->d_tw, D, 1, 1.0, st));
-    CK(rexi::launch_fft_rows(mid_c, out, false, true, p->d_tw, D, 1, 1.0, st));
+    const cd *in[3] = {acc, acc + n, acc + 2 * n};
+    cd *half[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
+    double *out[3] = {eta, u, v};
+    CK(rexi::launch_fft_inverse(in, half, out, hermitian, p->d_tw, D, st));
     p->launches += 2;
     return REXI_OK;
 }
@@ -358,7 +356,7 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
     rexi_status_t s;
     if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
     if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
-    return do_inverse(p, p->d_acc, eo, uo, vo, st);
+    return do_inverse(p, p->d_acc, eo, uo, vo, st, p->kind() == 6);
 }
 
 // One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
@@ -771,7 +769,7 @@ rexi_status_t rexi_run(rexi_plan_t p, int steps, double *eta, double *u, double 
         if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
         for (int k = 0; k < steps; ++k)
             if ((s = do_spectral_step(p, 0, N1, st)) != REXI_OK) return s;
-        return do_inverse(p, p->d_fhat, eta, u, v, st);
+        return do_inverse(p, p->d_fhat, eta, u, v, st, true);
     });
 }
 

@@ -1,7 +1,7 @@
 // kernels.cu — device kernels of librexi (sm_100a, fp64).
 //
-//  * fft_rows_kernel / fft_cols_kernel : batched radix-2 FFT passes in shared memory
-//    (S1 forward transform, S5 inverse transform + Re). PAPER.md:497 "all computations
+//  * fft_{rows,cols}_{fwd,inv}_kernel : real 2-D FFT by batched radix-8 Stockham passes in
+//    shared memory (S1 forward transform, S5 inverse transform + Re). PAPER.md:497 "all computations
 //    ... in Fourier space"; Alg. 1 lines 1 and last.
 //  * pole_kernel<VARIANT>             : S2 + S3, the fused per-mode two-solve REXII pole
 //    loop with the weighted accumulation in registers (eq:lswEta,
@@ -81,6 +81,28 @@ __device__ __forceinline__ void dftR(cd *v) {
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
 __host__ __device__ __forceinline__ int padded_len(int N) { return N + (N >> 3); }
 
+// Twiddles w_r = e^{-+2 pi i r step / N}, r = 1..R-1, of one butterfly: w_1, w_2, w_4 from the
+// table (e^{-2 pi i j / N}, j < N), the others as products of two or three of them (<= 3 ulp;
+// the table loads through L1 were the FFT's limiter with one load per r).
+template <int R, bool INV>
+__device__ __forceinline__ void pass_twiddles(const cd *__restrict__ tw, int step, cd *w) {
+    const double2 *t = reinterpret_cast<const double2 *>(tw);
+    const double2 a = __ldg(t + step);
+    w[1] = mk(a.x, INV ? -a.y : a.y);
+    if (R >= 4) {
+        const double2 b = __ldg(t + 2 * step);
+        w[2] = mk(b.x, INV ? -b.y : b.y);
+        w[3] = cmul(w[1], w[2]);
+    }
+    if (R == 8) {
+        const double2 c4 = __ldg(t + 4 * step);
+        w[4] = mk(c4.x, INV ? -c4.y : c4.y);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+    }
+}
+
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
 template <int R, bool INV>
@@ -95,14 +117,12 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
         if (b * tf < nbf && j < nbf) {
             const int k = j & (Ns - 1);
             const int step = k * (N / (Ns * R));  // twiddle index step: r * k * N / (Ns R)
+            cd w[R];
+            if (Ns > 1) pass_twiddles<R, INV>(tw, step, w);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 cd x = s[pidx(j + r * nbf)];
-                if (r > 0 && Ns > 1) {
-                    const double2 w2 = __ldg(reinterpret_cast<const double2 *>(tw) + ((r * step) & (N - 1)));
-                    const cd w = mk(w2.x, INV ? -w2.y : w2.y);
-                    x = cmul(x, w);
-                }
+                if (r > 0 && Ns > 1) x = cmul(x, w[r]);
                 v[b * R + r] = x;
             }
         }
@@ -134,29 +154,43 @@ __device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int t
     else if (rem == 1) stockham_pass<2, INV>(s, N, logN, Ns, t, tf, tw);
 }
 
-// Row pass: block = nb consecutive rows of one field; threads = nb * tf, tf = max(1, D/8).
-template <bool INV, bool REAL_IN, bool REAL_OUT>
-__global__ void __launch_bounds__(1024) fft_rows_kernel(FftArgs a) {
+// ----------------------------------------------------------------------------- real 2-D FFT
+// The physical fields are real, so both 2-D transforms use the two Hermitian symmetries
+// (half the butterflies and half the shared-memory traffic of a complex 2-D FFT):
+//  * rows: two real rows x1, x2 are transformed as one complex row z = x1 + i x2;
+//    X1[k] = (Z[k] + conj Z[N-k]) / 2, X2[k] = (Z[k] - conj Z[N-k]) / (2i).
+//  * half spectrum: a row's X[k] for k in [1, N/2) plus the two real values X[0], X[N/2]
+//    packed into slot 0 as (X[0], X[N/2]) — N/2 complex slots per row.
+//  * columns: only the N/2 columns of the half spectrum are transformed; slot 0 holds two real
+//    columns packed as one complex column and is separated with the same rule along l.
+// Shared memory: one transform per padded slab (pidx); column slabs are padded so that the 8
+// lanes of a 128-bit shared-memory wavefront (C columns x 8/C rows) hit distinct bank groups.
+
+__host__ __device__ __forceinline__ int col_stride(int N, int C) { return padded_len(N) + (C < 8 ? 8 / C : 1); }
+
+// Forward rows: real fields -> half spectra. Block = nb row pairs of one field, tf = N/8 threads
+// per pair.
+__global__ void __launch_bounds__(1024) fft_rows_fwd_kernel(FftArgs a) {
     extern __shared__ cd smem[];
     const int f = blockIdx.y;
     const int D = a.D, log2D = a.log2D, nb = a.per_block;
     const int tf = D >= 8 ? D / 8 : 1;
-    const size_t row0 = (size_t)blockIdx.x * nb;
-    const int n = nb * D;
-    const void *inp = f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2];
-    void *outp = f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2];
-    // every thread moves exactly 8 values (4 when D = 4): unrolled so all loads are in flight
+    const int H = D >> 1;
+    const size_t pair0 = (size_t)blockIdx.x * nb;
+    const int n = nb * D;   // complex values in the block
+    const double *inp = static_cast<const double *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *outp = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    const int PL = padded_len(D);
     cd tmp[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
         if (i < n) {
-            const size_t g = row0 * D + i;
-            tmp[q] = REAL_IN ? mk(__ldg(static_cast<const double *>(inp) + g), 0.0)
-                             : static_cast<const cd *>(inp)[g];
+            const int pr = i >> log2D, x = i & (D - 1);
+            const size_t g = (2 * (pair0 + pr)) * D + x;
+            tmp[q] = mk(__ldg(inp + g), __ldg(inp + g + D));
         }
     }
-    const int PL = padded_len(D);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
@@ -164,31 +198,39 @@ __global__ void __launch_bounds__(1024) fft_rows_kernel(FftArgs a) {
     }
     __syncthreads();
     const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
-    fft_in_smem<INV>(smem + row * PL, D, log2D, t, tf, a.twiddle);
-    const double sc = a.scale;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) {
-            const size_t g = row0 * D + i;
-            const cd v = smem[(i >> log2D) * PL + pidx(i & (D - 1))];
-            if (REAL_OUT) static_cast<double *>(outp)[g] = v.x * sc;
-            else static_cast<cd *>(outp)[g] = mk(v.x * sc, v.y * sc);
+    fft_in_smem<false>(smem + row * PL, D, log2D, t, tf, a.twiddle);
+    const double hs = 0.5 * a.scale;
+    // half-spectrum outputs: nb pairs x H slots x 2 rows
+    const int m = nb * H;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int pr = i / H, k = i - pr * H;
+        const cd *Z = smem + pr * PL;
+        cd X1, X2;
+        if (k == 0) {
+            const cd z0 = Z[pidx(0)], zh = Z[pidx(H)];
+            X1 = mk(2.0 * hs * z0.x, 2.0 * hs * zh.x);
+            X2 = mk(2.0 * hs * z0.y, 2.0 * hs * zh.y);
+        } else {
+            const cd zk = Z[pidx(k)], zm = Z[pidx(D - k)];
+            X1 = mk(hs * (zk.x + zm.x), hs * (zk.y - zm.y));
+            X2 = mk(hs * (zk.y + zm.y), hs * (zm.x - zk.x));
         }
+        const size_t g = (2 * (pair0 + pr)) * D + k;
+        outp[g] = X1;
+        outp[g + D] = X2;
     }
 }
 
-// Column pass: block = nb adjacent columns (a strip) of one field; smem column-major with the
-// column stride padded to D + 1.
-template <bool INV>
-__global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
+// Forward columns: half spectra -> full spectrum (scaled). Block = C adjacent slots of one
+// field; slot 0 is the packed (X[.][0], X[.][N/2]) pair of real columns.
+__global__ void __launch_bounds__(1024) fft_cols_fwd_kernel(FftArgs a) {
     extern __shared__ cd smem[];
     const int f = blockIdx.y;
     const int D = a.D, log2D = a.log2D, C = a.per_block;
     const int logC = __ffs(C) - 1;
     const int tf = D >= 8 ? D / 8 : 1;
-    const int stride = padded_len(D) + 1;
-    const size_t col0 = (size_t)blockIdx.x * C;
+    const int stride = col_stride(D, C);
+    const int col0 = blockIdx.x * C;
     const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int n = C << log2D;
@@ -205,7 +247,77 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
     }
     __syncthreads();
     const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
-    fft_in_smem<INV>(smem + col * stride, D, log2D, t, tf, a.twiddle);
+    fft_in_smem<false>(smem + col * stride, D, log2D, t, tf, a.twiddle);
+    const double sc = a.scale;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i >> logC, c = i & (C - 1);
+        const int k = col0 + c;
+        const int lm = (D - l) & (D - 1);
+        const cd v = smem[c * stride + pidx(l)];
+        if (k == 0) {
+            // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
+            // FH = (G - conj G(-l)) / (2i)
+            const cd w = smem[c * stride + pidx(lm)];
+            const double hs = 0.5 * sc;
+            out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+            out[(size_t)l * D + (D >> 1)] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+        } else {
+            out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+            out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
+        }
+    }
+}
+
+// Inverse columns: spectrum -> half-spectrum rows of Re(IDFT). SYM: symmetrise on load,
+// T(K) = (S(K) + conj S(-K)) / 2, so Re(IDFT S) = IDFT T for any complex S; without SYM the
+// input must already be Hermitian (the R2C finish writes the Hermitian part). Slot 0 carries
+// the two self-mirror columns k = 0 and k = N/2 packed: IDFT(T0 + i TH) = x0 + i xH.
+template <bool SYM>
+__global__ void __launch_bounds__(1024) fft_cols_inv_kernel(FftArgs a) {
+    extern __shared__ cd smem[];
+    const int f = blockIdx.y;
+    const int D = a.D, log2D = a.log2D, C = a.per_block;
+    const int logC = __ffs(C) - 1;
+    const int tf = D >= 8 ? D / 8 : 1;
+    const int stride = col_stride(D, C);
+    const int col0 = blockIdx.x * C;
+    const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    const int n = C << log2D;
+    const int H = D >> 1;
+    cd tmp[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) {
+            const int l = i >> logC, k = col0 + (i & (C - 1));
+            const int lm = (D - l) & (D - 1);
+            if (k == 0) {
+                cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
+                if (SYM) {
+                    const cd m0 = in[(size_t)lm * D], mh = in[(size_t)lm * D + H];
+                    t0 = mk(0.5 * (t0.x + m0.x), 0.5 * (t0.y - m0.y));
+                    th = mk(0.5 * (th.x + mh.x), 0.5 * (th.y - mh.y));
+                }
+                tmp[q] = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+            } else {
+                cd t = in[(size_t)l * D + k];
+                if (SYM) {
+                    const cd m = in[(size_t)lm * D + (D - k)];
+                    t = mk(0.5 * (t.x + m.x), 0.5 * (t.y - m.y));
+                }
+                tmp[q] = t;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
+    }
+    __syncthreads();
+    const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
+    fft_in_smem<true>(smem + col * stride, D, log2D, t, tf, a.twiddle);
     const double sc = a.scale;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -214,6 +326,50 @@ __global__ void __launch_bounds__(1024) fft_cols_kernel(FftArgs a) {
             const int r = i >> logC, c = i & (C - 1);
             const cd v = smem[c * stride + pidx(r)];
             out[(size_t)r * D + col0 + c] = mk(v.x * sc, v.y * sc);
+        }
+    }
+}
+
+// Inverse rows: half-spectrum rows -> real fields, two rows per complex transform:
+// Z[k] = g1[k] + i g2[k] over the full circle (g[N-k] = conj g[k]), IDFT(Z) = x1 + i x2.
+__global__ void __launch_bounds__(1024) fft_rows_inv_kernel(FftArgs a) {
+    extern __shared__ cd smem[];
+    const int f = blockIdx.y;
+    const int D = a.D, log2D = a.log2D, nb = a.per_block;
+    const int tf = D >= 8 ? D / 8 : 1;
+    const int H = D >> 1;
+    const size_t pair0 = (size_t)blockIdx.x * nb;
+    const cd *inp = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    double *outp = static_cast<double *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    const int PL = padded_len(D);
+    const int m = nb * H;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int pr = i / H, k = i - pr * H;
+        const size_t g = (2 * (pair0 + pr)) * D + k;
+        const cd g1 = inp[g], g2 = inp[g + D];
+        cd *Z = smem + pr * PL;
+        if (k == 0) {
+            Z[pidx(0)] = mk(g1.x, g2.x);
+            Z[pidx(H)] = mk(g1.y, g2.y);
+        } else {
+            Z[pidx(k)] = mk(g1.x - g2.y, g1.y + g2.x);        // g1 + i g2
+            Z[pidx(D - k)] = mk(g1.x + g2.y, g2.x - g1.y);    // conj g1 + i conj g2
+        }
+    }
+    __syncthreads();
+    const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
+    fft_in_smem<true>(smem + row * PL, D, log2D, t, tf, a.twiddle);
+    const double sc = a.scale;
+    const int n = nb * D;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = threadIdx.x + q * blockDim.x;
+        if (i < n) {
+            const int pr = i >> log2D, x = i & (D - 1);
+            const cd v = smem[pr * PL + pidx(x)];
+            const size_t g = (2 * (pair0 + pr)) * D + x;
+            outp[g] = v.x * sc;
+            outp[g + D] = v.y * sc;
         }
     }
 }
@@ -738,11 +894,17 @@ __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        a.acc[n + m] = red[0][0];
-        a.acc[2 * n + m] = red[1][0];
-        // R2C kind: the pole kernel skips the corners; at K = 0, eta1 = e0/alpha and
-        // eta2 = eta1/conj(alpha), so sum(w1 eta1 + w2 eta2) = S e0 with the finish-kernel S.
-        if (a.write_eta) a.acc[m] = cmul(a.S, a.fhat[m]);
+        if (a.write_eta) {
+            // R2C kind: the pole kernel skips the corners; at K = 0, eta1 = e0/alpha and
+            // eta2 = eta1/conj(alpha), so sum(w1 eta1 + w2 eta2) = S e0 with the finish-kernel S.
+            // The R2C accumulator is the Hermitian part H(A), which at a self-mirror mode is Re A.
+            a.acc[m] = mk(cmul(a.S, a.fhat[m]).x, 0.0);
+            a.acc[n + m] = mk(red[0][0].x, 0.0);
+            a.acc[2 * n + m] = mk(red[1][0].x, 0.0);
+        } else {
+            a.acc[n + m] = red[0][0];
+            a.acc[2 * n + m] = red[1][0];
+        }
     }
 }
 
@@ -771,21 +933,22 @@ static int ilog2(int x) {
     return r;
 }
 
-// FFT launch shapes: threads per transform tf = max(1, D/8); a block holds nb transforms with
-// nb * tf <= 256 threads (rows) or a strip of C columns with C * tf <= 1024 and C <= 8.
+// FFT launch shapes: threads per transform tf = max(1, D/8); a row block holds nb row pairs
+// (nb * tf <= 256 threads, nb <= D/2); a column block a strip of C <= 8 half-spectrum slots
+// (C * tf <= 512, C <= D/2).
 static int fft_rows_per_block(int D) {
     const int tf = D >= 8 ? D / 8 : 1;
     int nb = 256 / tf;
     if (nb < 1) nb = 1;
-    if (nb > D) nb = D;
+    if (nb > D / 2) nb = D / 2;
     return nb;
 }
 static int fft_cols_per_block(int D) {
     const int tf = D >= 8 ? D / 8 : 1;
-    int C = 512 / tf;   // <= 512 threads and ~74 KB of smem per block: 3 blocks per SM
+    int C = 512 / tf;
     if (C > 8) C = 8;
     if (C < 1) C = 1;
-    if (C > D) C = D;
+    if (C > D / 2) C = D / 2;
     return C;
 }
 
@@ -793,54 +956,70 @@ cudaError_t fft_setup_attributes() {
     cudaError_t e;
     const int maxsm = 200 * 1024;
 #define SETA(K) if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm))) return e;
-    SETA((fft_rows_kernel<false, true, false>))
-    SETA((fft_rows_kernel<true, false, true>))
-    SETA((fft_rows_kernel<false, false, false>))
-    SETA((fft_rows_kernel<true, false, false>))
-    SETA(fft_cols_kernel<false>)
-    SETA(fft_cols_kernel<true>)
+    SETA(fft_rows_fwd_kernel)
+    SETA(fft_cols_fwd_kernel)
+    SETA(fft_cols_inv_kernel<true>)
+    SETA(fft_cols_inv_kernel<false>)
+    SETA(fft_rows_inv_kernel)
 #undef SETA
     return cudaSuccess;
 }
 
-cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool real_in, bool real_out,
-                            const cd *tw, int D, int inverse, double scale, cudaStream_t st) {
+static FftArgs fft_args(const void *const in[3], void *const out[3], const cd *tw, int D, int per_block,
+                        int inverse, double scale) {
     FftArgs a;
     for (int f = 0; f < 3; ++f) { a.in[f] = in[f]; a.out[f] = out[f]; }
     a.twiddle = tw;
     a.D = D;
     a.log2D = ilog2(D);
-    a.per_block = fft_rows_per_block(D);
+    a.per_block = per_block;
     a.inverse = inverse;
     a.scale = scale;
+    return a;
+}
+
+cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
+                               const cd *tw, int D, double scale, cudaStream_t st) {
     const int tf = D >= 8 ? D / 8 : 1;
-    dim3 grid(D / a.per_block, 3);
-    const int threads = a.per_block * tf;
-    const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
-    if (!inverse && real_in && !real_out) fft_rows_kernel<false, true, false><<<grid, threads, sm, st>>>(a);
-    else if (inverse && !real_in && real_out) fft_rows_kernel<true, false, true><<<grid, threads, sm, st>>>(a);
-    else if (!inverse && !real_in && !real_out) fft_rows_kernel<false, false, false><<<grid, threads, sm, st>>>(a);
-    else if (inverse && !real_in && !real_out) fft_rows_kernel<true, false, false><<<grid, threads, sm, st>>>(a);
-    else return cudaErrorInvalidValue;
+    {
+        const void *i3[3] = {in[0], in[1], in[2]};
+        void *o3[3] = {half[0], half[1], half[2]};
+        const FftArgs a = fft_args(i3, o3, tw, D, fft_rows_per_block(D), 0, 1.0);
+        const dim3 grid((D / 2) / a.per_block, 3);
+        const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
+        fft_rows_fwd_kernel<<<grid, a.per_block * tf, sm, st>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const void *i3[3] = {half[0], half[1], half[2]};
+    void *o3[3] = {out[0], out[1], out[2]};
+    const FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 0, scale);
+    const dim3 grid((D / 2) / a.per_block, 3);
+    const size_t sm = (size_t)a.per_block * col_stride(D, a.per_block) * sizeof(cd);
+    fft_cols_fwd_kernel<<<grid, a.per_block * tf, sm, st>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const cd *tw, int D,
-                            int inverse, double scale, cudaStream_t st) {
-    FftArgs a;
-    for (int f = 0; f < 3; ++f) { a.in[f] = in[f]; a.out[f] = out[f]; }
-    a.twiddle = tw;
-    a.D = D;
-    a.log2D = ilog2(D);
-    a.per_block = fft_cols_per_block(D);
-    a.inverse = inverse;
-    a.scale = scale;
+cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double *const out[3],
+                               bool hermitian, const cd *tw, int D, cudaStream_t st) {
     const int tf = D >= 8 ? D / 8 : 1;
-    dim3 grid(D / a.per_block, 3);
-    const int threads = a.per_block * tf;
-    const size_t sm = (size_t)a.per_block * (padded_len(D) + 1) * sizeof(cd);
-    if (inverse) fft_cols_kernel<true><<<grid, threads, sm, st>>>(a);
-    else fft_cols_kernel<false><<<grid, threads, sm, st>>>(a);
+    {
+        const void *i3[3] = {in[0], in[1], in[2]};
+        void *o3[3] = {half[0], half[1], half[2]};
+        const FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 1, 1.0);
+        const dim3 grid((D / 2) / a.per_block, 3);
+        const size_t sm = (size_t)a.per_block * col_stride(D, a.per_block) * sizeof(cd);
+        if (hermitian) fft_cols_inv_kernel<false><<<grid, a.per_block * tf, sm, st>>>(a);
+        else fft_cols_inv_kernel<true><<<grid, a.per_block * tf, sm, st>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const void *i3[3] = {half[0], half[1], half[2]};
+    void *o3[3] = {out[0], out[1], out[2]};
+    const FftArgs a = fft_args(i3, o3, tw, D, fft_rows_per_block(D), 1, 1.0);
+    const dim3 grid((D / 2) / a.per_block, 3);
+    const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
+    fft_rows_inv_kernel<<<grid, a.per_block * tf, sm, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -894,7 +1073,7 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
 
 // R2C pair kernel instantiations: (quads per thread NQ, poles per loop trip PU, min blocks).
 #define REXI_R2C_CONFIGS(X) \
-    X(1, 1, 4) X(1, 1, 5) X(1, 1, 6) X(1, 2, 3) X(1, 2, 4) X(2, 1, 2) X(2, 1, 3) X(2, 2, 2)
+    X(1, 1, 4) X(1, 1, 5) X(1, 1, 6) X(1, 2, 3) X(1, 2, 4) X(2, 1, 2) X(2, 1, 3) X(2, 2, 2) X(2, 4, 2) X(1, 4, 3) X(2, 3, 2)
 
 bool pole_r2c_supported(int nq, int pu, int minb) {
 #define X(Q, U, B) if (nq == Q && pu == U && minb == B) return true;

@@ -8,10 +8,12 @@
 namespace rexi {
 
 cudaError_t fft_setup_attributes();
-cudaError_t launch_fft_rows(const void *const in[3], void *const out[3], bool real_in, bool real_out,
-                            const cd *tw, int D, int inverse, double scale, cudaStream_t st);
-cudaError_t launch_fft_cols(const void *const in[3], void *const out[3], const cd *tw, int D,
-                            int inverse, double scale, cudaStream_t st);
+// S1: real fields -> full spectrum (x scale); half = D x D complex scratch per field.
+cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
+                               const cd *tw, int D, double scale, cudaStream_t st);
+// S5: Re(IDFT(in)) -> real fields; hermitian: in is known Hermitian (skip symmetrisation).
+cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double *const out[3],
+                               bool hermitian, const cd *tw, int D, cudaStream_t st);
 int pole_modes_per_block(int mpt);
 bool pole_config_supported(int variant, int mpt, int pu, int minb);
 cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_per_sm);

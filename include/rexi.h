@@ -222,6 +222,16 @@ rexi_status_t rexi_apply_host(rexi_plan_t plan, const double *eta, const double 
                               const double *v, double *eta_out, double *u_out, double *v_out,
                               void *stream);
 
+/* rexi_apply_host over `batch` independent problems: HOST arrays of batch consecutive D x D
+ * fields each (problem i at offset i * D * D), outputs likewise. The host<->device copies of
+ * problem i+1 (inputs) and i-1 (outputs) run on two private copy streams while problem i is
+ * computed on `stream` (two device staging sets, allocated on first use), so with pinned host
+ * memory the copies hide behind the steps. Returns when every output is in host memory.
+ * batch = 0 is a no-op; EINVAL for batch < 0 or a NULL pointer. */
+rexi_status_t rexi_apply_host_batch(rexi_plan_t plan, long batch, const double *eta,
+                                    const double *u, const double *v, double *eta_out,
+                                    double *u_out, double *v_out, void *stream);
+
 /* S6: `steps` successive steps in place on device fields (T_final = steps * tau). For
  * steps >= 2 the state stays in Fourier space between steps (NEXT-4): one forward FFT, then per
  * step the pole sum and the spectral form of the real part, (X(K) + conj(X(-K)))/2 — the same

@@ -86,6 +86,9 @@ struct rexi_plan_s {
     cd *d_tmp = nullptr;    // [3][n_modes]
     cd *d_partial = nullptr;  // [max_chunks][3][n_modes]
     double *d_stage = nullptr;  // [6][n_modes] (rexi_apply_host)
+    double *d_stage2 = nullptr;  // [6][n_modes] second set (rexi_apply_host_batch)
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_step[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // pairs
@@ -128,12 +131,17 @@ struct rexi_plan_s {
         clear_graphs();
         if (cap_stream) cudaStreamDestroy(cap_stream);
         if (aux_stream) cudaStreamDestroy(aux_stream);
+        if (h2d_stream) cudaStreamDestroy(h2d_stream);
+        if (d2h_stream) cudaStreamDestroy(d2h_stream);
+        for (int i = 0; i < 2; ++i)
+            for (cudaEvent_t e : {ev_in[i], ev_step[i], ev_out[i]})
+                if (e) cudaEventDestroy(e);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
-                        (void *)d_tmp, (void *)d_partial, (void *)d_stage})
+                        (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -751,6 +759,63 @@ rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u,
             return s;
         for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return REXI_OK;
+    });
+}
+
+rexi_status_t rexi_apply_host_batch(rexi_plan_t p, long batch, const double *eta, const double *u,
+                                    const double *v, double *eo, double *uo, double *vo, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (batch < 0) return fail(REXI_EINVAL, "batch must be >= 0");
+        if (batch == 0) return REXI_OK;
+        if (!eta || !u || !v || !eo || !uo || !vo) return fail(REXI_EINVAL, "null pointer");
+        const size_t n = (size_t)p->n_modes;
+        for (double **buf : {&p->d_stage, &p->d_stage2}) {
+            if (*buf) continue;
+            cudaError_t e = cudaMalloc((void **)buf, 6 * n * sizeof(double));
+            if (e != cudaSuccess) {
+                *buf = nullptr;
+                cudaGetLastError();
+                return fail(REXI_ENOMEM, "cudaMalloc (staging) failed");
+            }
+        }
+        if (!p->h2d_stream) CK(cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking));
+        if (!p->d2h_stream) CK(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i)
+            for (cudaEvent_t *e : {&p->ev_in[i], &p->ev_step[i], &p->ev_out[i]})
+                if (!*e) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t bytes = n * sizeof(double);
+        const double *hin[3] = {eta, u, v};
+        double *hout[3] = {eo, uo, vo};
+        // order the copy streams after whatever the caller queued on `stream` before this call
+        CK(cudaEventRecord(p->ev_step[0], st));
+        CK(cudaStreamWaitEvent(p->h2d_stream, p->ev_step[0], 0));
+        for (long i = 0; i < batch; ++i) {
+            const int b = (int)(i & 1);
+            double *d = b ? p->d_stage2 : p->d_stage;
+            // H2D of step i into set b, once step i-2 (the last user of set b's inputs) is done
+            if (i >= 2) CK(cudaStreamWaitEvent(p->h2d_stream, p->ev_step[b], 0));
+            for (int f = 0; f < 3; ++f)
+                CK(cudaMemcpyAsync(d + f * n, hin[f] + (size_t)i * n, bytes, cudaMemcpyHostToDevice,
+                                   p->h2d_stream));
+            CK(cudaEventRecord(p->ev_in[b], p->h2d_stream));
+            // step i on `stream`, once its inputs landed and step i-2's outputs left set b
+            CK(cudaStreamWaitEvent(st, p->ev_in[b], 0));
+            if (i >= 2) CK(cudaStreamWaitEvent(st, p->ev_out[b], 0));
+            rexi_status_t s = do_step(p, 0, p->host.n_poles, d, d + n, d + 2 * n, d + 3 * n, d + 4 * n,
+                                      d + 5 * n, st);
+            if (s != REXI_OK) return s;
+            CK(cudaEventRecord(p->ev_step[b], st));
+            // D2H of step i
+            CK(cudaStreamWaitEvent(p->d2h_stream, p->ev_step[b], 0));
+            for (int f = 0; f < 3; ++f)
+                CK(cudaMemcpyAsync(hout[f] + (size_t)i * n, d + (3 + f) * n, bytes, cudaMemcpyDeviceToHost,
+                                   p->d2h_stream));
+            CK(cudaEventRecord(p->ev_out[b], p->d2h_stream));
+        }
+        CK(cudaStreamSynchronize(p->d2h_stream));
         CK(cudaStreamSynchronize(st));
         return REXI_OK;
     });

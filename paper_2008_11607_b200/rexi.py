@@ -57,6 +57,7 @@ EXPORTS = {
     "rexi_apply_partial": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp,
                                           _vp, _vp, _vp, _vp]),
     "rexi_apply_host": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "rexi_apply_host_batch": (ctypes.c_int, [_vp, ctypes.c_long, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rexi_run": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "rexi_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_timing_read": (ctypes.c_int, [_vp, _dp, _lp, _lp]),
@@ -322,6 +323,31 @@ class Plan:
             out = tuple(np.empty((self.D, self.D)) for _ in range(3))
         _check(_lib.rexi_apply_host(self._h, ptr(eta, "eta"), ptr(u, "u"), ptr(v, "v"),
                                     *(ptr(o, "out") for o in out), self._stream()), "rexi_apply_host")
+        return out
+
+    def apply_host_batch(self, eta, u, v, out=None):
+        """`batch` independent problems from host arrays of shape (batch, D, D) (numpy float64 or
+        CPU tensors, ideally pinned); copies overlap the steps (rexi_apply_host_batch)."""
+        def ptr(a, name):
+            if isinstance(a, np.ndarray):
+                if a.dtype != np.float64 or a.ndim != 3 or a.shape[1:] != (self.D, self.D) \
+                        or not a.flags.c_contiguous:
+                    raise ValueError(f"{name}: expected C-contiguous float64 (batch, {self.D}, {self.D})")
+                return _vp(a.ctypes.data), a.shape[0]
+            torch = _torch()
+            if a.device.type != "cpu" or a.dtype != torch.float64 or a.dim() != 3 \
+                    or tuple(a.shape[1:]) != (self.D, self.D) or not a.is_contiguous():
+                raise ValueError(f"{name}: expected a contiguous float64 CPU tensor (batch, D, D)")
+            return _vp(a.data_ptr()), a.shape[0]
+        ins = [ptr(x, nm) for x, nm in ((eta, "eta"), (u, "u"), (v, "v"))]
+        batch = ins[0][1]
+        if out is None:
+            out = tuple(np.empty((batch, self.D, self.D)) for _ in range(3))
+        outs = [ptr(o, "out") for o in out]
+        if any(b != batch for _, b in ins + outs):
+            raise ValueError("all batch arrays must have the same leading dimension")
+        _check(_lib.rexi_apply_host_batch(self._h, int(batch), *(x for x, _ in ins), *(o for o, _ in outs),
+                                          self._stream()), "rexi_apply_host_batch")
         return out
 
     def run(self, steps, eta, u, v):

@@ -257,6 +257,40 @@ def test_apply_in_place_and_host_and_run(R):
     assert rel_l2([host(x) for x in t], g) < TOL
 
 
+@pytest.mark.parametrize("batch", [1, 2, 5])
+def test_apply_host_batch(R, batch):
+    """rexi_apply_host_batch: problem i of the batch equals rexi_apply on it (same kernels,
+    bit-identical), for numpy and pinned-tensor host buffers; one problem checked vs the oracle."""
+    import torch
+    D, tau = 32, 0.4
+    p = R.Plan(D, tau)
+    fs = [inputs.white_noise(D, seed=100 + 10 * i) for i in range(batch)]
+    stack = [np.ascontiguousarray(np.stack([f[c] for f in fs])) for c in range(3)]
+    out = p.apply_host_batch(*stack)
+    for i, f in enumerate(fs):
+        ref = [host(t) for t in p.apply(*(dev(x) for x in f))]
+        assert rel_l2([o[i] for o in out], ref) == 0.0
+    pin = [torch.from_numpy(x).pin_memory() for x in stack]
+    pout = [torch.empty_like(x).pin_memory() for x in pin]
+    p.apply_host_batch(*pin, out=pout)
+    for c in range(3):
+        assert np.array_equal(pout[c].numpy(), out[c])
+    info = p.info
+    g = lrsw.rexii_step(*fs[-1], tau, info["h"], info["M"])
+    assert rel_l2([o[-1] for o in out], g) < TOL
+
+
+def test_apply_host_batch_errors(R):
+    p = R.Plan(8, 0.3)
+    z = np.zeros((2, 8, 8))
+    with pytest.raises(ValueError):
+        p.apply_host_batch(z, z, np.zeros((3, 8, 8)))
+    with pytest.raises(ValueError):
+        p.apply_host_batch(z, z, np.zeros((2, 8, 4)))
+    out = p.apply_host_batch(z[:0], z[:0], z[:0])
+    assert out[0].shape == (0, 8, 8)
+
+
 def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]

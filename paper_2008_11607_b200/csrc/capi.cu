@@ -57,7 +57,7 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 3}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 2}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
     int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)

@@ -550,6 +550,7 @@ __device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) 
 // is accumulated directly per pole:
 //   H_eta   += X1 eta1 + X2 eta_t + (conj(W1 q) - conj(W2) q) d0
 //   H_delta' += Y1 eta1 + Y2 eta_t + (conj(P1 q) - conj(P2) q) d0
+// (the d0 coefficients are summed per quad and applied once, after the pole loop)
 // (X, Y: half-weights from the planner). Each thread owns one K2 quad = two pairs; the
 // corner quad (four self-mirror K = 0 modes) is left to fixup_k0_kernel.
 struct PairState {
@@ -605,6 +606,14 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
             K2[g] = fma(kx, kx, ky * ky);
         }
     }
+    // the d0 terms of H_eta and H_delta' have pole-sum coefficients that depend on the quad
+    // only (sigma, tau' are functions of K2): summed once per quad, applied to d0 at the end
+    cd Ssig[NQ], Stau[NQ];
+#pragma unroll
+    for (int g = 0; g < NQ; ++g) {
+        Ssig[g] = mk(0, 0);
+        Stau[g] = mk(0, 0);
+    }
 
     for (long pt = p0; pt < p1; pt += kPoleTile) {
         const int cnt = (int)min((long)kPoleTile, p1 - pt);
@@ -628,8 +637,8 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
                 const cd qd = pole_den(P, K2[g]);
                 // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, quad)
                 const cd W1q = cmul(mk(P.W1r, P.W1i), qd), P1q = cmul(mk(P.P1r, P.P1i), qd);
-                const cd sig = cjfms(mk(P.W2r, P.W2i), qd, mk(W1q.x, -W1q.y));
-                const cd tau = cjfms(mk(P.P2r, P.P2i), qd, mk(P1q.x, -P1q.y));
+                Ssig[g] = cjfms(mk(P.W2r, P.W2i), qd, mk(Ssig[g].x + W1q.x, Ssig[g].y - W1q.y));
+                Stau[g] = cjfms(mk(P.P2r, P.P2i), qd, mk(Stau[g].x + P1q.x, Stau[g].y - P1q.y));
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                     PairState &s = st[2 * g + j];
@@ -637,8 +646,8 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
                     const cd eta1 = cmul(cfms(s2, s.m0, t), qd);
                     const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
                     const cd etat = cjfma(qd, cjfms(s2, s.m0, tt), mk(0, 0));
-                    s.H0 = cfma(sig, s.d0, cfma(X2, etat, cfma(X1, eta1, s.H0)));
-                    s.H1 = cfma(tau, s.d0, cfma(Y2, etat, cfma(Y1, eta1, s.H1)));
+                    s.H0 = cfma(X2, etat, cfma(X1, eta1, s.H0));
+                    s.H1 = cfma(Y2, etat, cfma(Y1, eta1, s.H1));
                 }
             }
         }
@@ -649,8 +658,9 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
         if (ok[g]) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                out[rep[2 * g + j]] = st[2 * g + j].H0;
-                out[n_modes + rep[2 * g + j]] = st[2 * g + j].H1;
+                const PairState &s = st[2 * g + j];
+                out[rep[2 * g + j]] = cfma(Ssig[g], s.d0, s.H0);
+                out[n_modes + rep[2 * g + j]] = cfma(Stau[g], s.d0, s.H1);
             }
         }
     }

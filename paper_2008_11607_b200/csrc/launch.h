@@ -34,19 +34,19 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //   kind 4 (PF): two solves of f0 (num 6/12 and numt 6/12, eta 4/6 each, delta 4/8 each),
 //                shared den 7/11, 4 MACs 16/32: 51 / 95
 //   kind 5 (PFH): PF without the two delta back-substitutions (4/8 each): 43 / 79
-//   kind 6 (R2C pairs, real input, per quad = two pairs): den 7/11 + sigma, tau 16/28 +
-//     2 x (num 6/12, numt 6/12, eta 4/6, eta_t 4/6, 6 MACs 24/48) = 111 / 207 per quad
-//     = 27.75 / 51.75 per mode (always quads)
+//   kind 6 (R2C pairs, real input, per quad = two pairs): den 7/11 + the per-quad sums of
+//     sigma, tau 20/32 + 2 x (num 6/12, numt 6/12, eta 4/6, eta_t 4/6, 4 MACs 16/32)
+//     = 99 / 179 per quad = 24.75 / 44.75 per mode (always quads)
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
 // by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
 inline double pole_flops(int kind, int mpt) {
-    if (kind == 6) return 51.75;
+    if (kind == 6) return 44.75;
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt) {
-    if (kind == 6) return 27.75;
+    if (kind == 6) return 24.75;
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

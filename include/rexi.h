@@ -161,9 +161,11 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
  *   REXII PF:  (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4)         default (4,1,3)
  *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4) (1,2,6) (2,2,3) (2,2,4) (4,2,2)
  *                                                                      default (4,2,2)
- *   REXII PFHR: modes_per_thread 4 or 8 (one or two K2 quads = two or four R2C pairs):
+ *   REXII PFHR: modes_per_thread 4 (one K2 quad = two R2C pairs), 8 (an "octet": quads (a, b)
+ *               and (b, a), which share K2, or two of the remaining quads = four pairs) or 16
+ *               (two quads in linear order, no K2 sharing):
  *               (4,1,4) (4,1,5) (4,1,6) (4,2,3) (4,2,4) (4,4,3) (8,1,2) (8,1,3) (8,2,2) (8,3,2)
- *               (8,4,2)                                                   default (8,2,2)
+ *               (8,4,2) (16,2,2)                                          default (8,4,2)
  *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).

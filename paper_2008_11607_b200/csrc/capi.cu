@@ -57,7 +57,7 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 2}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 4}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
     int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
@@ -159,11 +159,12 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range, int v) {
     if (n_range <= 0) return 0;
-    const long mpb = v == 6 ? (long)p->mpt[v] * 128 : rexi::pole_modes_per_block(p->mpt[v]);
-    const long tiles = (p->n_modes + mpb - 1) / mpb;
+    const long tiles = v == 6 ? rexi::pole_r2c_blocks(p->host.D, p->mpt[v])
+                              : (p->n_modes + rexi::pole_modes_per_block(p->mpt[v]) - 1) /
+                                    rexi::pole_modes_per_block(p->mpt[v]);
     int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];
     if (occ <= 0) {
-        cudaError_t e = v == 6 ? rexi::pole_r2c_occupancy(p->mpt[v] / 4, p->pu[v], p->minb[v], &occ)
+        cudaError_t e = v == 6 ? rexi::pole_r2c_occupancy(p->mpt[v], p->pu[v], p->minb[v], &occ)
                                : rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ);
         if (e != cudaSuccess) occ = 1;
     }
@@ -293,7 +294,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         p->launches += 1;
     }
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    if (kd == 6) CK(rexi::launch_poles_r2c(a, p->mpt[kd] / 4, p->pu[kd], p->minb[kd], st));
+    if (kd == 6) CK(rexi::launch_poles_r2c(a, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     else CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
@@ -591,8 +592,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
     info->m0 = h.m0;
     info->rho = h.rho;
     info->predicted_floor = h.predicted_floor;
-    info->flops_per_pole_mode = rexi::pole_flops(p->kind(), p->mpt[p->kind()]);
-    info->fp64_ops_per_pole_mode = rexi::pole_ops(p->kind(), p->mpt[p->kind()]);
+    info->flops_per_pole_mode = rexi::pole_flops(p->kind(), p->mpt[p->kind()], p->host.D);
+    info->fp64_ops_per_pole_mode = rexi::pole_ops(p->kind(), p->mpt[p->kind()], p->host.D);
     return REXI_OK;
 }
 
@@ -661,8 +662,7 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int pole
                                    int min_blocks_per_sm) {
     if (!p) return fail(REXI_EINVAL, "null plan");
     const int v = p->kind();
-    const bool ok = v == 6 ? (modes_per_thread % 4 == 0 &&
-                              rexi::pole_r2c_supported(modes_per_thread / 4, poles_per_iter, min_blocks_per_sm))
+    const bool ok = v == 6 ? rexi::pole_r2c_supported(modes_per_thread, poles_per_iter, min_blocks_per_sm)
                            : rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm);
     if (!ok) return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
     p->mpt[v] = modes_per_thread;

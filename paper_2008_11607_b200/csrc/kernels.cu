@@ -551,14 +551,75 @@ __device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) 
 //   H_eta   += X1 eta1 + X2 eta_t + (conj(W1 q) - conj(W2) q) d0
 //   H_delta' += Y1 eta1 + Y2 eta_t + (conj(P1 q) - conj(P2) q) d0
 // (the d0 coefficients are summed per quad and applied once, after the pole loop)
-// (X, Y: half-weights from the planner). Each thread owns one K2 quad = two pairs; the
-// corner quad (four self-mirror K = 0 modes) is left to fixup_k0_kernel.
+// (X, Y: half-weights from the planner). A thread owns one or two K2 quads (two or four pairs,
+// see r2c work items below); the corner quad (four self-mirror K = 0 modes) is left to
+// fixup_k0_kernel.
 struct PairState {
     cd e0, B0, Bt0, m0, d0;  // data of the representative mode
     cd H0, H1;               // Hermitian accumulators: eta, delta' (before the e0 term)
 };
 
-template <int PU, int MINB, int NQ>
+// Work items of the R2C kernel (four pairs = eight modes per thread):
+//  * OCT: "octets" — the interior quads (a, b) and (b, a), 1 <= a < b < H, share K2 (square
+//    grid, the same symbol in x and y), so one denominator and one (sigma, tau') sum per pole
+//    serve eight modes; items n_oct.. hold two of the remaining 3 (H - 1) quads (diagonal a = b,
+//    axes, Nyquist lines) with their own K2 each.
+//  * !OCT: NQ quads per thread in linear quad order.
+// Quad 0 (the four K = 0 corners) is left to the fix-up kernel.
+__host__ __device__ __forceinline__ long r2c_n_oct(int D) {
+    const long H = D >> 1;
+    return H >= 3 ? (H - 1) * (H - 2) / 2 : 0;
+}
+__host__ __device__ __forceinline__ long r2c_items(int D, int nq, bool oct) {
+    const long H = D >> 1;
+    if (oct) return r2c_n_oct(D) + (3 * (H - 1) + 1) / 2;
+    return ((long)D * D / 4 + nq - 1) / nq;
+}
+// the s-th of the 3 (H - 1) non-octet quads (s < 3 (H - 1)) as a quad index a * H + b
+__device__ __forceinline__ long r2c_single_quad(long s, int H) {
+    long qa, qb;
+    if (s < H - 1) { qa = s + 1; qb = s + 1; }
+    else if (s < 2 * (H - 1)) { qa = 0; qb = s - (H - 1) + 1; }
+    else { qa = s - 2 * (H - 1) + 1; qb = 0; }
+    return qa * H + qb;
+}
+
+// One tile of poles for the thread's four pairs. SHARED: both quads have the same K2 (octet).
+template <int PU, int NQ, bool SHARED>
+__device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const double (&K2)[NQ],
+                                         PairState (&st)[2 * NQ], cd (&Ssig)[NQ], cd (&Stau)[NQ]) {
+    constexpr int NG = SHARED ? 1 : NQ;
+#pragma unroll PU
+    for (int qq = 0; qq < cnt; ++qq) {
+        const PoleConst &P = sp[qq];
+        const cd s2 = mk(P.s2r, P.s2i);
+        const double hn = P.ai;
+        const cd X1 = mk(P.X1r, P.X1i), X2 = mk(P.X2r, P.X2i);
+        const cd Y1 = mk(P.Y1r, P.Y1i), Y2 = mk(P.Y2r, P.Y2i);
+        cd qd[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            qd[g] = pole_den(P, K2[g]);
+            // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, quad)
+            const cd W1q = cmul(mk(P.W1r, P.W1i), qd[g]), P1q = cmul(mk(P.P1r, P.P1i), qd[g]);
+            Ssig[g] = cjfms(mk(P.W2r, P.W2i), qd[g], mk(Ssig[g].x + W1q.x, Ssig[g].y - W1q.y));
+            Stau[g] = cjfms(mk(P.P2r, P.P2i), qd[g], mk(Stau[g].x + P1q.x, Stau[g].y - P1q.y));
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * NQ; ++j) {
+            const cd q = qd[SHARED ? 0 : j >> 1];
+            PairState &s = st[j];
+            const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
+            const cd eta1 = cmul(cfms(s2, s.m0, t), q);
+            const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
+            const cd etat = cjfma(q, cjfms(s2, s.m0, tt), mk(0, 0));
+            s.H0 = cfma(X2, etat, cfma(X1, eta1, s.H0));
+            s.H1 = cfma(Y2, etat, cfma(Y1, eta1, s.H1));
+        }
+    }
+}
+
+template <int PU, int MINB, int NQ, bool OCT>
 __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
     __shared__ PoleConst sp[kPoleTile];
     const long n_modes = a.n_modes;
@@ -569,17 +630,45 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
     const double c = a.tau;
     const double hmu = a.hmu;
     const int H = a.D >> 1;
-    // NQ K2 quads per thread (quad q = blockIdx.x * 128 NQ + g * 128 + tid); quad 0 = the four
-    // K = 0 corners, left to the fix-up kernel
-    long rep[2 * NQ];
+    const long item = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+    long quad[NQ];
     bool ok[NQ];
+    bool shared_k2 = false;
+    if (OCT) {
+        static_assert(!OCT || NQ == 2, "octet items hold two quads");
+        const long n_oct = r2c_n_oct(a.D);
+        if (item < n_oct) {
+            // triangular decode: item = b'(b'-1)/2 + a', 0 <= a' < b' <= H - 2; (a, b) = (a'+1, b'+1)
+            long bp = (long)((1.0 + sqrt(1.0 + 8.0 * (double)item)) * 0.5);
+            while (bp * (bp - 1) / 2 > item) --bp;
+            while ((bp + 1) * bp / 2 <= item) ++bp;
+            const long ap = item - bp * (bp - 1) / 2;
+            quad[0] = (ap + 1) * H + (bp + 1);
+            quad[NQ - 1] = (bp + 1) * H + (ap + 1);
+            ok[0] = ok[NQ - 1] = true;
+            shared_k2 = true;
+        } else {
+#pragma unroll
+            for (int g = 0; g < NQ; ++g) {
+                const long sidx = 2 * (item - n_oct) + g;
+                ok[g] = sidx < 3L * (H - 1);
+                quad[g] = ok[g] ? r2c_single_quad(sidx, H) : 1;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int g = 0; g < NQ; ++g) {
+            const long q = (long)blockIdx.x * (kPoleBlock * NQ) + g * kPoleBlock + threadIdx.x;
+            ok[g] = q > 0 && q < (n_modes >> 2);
+            quad[g] = ok[g] ? q : 1;
+        }
+    }
+    long rep[2 * NQ];
     double K2[NQ];
     PairState st[2 * NQ];
 #pragma unroll
     for (int g = 0; g < NQ; ++g) {
-        const long q = (long)blockIdx.x * (kPoleBlock * NQ) + g * kPoleBlock + threadIdx.x;
-        ok[g] = q > 0 && q < (n_modes >> 2);
-        const long qs = ok[g] ? q : 1;
+        const long qs = quad[g];
         long mq[4];
         quad_modes(qs, a.D, a.log2D, mq);
         // representatives: interior quads pair (0,3) and (1,2); axis / Nyquist quads (0,1), (2,3)
@@ -606,8 +695,8 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
             K2[g] = fma(kx, kx, ky * ky);
         }
     }
-    // the d0 terms of H_eta and H_delta' have pole-sum coefficients that depend on the quad
-    // only (sigma, tau' are functions of K2): summed once per quad, applied to d0 at the end
+    // the d0 terms of H_eta and H_delta' have pole-sum coefficients that depend on K2 only
+    // (sigma, tau'): summed once per K2, applied to d0 after the pole loop
     cd Ssig[NQ], Stau[NQ];
 #pragma unroll
     for (int g = 0; g < NQ; ++g) {
@@ -625,31 +714,14 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
             for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
         }
         __syncthreads();
-#pragma unroll PU
-        for (int qq = 0; qq < cnt; ++qq) {
-            const PoleConst &P = sp[qq];
-            const cd s2 = mk(P.s2r, P.s2i);
-            const double hn = P.ai;
-            const cd X1 = mk(P.X1r, P.X1i), X2 = mk(P.X2r, P.X2i);
-            const cd Y1 = mk(P.Y1r, P.Y1i), Y2 = mk(P.Y2r, P.Y2i);
+        if (OCT && shared_k2) r2c_tile<PU, NQ, true>(sp, cnt, K2, st, Ssig, Stau);
+        else r2c_tile<PU, NQ, false>(sp, cnt, K2, st, Ssig, Stau);
+    }
+    if (OCT && shared_k2) {
 #pragma unroll
-            for (int g = 0; g < NQ; ++g) {
-                const cd qd = pole_den(P, K2[g]);
-                // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, quad)
-                const cd W1q = cmul(mk(P.W1r, P.W1i), qd), P1q = cmul(mk(P.P1r, P.P1i), qd);
-                Ssig[g] = cjfms(mk(P.W2r, P.W2i), qd, mk(Ssig[g].x + W1q.x, Ssig[g].y - W1q.y));
-                Stau[g] = cjfms(mk(P.P2r, P.P2i), qd, mk(Stau[g].x + P1q.x, Stau[g].y - P1q.y));
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    PairState &s = st[2 * g + j];
-                    const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
-                    const cd eta1 = cmul(cfms(s2, s.m0, t), qd);
-                    const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
-                    const cd etat = cjfma(qd, cjfms(s2, s.m0, tt), mk(0, 0));
-                    s.H0 = cfma(X2, etat, cfma(X1, eta1, s.H0));
-                    s.H1 = cfma(Y2, etat, cfma(Y1, eta1, s.H1));
-                }
-            }
+        for (int g = 1; g < NQ; ++g) {
+            Ssig[g] = Ssig[0];
+            Stau[g] = Stau[0];
         }
     }
     cd *out = a.partial + (size_t)chunk * 3 * n_modes;
@@ -1081,31 +1153,38 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
     return cudaErrorInvalidValue;
 }
 
-// R2C pair kernel instantiations: (quads per thread NQ, poles per loop trip PU, min blocks).
+// R2C pair kernel instantiations: (modes per thread M, poles per loop trip PU, min blocks).
+// M = 4: one quad per thread; M = 8: octet items (shared K2, default); M = 16: two quads per
+// thread in linear order (eight modes, no K2 sharing; kept for comparison).
 #define REXI_R2C_CONFIGS(X) \
-    X(1, 1, 4) X(1, 1, 5) X(1, 1, 6) X(1, 2, 3) X(1, 2, 4) X(2, 1, 2) X(2, 1, 3) X(2, 2, 2) X(2, 4, 2) X(1, 4, 3) X(2, 3, 2)
+    X(4, 1, 4) X(4, 1, 5) X(4, 1, 6) X(4, 2, 3) X(4, 2, 4) X(4, 4, 3) \
+    X(8, 1, 2) X(8, 1, 3) X(8, 2, 2) X(8, 3, 2) X(8, 4, 2) X(16, 2, 2)
+#define R2C_KERNEL(M, U, B) pole_kernel_r2c<U, B, ((M) == 4 ? 1 : 2), ((M) == 8)>
 
-bool pole_r2c_supported(int nq, int pu, int minb) {
-#define X(Q, U, B) if (nq == Q && pu == U && minb == B) return true;
+bool pole_r2c_supported(int mpt, int pu, int minb) {
+#define X(M, U, B) if (mpt == M && pu == U && minb == B) return true;
     REXI_R2C_CONFIGS(X)
 #undef X
     return false;
 }
 
-cudaError_t pole_r2c_occupancy(int nq, int pu, int minb, int *blocks_per_sm) {
-#define X(Q, U, B) if (nq == Q && pu == U && minb == B) \
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2c<U, B, Q>, kPoleBlock, 0);
+long pole_r2c_blocks(int D, int mpt) {
+    const long items = r2c_items(D, mpt == 4 ? 1 : 2, mpt == 8);
+    return (items + kPoleBlock - 1) / kPoleBlock;
+}
+
+cudaError_t pole_r2c_occupancy(int mpt, int pu, int minb, int *blocks_per_sm) {
+#define X(M, U, B) if (mpt == M && pu == U && minb == B) \
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, R2C_KERNEL(M, U, B), kPoleBlock, 0);
     REXI_R2C_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_poles_r2c(const PoleArgs &a, int nq, int pu, int minb, cudaStream_t st) {
-    const long quads = a.n_modes >> 2;
-    const long per_block = (long)kPoleBlock * nq;
-    dim3 grid((unsigned)((quads + per_block - 1) / per_block), (unsigned)a.n_chunks);
-#define X(Q, U, B) if (nq == Q && pu == U && minb == B) { \
-    pole_kernel_r2c<U, B, Q><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
+cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaStream_t st) {
+    dim3 grid((unsigned)pole_r2c_blocks(a.D, mpt), (unsigned)a.n_chunks);
+#define X(M, U, B) if (mpt == M && pu == U && minb == B) { \
+    R2C_KERNEL(M, U, B)<<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
     REXI_R2C_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -19,9 +19,10 @@ bool pole_config_supported(int variant, int mpt, int pu, int minb);
 cudaError_t pole_occupancy(int variant, int mpt, int pu, int minb, int *blocks_per_sm);
 cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int minb, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st);
-bool pole_r2c_supported(int nq, int pu, int minb);
-cudaError_t pole_r2c_occupancy(int nq, int pu, int minb, int *blocks_per_sm);
-cudaError_t launch_poles_r2c(const PoleArgs &a, int nq, int pu, int minb, cudaStream_t st);
+bool pole_r2c_supported(int mpt, int pu, int minb);
+long pole_r2c_blocks(int D, int mpt);
+cudaError_t pole_r2c_occupancy(int mpt, int pu, int minb, int *blocks_per_sm);
+cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 
@@ -34,19 +35,26 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //   kind 4 (PF): two solves of f0 (num 6/12 and numt 6/12, eta 4/6 each, delta 4/8 each),
 //                shared den 7/11, 4 MACs 16/32: 51 / 95
 //   kind 5 (PFH): PF without the two delta back-substitutions (4/8 each): 43 / 79
-//   kind 6 (R2C pairs, real input, per quad = two pairs): den 7/11 + the per-quad sums of
-//     sigma, tau 20/32 + 2 x (num 6/12, numt 6/12, eta 4/6, eta_t 4/6, 4 MACs 16/32)
-//     = 99 / 179 per quad = 24.75 / 44.75 per mode (always quads)
+//   kind 6 (R2C pairs, real input): per K2 value, den 7/11 + the sums of sigma, tau' 20/32;
+//     per pair (two modes), num 6/12, numt 6/12, eta 4/6, eta_t 4/6, 4 MACs 16/32 = 36/68.
+//     A quad (4 modes, own K2) = 99 / 179; an octet (8 modes, shared K2) = 171 / 315, i.e.
+//     24.75 / 44.75 resp. 21.375 / 39.375 per mode; modes_per_thread 8 uses octets for the
+//     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and single quads for the other 3(H-1).
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
 // by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
-inline double pole_flops(int kind, int mpt) {
-    if (kind == 6) return 44.75;
+inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
+    if (mpt != 8 || D < 6) return quad / 4.0;
+    const double H = D / 2, n_oct = (H - 1) * (H - 2) / 2, n_single = 3 * (H - 1);
+    return (n_oct * octet + n_single * quad) / (8 * n_oct + 4 * n_single);
+}
+inline double pole_flops(int kind, int mpt, int D) {
+    if (kind == 6) return r2c_per_mode(mpt, D, 179.0, 315.0);
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
-inline double pole_ops(int kind, int mpt) {
-    if (kind == 6) return 24.75;
+inline double pole_ops(int kind, int mpt, int D) {
+    if (kind == 6) return r2c_per_mode(mpt, D, 99.0, 171.0);
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

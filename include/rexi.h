@@ -120,6 +120,9 @@ typedef struct {
     double predicted_floor; /* predicted scalar error floor (readings G8, G9)         */
     double flops_per_pole_mode; /* algorithmic fp64 flops per pole x Fourier mode     */
     double fp64_ops_per_pole_mode; /* fp64-pipe instructions (FMA = 1) per pole x mode */
+    int schedule;           /* rexi_schedule_t set on the plan                          */
+    int last_schedule;      /* schedule the last pole-kernel launch used (CHUNKED or
+                               STREAMK; AUTO = none yet)                                 */
 } rexi_plan_info_t;
 
 /* Create a plan for one step of size tau on a D x D grid.
@@ -174,6 +177,27 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
  * results agree to rounding, not bit for bit. EINVAL otherwise. */
 rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter,
                                    int min_blocks_per_sm);
+
+/* How the R2C pole kernel (REXII PFHR, modes_per_thread 8, real-input calls) distributes its
+ * (item tile x pole) iterations over the GPU:
+ *  REXI_SCHEDULE_CHUNKED: grid = (tiles, pole chunks), chunk count chosen to fill whole waves of
+ *                         resident blocks; one partial sum per chunk.
+ *  REXI_SCHEDULE_STREAMK: a persistent grid of one 256-thread block per SM splits the
+ *                         iteration space evenly (no wave tail); one partial per tile segment.
+ *  REXI_SCHEDULE_AUTO:    CHUNKED (default). With octet items every block costs the same, so
+ *                         the chunked waves are already balanced, and two 128-thread blocks per
+ *                         SM issue better than one 256-thread block: measured on B200 the
+ *                         chunked pole kernel is 2-4 % faster (C2 1.695 vs 1.735 ms, C4 830 vs
+ *                         863 ms).
+ * STREAMK falls back to CHUNKED when the segment partials do not fit the partial buffer. The kernels of every other variant are
+ * always chunked. Schedules differ only in the summation order of the pole sum. Clears the
+ * plan's graph cache. EINVAL for an unknown schedule. */
+typedef enum {
+    REXI_SCHEDULE_AUTO = 0,
+    REXI_SCHEDULE_CHUNKED = 1,
+    REXI_SCHEDULE_STREAMK = 2
+} rexi_schedule_t;
+rexi_status_t rexi_plan_set_schedule(rexi_plan_t plan, int schedule);
 
 /* Whole-step CUDA graphs (default on): rexi_apply / rexi_apply_partial / rexi_apply_host /
  * rexi_run capture their kernel sequence once per (buffers, pole range, method, variant,

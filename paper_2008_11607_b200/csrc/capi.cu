@@ -57,8 +57,11 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 4}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 1}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
     int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
+    int sk_occ = 0;                            // same, stream-K R2C kernel
+    int schedule = REXI_SCHEDULE_AUTO;
+    int last_schedule = REXI_SCHEDULE_AUTO;
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
     int kind() const {
@@ -248,7 +251,27 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     }
     int kd = p->kind();
     if (kd == 6 && !real_input) kd = 5;
-    const int chunks = choose_chunks(p, e - b, kd);
+    // R2C with octet items, REXI_SCHEDULE_STREAMK: a persistent grid when the segment partials
+    // fit the partial buffer (AUTO = chunked: measured 2-4 % faster, rexi.h)
+    long sk_tiles = 0;
+    int sk_slots = 0, sk_ctas = 0;
+    if (kd == 6 && p->mpt[6] == 8 && p->schedule == REXI_SCHEDULE_STREAMK) {
+        if (p->sk_occ <= 0 && rexi::pole_r2c_sk_occupancy(p->pu[6], &p->sk_occ) != cudaSuccess)
+            p->sk_occ = -1;
+        if (p->sk_occ > 0) {
+            const long T = rexi::pole_r2c_sk_tiles(p->host.D);
+            const long P = (long)p->num_sms * p->sk_occ;
+            const long slots = rexi::sk_slots_bound(T, e - b, P);
+            const size_t need = (size_t)T * (size_t)std::max(0L, slots) * 8 * 256 * sizeof(cd);
+            if (p->schedule == REXI_SCHEDULE_STREAMK && T * (e - b) / P >= 1 && slots > 0 &&
+                need <= sizeof(cd) * 3 * (size_t)n * p->max_chunks) {
+                sk_tiles = T;
+                sk_slots = (int)slots;
+                sk_ctas = (int)P;
+            }
+        }
+    }
+    const int chunks = sk_tiles ? 1 : choose_chunks(p, e - b, kd);
     rexi::PoleArgs a;
     a.fhat = fhat;
     a.partial = p->d_partial;
@@ -263,6 +286,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     while ((1 << a.log2D) < a.D) ++a.log2D;
     a.tau = p->host.tau;
     a.hmu = p->host.poles[0].ar;
+    a.sk_tiles = sk_tiles;
+    a.sk_slots = sk_slots;
     rexi_status_t s;
     const bool fork = (kd == 6);
     if (fork) {
@@ -294,7 +319,9 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         p->launches += 1;
     }
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    if (kd == 6) CK(rexi::launch_poles_r2c(a, p->mpt[kd], p->pu[kd], p->minb[kd], st));
+    p->last_schedule = sk_tiles ? REXI_SCHEDULE_STREAMK : REXI_SCHEDULE_CHUNKED;
+    if (sk_tiles) CK(rexi::launch_poles_r2c_sk(a, p->pu[kd], sk_ctas, st));
+    else if (kd == 6) CK(rexi::launch_poles_r2c(a, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     else CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
@@ -317,14 +344,19 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         const long double wi = p->host.wpre_im[(size_t)e] - p->host.wpre_im[(size_t)b];
         f.Sd = cd{(double)wr, (double)wi};
     }
-    CK(rexi::launch_finish(f, st));
+    f.sk_tiles = sk_tiles;
+    f.sk_slots = sk_slots;
+    f.sk_ctas = sk_ctas;
+    f.sk_poles = e - b;
+    if (sk_tiles) CK(rexi::launch_finish_r2c_sk(f, st));
+    else CK(rexi::launch_finish(f, st));
     p->launches += 2;
     if (fork) {
         CK(cudaStreamWaitEvent(st, p->ev_join, 0));
     } else if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
         rexi::FixupArgs x;
         x.method = p->method;
-        x.write_eta = 0;
+        x.write_eta = kd == 6;
         x.S = f.S;
         x.fhat = fhat;
         x.acc = acc;
@@ -594,6 +626,8 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
     info->predicted_floor = h.predicted_floor;
     info->flops_per_pole_mode = rexi::pole_flops(p->kind(), p->mpt[p->kind()], p->host.D);
     info->fp64_ops_per_pole_mode = rexi::pole_ops(p->kind(), p->mpt[p->kind()], p->host.D);
+    info->schedule = p->schedule;
+    info->last_schedule = p->last_schedule;
     return REXI_OK;
 }
 
@@ -669,6 +703,17 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int pole
     p->pu[v] = poles_per_iter;
     p->minb[v] = min_blocks_per_sm;
     p->occ_cache[v] = 0;
+    p->sk_occ = 0;
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_set_schedule(rexi_plan_t p, int schedule) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    if (schedule != REXI_SCHEDULE_AUTO && schedule != REXI_SCHEDULE_CHUNKED && schedule != REXI_SCHEDULE_STREAMK)
+        return fail(REXI_EINVAL, "unknown schedule");
+    DeviceGuard g(p->device);
+    p->schedule = schedule;
+    p->clear_graphs();
     return REXI_OK;
 }
 

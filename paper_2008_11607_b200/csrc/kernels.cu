@@ -562,8 +562,8 @@ struct PairState {
 // Work items of the R2C kernel (four pairs = eight modes per thread):
 //  * OCT: "octets" — the interior quads (a, b) and (b, a), 1 <= a < b < H, share K2 (square
 //    grid, the same symbol in x and y), so one denominator and one (sigma, tau') sum per pole
-//    serve eight modes; items n_oct.. hold two of the remaining 3 (H - 1) quads (diagonal a = b,
-//    axes, Nyquist lines) with their own K2 each.
+//    serve eight modes; items n_oct.. hold one of the remaining 3 (H - 1) quads each (diagonal
+//    a = b, axes, Nyquist lines), computed as a half-discarded octet.
 //  * !OCT: NQ quads per thread in linear quad order.
 // Quad 0 (the four K = 0 corners) is left to the fix-up kernel.
 __host__ __device__ __forceinline__ long r2c_n_oct(int D) {
@@ -572,7 +572,7 @@ __host__ __device__ __forceinline__ long r2c_n_oct(int D) {
 }
 __host__ __device__ __forceinline__ long r2c_items(int D, int nq, bool oct) {
     const long H = D >> 1;
-    if (oct) return r2c_n_oct(D) + (3 * (H - 1) + 1) / 2;
+    if (oct) return r2c_n_oct(D) + 3 * (H - 1);
     return ((long)D * D / 4 + nq - 1) / nq;
 }
 // the s-th of the 3 (H - 1) non-octet quads (s < 3 (H - 1)) as a quad index a * H + b
@@ -582,6 +582,53 @@ __device__ __forceinline__ long r2c_single_quad(long s, int H) {
     else if (s < 2 * (H - 1)) { qa = 0; qb = s - (H - 1) + 1; }
     else { qa = s - 2 * (H - 1) + 1; qb = 0; }
     return qa * H + qb;
+}
+
+// Octet work item -> its two quads (quad index a * H + b), validity, shared K2.
+__device__ __forceinline__ void r2c_octet_item(long item, int D, long quad[2], bool ok[2], bool &shared_k2) {
+    const int H = D >> 1;
+    const long n_oct = r2c_n_oct(D);
+    if (item < n_oct) {
+        // triangular decode: item = b'(b'-1)/2 + a', 0 <= a' < b' <= H - 2; (a, b) = (a'+1, b'+1)
+        long bp = (long)((1.0 + sqrt(1.0 + 8.0 * (double)item)) * 0.5);
+        while (bp * (bp - 1) / 2 > item) --bp;
+        while ((bp + 1) * bp / 2 <= item) ++bp;
+        const long ap = item - bp * (bp - 1) / 2;
+        quad[0] = (ap + 1) * H + (bp + 1);
+        quad[1] = (bp + 1) * H + (ap + 1);
+        ok[0] = ok[1] = true;
+        shared_k2 = true;
+    } else {
+        // one of the other 3 (H - 1) quads, as an octet whose second quad is a discarded copy
+        // of the first: every item then costs the same (one denominator, four pairs per pole),
+        // which keeps warps convergent and the stream-K split balanced (1.2 % extra work)
+        const long sidx = item - n_oct;
+        ok[0] = sidx < 3L * (H - 1);
+        ok[1] = false;
+        quad[0] = quad[1] = ok[0] ? r2c_single_quad(sidx, H) : 1;
+        shared_k2 = true;
+    }
+}
+
+// Representative mode of pair j (0, 1) of a quad: interior quads pair modes (0,3) and (1,2) of
+// quad_modes, axis / Nyquist quads (0,1) and (2,3); the representative is the smaller index.
+__device__ __forceinline__ long r2c_rep(long quad, int j, int D, int log2D) {
+    long mq[4];
+    quad_modes(quad, D, log2D, mq);
+    const int H = D >> 1;
+    const int qa = (int)(quad >> (log2D - 1)), qb = (int)(quad & (H - 1));
+    return j == 0 ? mq[0] : ((qa > 0 && qb > 0) ? mq[1] : mq[2]);
+}
+
+// Stream-K partition of the (tile, pole) iteration space over the persistent CTAs: CTA i owns
+// [W i / P, W (i + 1) / P), W = tiles x poles; sk_cta_of(x) is the CTA owning iteration x.
+__host__ __device__ __forceinline__ long sk_cta_of(long x, long W, long P) {
+    long i = (long)((double)x * (double)P / (double)W);
+    if (i >= P) i = P - 1;
+    if (i < 0) i = 0;
+    while (i + 1 < P && W * (i + 1) / P <= x) ++i;
+    while (i > 0 && W * i / P > x) --i;
+    return i;
 }
 
 // One tile of poles for the thread's four pairs. SHARED: both quads have the same K2 (octet).
@@ -634,27 +681,9 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
     long quad[NQ];
     bool ok[NQ];
     bool shared_k2 = false;
-    if (OCT) {
+    if constexpr (OCT) {
         static_assert(!OCT || NQ == 2, "octet items hold two quads");
-        const long n_oct = r2c_n_oct(a.D);
-        if (item < n_oct) {
-            // triangular decode: item = b'(b'-1)/2 + a', 0 <= a' < b' <= H - 2; (a, b) = (a'+1, b'+1)
-            long bp = (long)((1.0 + sqrt(1.0 + 8.0 * (double)item)) * 0.5);
-            while (bp * (bp - 1) / 2 > item) --bp;
-            while ((bp + 1) * bp / 2 <= item) ++bp;
-            const long ap = item - bp * (bp - 1) / 2;
-            quad[0] = (ap + 1) * H + (bp + 1);
-            quad[NQ - 1] = (bp + 1) * H + (ap + 1);
-            ok[0] = ok[NQ - 1] = true;
-            shared_k2 = true;
-        } else {
-#pragma unroll
-            for (int g = 0; g < NQ; ++g) {
-                const long sidx = 2 * (item - n_oct) + g;
-                ok[g] = sidx < 3L * (H - 1);
-                quad[g] = ok[g] ? r2c_single_quad(sidx, H) : 1;
-            }
-        }
+        r2c_octet_item(item, a.D, quad, ok, shared_k2);
     } else {
 #pragma unroll
         for (int g = 0; g < NQ; ++g) {
@@ -735,6 +764,83 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
                 out[n_modes + rep[2 * g + j]] = cfma(Stau[g], s.d0, s.H1);
             }
         }
+    }
+}
+
+// Stream-K R2C pole kernel (octet items): a persistent grid of P CTAs splits the W = tiles x
+// poles iteration space evenly (every CTA runs the same number of pole iterations, so no wave
+// tail); a CTA walks its range tile segment by tile segment and writes one partial per segment
+// to slot (tile, segment): partial[((tile * slots + s) * 8 + 2 pair + {0: H_eta, 1: H_delta'})
+// * 128 + tid]. finish_r2c_sk_kernel sums the segments of each tile in a fixed order.
+// One 256-thread CTA per SM (8 warps, 2 per scheduler): two independent 128-thread CTAs on one
+// SM do not share the fp64 pipe evenly (the older one is favoured), so with a static split the
+// younger one would finish alone at half the issue rate; warps of one CTA stay within a pole
+// tile of each other (block barrier per tile).
+constexpr int kSkBlock = 256;
+
+template <int PU>
+__global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
+    __shared__ PoleConst sp[kPoleTile];
+    const long n_modes = a.n_modes;
+    const long Nr = a.pole_end - a.pole_begin;
+    const long T = a.sk_tiles, P = gridDim.x;
+    const long W = T * Nr;
+    const long g1 = W * (blockIdx.x + 1) / P;
+    const double c = a.tau;
+    const double hmu = a.hmu;
+    for (long g = W * blockIdx.x / P; g < g1;) {
+        const long t = g / Nr;
+        const long plo = g - t * Nr;
+        const long phi = min(Nr, plo + (g1 - g));
+        const int seg = (int)(blockIdx.x - sk_cta_of(t * Nr, W, P));
+        long quad[2];
+        bool ok[2], shared_k2;
+        r2c_octet_item(t * kSkBlock + threadIdx.x, a.D, quad, ok, shared_k2);
+        double K2[2];
+        PairState st[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const long mm = r2c_rep(quad[j >> 1], j & 1, a.D, a.log2D);
+            const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
+            const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
+            const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
+            const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
+            const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
+            PairState &s = st[j];
+            s.e0 = e;
+            s.d0 = d;
+            s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+            s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
+            s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+            s.H0 = mk(0, 0);
+            s.H1 = mk(0, 0);
+            K2[j >> 1] = fma(kx, kx, ky * ky);
+        }
+        cd Ssig[2] = {mk(0, 0), mk(0, 0)}, Stau[2] = {mk(0, 0), mk(0, 0)};
+        for (long pt = a.pole_begin + plo; pt < a.pole_begin + phi; pt += kPoleTile) {
+            const int cnt = (int)min((long)kPoleTile, a.pole_begin + phi - pt);
+            __syncthreads();
+            {
+                const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
+                double2 *dst = reinterpret_cast<double2 *>(sp);
+                constexpr int kPer = (int)(sizeof(PoleConst) / sizeof(double2));
+                for (int i = threadIdx.x; i < cnt * kPer; i += kSkBlock) dst[i] = src[i];
+            }
+            __syncthreads();
+            if (shared_k2) r2c_tile<PU, 2, true>(sp, cnt, K2, st, Ssig, Stau);
+            else r2c_tile<PU, 2, false>(sp, cnt, K2, st, Ssig, Stau);
+        }
+        if (shared_k2) {
+            Ssig[1] = Ssig[0];
+            Stau[1] = Stau[0];
+        }
+        cd *out = a.partial + (((size_t)t * a.sk_slots + seg) * 8) * kSkBlock + threadIdx.x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            out[(2 * j) * kSkBlock] = cfma(Ssig[j >> 1], st[j].d0, st[j].H0);
+            out[(2 * j + 1) * kSkBlock] = cfma(Stau[j >> 1], st[j].d0, st[j].H1);
+        }
+        g += phi - plo;
     }
 }
 
@@ -933,6 +1039,50 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     a.acc[m] = s0;
     a.acc[n + m] = s1;
     a.acc[2 * n + m] = s2;
+}
+
+// Finish of the stream-K R2C kernel: one thread per (tile, pair, item lane); sums the tile's
+// segment partials in segment order and rebuilds (u, v) from the Hermitian (eta, delta, zeta)
+// sums (as finish_kernel, kind 6) at the representative K and, conjugated, at -K.
+__global__ void __launch_bounds__(256) finish_r2c_sk_kernel(FinishArgs a) {
+    const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = (int)(gid & (kSkBlock - 1)), pair = (int)((gid >> 8) & 3);
+    const long t = gid >> 10;
+    if (t >= a.sk_tiles) return;
+    long quad[2];
+    bool ok[2], shared_k2;
+    r2c_octet_item(t * kSkBlock + tid, a.D, quad, ok, shared_k2);
+    if (!ok[pair >> 1]) return;
+    const long n = a.n_modes;
+    const long r = r2c_rep(quad[pair >> 1], pair & 1, a.D, a.log2D);
+    const int rl = (int)(r >> a.log2D), rk = (int)(r & (a.D - 1));
+    const long mm = ((long)((a.D - rl) & (a.D - 1)) << a.log2D) + ((a.D - rk) & (a.D - 1));
+    const long Nr = a.sk_poles, P = a.sk_ctas, W = a.sk_tiles * Nr;
+    const long i0 = sk_cta_of(t * Nr, W, P), i1 = sk_cta_of((t + 1) * Nr - 1, W, P);
+    cd h0 = mk(0, 0), h1 = mk(0, 0);
+    const cd *p = a.partial + ((size_t)t * a.sk_slots * 8 + 2 * pair) * kSkBlock + tid;
+    for (long s = 0; s <= i1 - i0; ++s) {
+        const cd x0 = p[s * 8 * kSkBlock], x1 = p[(s * 8 + 1) * kSkBlock];
+        h0 = mk(h0.x + x0.x, h0.y + x0.y);
+        h1 = mk(h1.x + x1.x, h1.y + x1.y);
+    }
+    const double kx = a.ksym[rk], ky = a.ksym[rl];
+    const cd e = a.fhat[r], uu = a.fhat[n + r], vv = a.fhat[2 * n + r];
+    const double c = a.tau;
+    // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
+    h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
+    const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
+    const cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
+    const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0 off the corners
+    const cd tt = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
+    const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
+    const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
+    a.acc[r] = h0;
+    a.acc[n + r] = U;
+    a.acc[2 * n + r] = V;
+    a.acc[mm] = mk(h0.x, -h0.y);      // the Hermitian spectrum at -K is the conjugate
+    a.acc[n + mm] = mk(U.x, -U.y);
+    a.acc[2 * n + mm] = mk(V.x, -V.y);
 }
 
 // ============================================================================= K = 0 modes (DZ)
@@ -1188,6 +1338,37 @@ cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaS
     REXI_R2C_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;
+}
+
+#define REXI_R2C_SK_CONFIGS(X) X(1) X(2) X(3) X(4)
+
+cudaError_t launch_poles_r2c_sk(const PoleArgs &a, int pu, int ctas, cudaStream_t st) {
+#define X(U) if (pu == U) { pole_kernel_r2c_sk<U><<<ctas, kSkBlock, 0, st>>>(a); return cudaGetLastError(); }
+    REXI_R2C_SK_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t pole_r2c_sk_occupancy(int pu, int *blocks_per_sm) {
+#define X(U) if (pu == U) \
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2c_sk<U>, kSkBlock, 0);
+    REXI_R2C_SK_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+long pole_r2c_sk_tiles(int D) { return (r2c_items(D, 2, true) + kSkBlock - 1) / kSkBlock; }
+
+long sk_slots_bound(long tiles, long poles, long ctas) {
+    // segments of one tile <= ceil(poles / floor(W / P)) + 1
+    const long per = tiles * poles / ctas;
+    return per > 0 ? (poles + per - 1) / per + 1 : -1;
+}
+
+cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st) {
+    const long threads = a.sk_tiles * 4 * kSkBlock;
+    finish_r2c_sk_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st) {

@@ -69,6 +69,8 @@ struct PoleArgs {
     int D, log2D;
     double tau;            // c (tau-scaled Coriolis)
     double hmu;            // Re(alpha_n) = h mu (same for every pole)
+    long sk_tiles;         // R2C stream-K: tiles of 128 octet items (0: chunked launch)
+    int sk_slots;          // R2C stream-K: partial slots per tile
 };
 
 struct FinishArgs {
@@ -83,6 +85,9 @@ struct FinishArgs {
     double tau;
     cd S;                  // zeta rebuild: sum over the pole range of w1/alpha + w2/|alpha|^2
     cd Sd;                 // kind 5: sum over the pole range of w1
+    long sk_tiles;         // R2C stream-K (see PoleArgs); 0: chunked partials
+    int sk_slots, sk_ctas;
+    long sk_poles;         // pole-range length
 };
 
 struct FixupArgs {

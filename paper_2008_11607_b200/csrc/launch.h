@@ -23,6 +23,12 @@ bool pole_r2c_supported(int mpt, int pu, int minb);
 long pole_r2c_blocks(int D, int mpt);
 cudaError_t pole_r2c_occupancy(int mpt, int pu, int minb, int *blocks_per_sm);
 cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaStream_t st);
+// stream-K R2C (octet items, modes_per_thread 8): persistent grid of `ctas` blocks
+cudaError_t launch_poles_r2c_sk(const PoleArgs &a, int pu, int ctas, cudaStream_t st);
+cudaError_t pole_r2c_sk_occupancy(int pu, int *blocks_per_sm);
+long pole_r2c_sk_tiles(int D);
+long sk_slots_bound(long tiles, long poles, long ctas);
+cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 
@@ -39,14 +45,17 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //     per pair (two modes), num 6/12, numt 6/12, eta 4/6, eta_t 4/6, 4 MACs 16/32 = 36/68.
 //     A quad (4 modes, own K2) = 99 / 179; an octet (8 modes, shared K2) = 171 / 315, i.e.
 //     24.75 / 44.75 resp. 21.375 / 39.375 per mode; modes_per_thread 8 uses octets for the
-//     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and single quads for the other 3(H-1).
+//     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and half-discarded octets for the other
+//     3(H-1) quads.
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
 // by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
 inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
-    if (mpt != 8 || D < 6) return quad / 4.0;
-    const double H = D / 2, n_oct = (H - 1) * (H - 2) / 2, n_single = 3 * (H - 1);
-    return (n_oct * octet + n_single * quad) / (8 * n_oct + 4 * n_single);
+    if (mpt != 8) return quad / 4.0;
+    // every octet item (incl. the 3 (H-1) single quads run as half-discarded octets) costs
+    // `octet`; the work per useful mode counts the discarded half
+    const double H = D / 2, n_oct = H >= 3 ? (H - 1) * (H - 2) / 2 : 0, n_single = 3 * (H - 1);
+    return (n_oct + n_single) * octet / (8 * n_oct + 4 * n_single);
 }
 inline double pole_flops(int kind, int mpt, int D) {
     if (kind == 6) return r2c_per_mode(mpt, D, 179.0, 315.0);

@@ -24,6 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
 VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4, "pfhr": 5}
 METHODS = {"rexii": 0, "rexi": 1}
+SCHEDULES = {"auto": 0, "chunked": 1, "streamk": 2}
 
 _vp = ctypes.c_void_p
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -37,7 +38,8 @@ class PlanInfo(ctypes.Structure):
                 ("M", ctypes.c_long), ("L", ctypes.c_long), ("N", ctypes.c_long),
                 ("n_poles", ctypes.c_long), ("m0", ctypes.c_long), ("rho", ctypes.c_double),
                 ("predicted_floor", ctypes.c_double), ("flops_per_pole_mode", ctypes.c_double),
-                ("fp64_ops_per_pole_mode", ctypes.c_double)]
+                ("fp64_ops_per_pole_mode", ctypes.c_double), ("schedule", ctypes.c_int),
+                ("last_schedule", ctypes.c_int)]
 
 
 EXPORTS = {
@@ -48,6 +50,7 @@ EXPORTS = {
     "rexi_plan_set_variant": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_method": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_plan_set_schedule": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -210,6 +213,12 @@ class Plan:
         v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
         _check(_lib.rexi_plan_set_variant(self._h, v), "rexi_plan_set_variant")
         self.variant = v
+
+    def set_schedule(self, schedule):
+        """'auto' | 'chunked' | 'streamk' distribution of the R2C pole kernel (rexi_plan_set_schedule)."""
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
+        _check(_lib.rexi_plan_set_schedule(self._h, SCHEDULES[schedule]), "rexi_plan_set_schedule")
 
     def set_graphs(self, enable):
         _check(_lib.rexi_plan_set_graphs(self._h, int(bool(enable))), "rexi_plan_set_graphs")

@@ -291,6 +291,38 @@ def test_apply_host_batch_errors(R):
     assert out[0].shape == (0, 8, 8)
 
 
+@pytest.mark.parametrize("D,tau,tol", [(64, 1.0, 1e-12), (128, 1.0, 1e-12), (128, 3.0, 1e-8),
+                                       (256, 0.5, 1e-12)])
+def test_schedules_agree(R, D, tau, tol):
+    """Stream-K and chunked R2C pole schedules: same result up to summation order; stream-K vs
+    the oracle on the smaller cases; AUTO runs the chunked schedule."""
+    import torch
+    f = inputs.white_noise(D, seed=5)
+    fd = [dev(x) for x in f]
+    res = {}
+    for sched in ("chunked", "streamk", "auto"):
+        p = R.Plan(D, tau, tol=tol)
+        p.set_schedule(sched)
+        res[sched] = [host(t) for t in p.apply(*fd)]
+        info = p.info
+        res[sched + "_used"] = info["last_schedule"]
+    assert res["chunked_used"] == 1 and res["auto_used"] == 1
+    assert res["streamk_used"] == 2
+    assert rel_l2(res["streamk"], res["chunked"]) < 1e-14
+    assert rel_l2(res["auto"], res["chunked"]) < 1e-14
+    if D <= 128:
+        info = R.Plan(D, tau, tol=tol).info
+        g = lrsw.rexii_step(*f, tau, info["h"], info["M"])
+        assert rel_l2(res["streamk"], g) < TOL
+
+
+def test_schedule_errors(R):
+    p = R.Plan(16, 0.3)
+    with pytest.raises(ValueError):
+        p.set_schedule("dynamic")
+    assert p.info["schedule"] == 0 and p.info["last_schedule"] == 0
+
+
 def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]

@@ -11,7 +11,8 @@ from paper_2008_11607_b200 import inputs, rexi
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 D, tau, tol = {"c1": (64, 0.02, 1e-12), "c2": (512, 1.0, 1e-8), "c3": (1024, 0.1, 1e-12),
                "c4": (4096, 1.0, 1e-12)}[cfg]
-f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
+import os
+f = [torch.from_numpy(x).cuda() for x in (inputs.white_noise(D) if os.environ.get("TUNE_INPUT") == "white" else inputs.gaussian_scenario(D))]
 res = []
 TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (3, 1, 4), (4, 1, 3), (4, 1, 4)],
            "uv": [(1, 1, 6), (2, 1, 3), (2, 1, 4), (3, 1, 3), (4, 1, 2), (4, 1, 3)],
@@ -25,6 +26,10 @@ for variant in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dz", "uv", "dz
     for mpt, pu, minb in TUNINGS[variant]:
         p = rexi.Plan(D, tau, tol=tol, variant=variant)
         p.set_tuning(mpt, pu, minb)
+        if os.environ.get("TUNE_SCHEDULE"):
+            p.set_schedule(os.environ["TUNE_SCHEDULE"])
+        if os.environ.get("TUNE_NOGRAPH"):
+            p.set_graphs(False)
         F = p.forward(*f)
         out = p.apply(*f)
         acc = p.poles(F)

@@ -100,7 +100,10 @@ typedef enum {
  *                     Re sum_{n=-N}^{N} beta^Re_n (tau A + alpha_n I)^{-1} f0, one solve per
  *                     term, evaluated as the half-sum n = 0..N with Gamma_n (the Appendix A
  *                     table is conjugate-symmetric, so beta^Re_{-n} = conj(beta^Re_n);
- *                     DESIGN.md reading R2). Always uses the DZ back-substitution. */
+ *                     DESIGN.md reading R2). With w2 = 0 the partial-fraction weights are
+ *                     W1 = w1, W2 = 0, so variants PF, PFH and PFHR (default) run the same
+ *                     kernels as REXII; UV, DZ and DZ3 select the DZ back-substitution kernel
+ *                     (one solve per term). */
 typedef enum { REXI_METHOD_REXII = 0, REXI_METHOD_REXI = 1 } rexi_method_t;
 
 typedef struct {

@@ -65,7 +65,17 @@ struct rexi_plan_s {
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
     int kind() const {
-        if (method == REXI_METHOD_REXI) return 2;
+        if (method == REXI_METHOD_REXI) {
+            // REXI: w2 = 0, so the partial-fraction weights are W1 = w1, W2 = 0 and the PF / PFH /
+            // R2C rearrangements hold unchanged (one solve per term and mode: a {K, -K} pair
+            // takes the solves at K and, through the Hermitian symmetry, at -K)
+            switch (variant) {
+                case REXI_VARIANT_PF: return 4;
+                case REXI_VARIANT_PFH: return 5;
+                case REXI_VARIANT_PFHR: return 6;
+                default: return 2;
+            }
+        }
         // tau = 0: every symbol vanishes, (delta, zeta) carry no velocity anywhere -> UV route
         if (host.tau == 0.0) return 1;
         switch (variant) {

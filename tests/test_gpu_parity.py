@@ -431,11 +431,23 @@ def test_rexi_method_vs_oracle(R, D, tau, h, M):
     assert rel_l2(got, ref) < TOL
 
 
+@pytest.mark.parametrize("variant", ["uv", "dz", "dz3", "pf", "pfh", "pfhr"])
+@pytest.mark.parametrize("D,tau,h,M", [(16, 1.0, 0.2, 150), (64, 0.5, 0.2, 500)])
+def test_rexi_method_variants(R, variant, D, tau, h, M):
+    """REXI (w2 = 0) through every variant: the DZ back-substitution kernel (uv, dz, dz3) and
+    the partial-fraction kernels with W1 = w1, W2 = 0 (pf, pfh, pfhr incl. R2C octets)."""
+    f = inputs.white_noise(D, seed=21)
+    p = R.Plan(D, tau, h=h, M=M, method="rexi", variant=variant)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    ref = lrsw.rexi_step(*f, tau, h, M)
+    assert rel_l2(got, ref) < TOL
+
+
 @pytest.mark.parametrize("mpt,pu,minb", [(1, 1, 8), (2, 1, 4), (4, 1, 4), (4, 1, 5)])
 def test_rexi_method_tunings(R, mpt, pu, minb):
     D, tau, h, M = 32, 1.0, 0.2, 300
     f = [dev(x) for x in inputs.white_noise(D)]
-    p = R.Plan(D, tau, h=h, M=M, method="rexi")
+    p = R.Plan(D, tau, h=h, M=M, method="rexi", variant="dz")
     base = [host(t) for t in p.apply(*f)]
     p.set_tuning(mpt, pu, minb)
     got = [host(t) for t in p.apply(*f)]

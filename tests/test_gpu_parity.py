@@ -530,6 +530,36 @@ def test_pfhr_tunings_vs_oracle(R, mpt, pu, minb, D):
     assert rel_l2(got, ref) < TOL
 
 
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_apply_full_size_sampled_vs_oracle(R, cfg):
+    """The bench's launch configuration (default plan: PFHR octet kernel, chunked schedule,
+    whole-step graph) at BASELINE's full sizes, element by element against the oracle on
+    sampled modes: the spectrum of the GPU's physical output at K must equal the Hermitian part
+    of the oracle's dense-LU pole sum, (A(K) + conj A(-K)) / 2 — the spectral form of
+    Re(IDFT(.)). Input spectra: the oracle's naive DFT at 512^2, numpy's FFT
+    above (the naive O(D^3) DFT takes minutes to hours there); output spectra: numpy's FFT."""
+    D, tau, tol, S = {"c2": (512, 1.0, 1e-8, 2048), "c3": (1024, 0.1, 1e-12, 1024),
+                      "c4": (4096, 1.0, 1e-12, 256)}[cfg]
+    f = inputs.white_noise(D, seed=13)
+    p = R.Plan(D, tau, tol=tol)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    ml, mk = inputs.sample_modes(D, S)
+    mlm, mkm = (-ml) % D, (-mk) % D
+    if D <= 512:
+        F = lrsw.spectral_fields(*f)
+    else:
+        F = np.stack([np.fft.fft2(x) / D ** 2 for x in f], axis=-1)
+    Fs, Fm = F[ml, mk, :], F[mlm, mkm, :]
+    del F
+    got_s = np.stack([(np.fft.fft2(g) / D ** 2)[ml, mk] for g in got], axis=-1)
+    n, al, c1, c2, gm = oracle_terms(p).half()
+    A = lrsw.rexii_pole_sum(D, tau, Fs, ml, mk, al, c1, c2, gm)
+    Am = lrsw.rexii_pole_sum(D, tau, Fm, mlm, mkm, al, c1, c2, gm)
+    ref = (A + np.conj(Am)) / 2
+    err = float(np.linalg.norm(got_s - ref) / np.linalg.norm(ref))
+    assert err < TOL, err
+
+
 def test_pfhr_c2_full_size_properties(R):
     """The default (PFHR) at the bench configuration: vs DZ3 (all per-pole components formed)
     and vs the exact propagator."""

@@ -810,8 +810,10 @@ rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u,
         for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(d[i], hin[i], n * sizeof(double), cudaMemcpyHostToDevice, st));
         rexi_status_t s;
-        if ((s = do_step(p, 0, p->host.n_poles, d[0], d[1], d[2], d[3], d[4], d[5], st)) != REXI_OK)
+        if ((s = do_step(p, 0, p->host.n_poles, d[0], d[1], d[2], d[3], d[4], d[5], st)) != REXI_OK) {
+            cudaStreamSynchronize(st);   // the input copies must not outlive the call
             return s;
+        }
         for (int i = 0; i < 3; ++i)
             CK(cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -844,6 +846,7 @@ rexi_status_t rexi_apply_host_batch(rexi_plan_t p, long batch, const double *eta
         const size_t bytes = n * sizeof(double);
         const double *hin[3] = {eta, u, v};
         double *hout[3] = {eo, uo, vo};
+        auto pipeline = [&]() -> rexi_status_t {
         // order the copy streams after whatever the caller queued on `stream` before this call
         CK(cudaEventRecord(p->ev_step[0], st));
         CK(cudaStreamWaitEvent(p->h2d_stream, p->ev_step[0], 0));
@@ -870,8 +873,18 @@ rexi_status_t rexi_apply_host_batch(rexi_plan_t p, long batch, const double *eta
                                    p->d2h_stream));
             CK(cudaEventRecord(p->ev_out[b], p->d2h_stream));
         }
-        CK(cudaStreamSynchronize(p->d2h_stream));
-        CK(cudaStreamSynchronize(st));
+        return REXI_OK;
+        };
+        const rexi_status_t s = pipeline();
+        // drain all three streams, also after an error: no copy may touch the caller's host
+        // buffers once this call has returned
+        const cudaError_t e1 = cudaStreamSynchronize(p->h2d_stream);
+        const cudaError_t e2 = cudaStreamSynchronize(p->d2h_stream);
+        const cudaError_t e3 = cudaStreamSynchronize(st);
+        if (s != REXI_OK) return s;
+        if (e1 != cudaSuccess) return cuda_fail(e1, "cudaStreamSynchronize (h2d)");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamSynchronize (d2h)");
+        if (e3 != cudaSuccess) return cuda_fail(e3, "cudaStreamSynchronize");
         return REXI_OK;
     });
 }

@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--h", default="0.5", help="Gaussian spacing h, or 'auto' (NEXT-2 h_for_tol)")
     ap.add_argument("--tuning", default=None,
                     help="pole kernel tuning 'modes_per_thread,poles_per_iter,min_blocks' (default: plan's)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional check only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -215,10 +217,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if args.backend == "gloo":
+        # functional check of the multi-rank control flow on fewer GPUs than ranks (host-side
+        # all-reduce, no kernel waits on another rank); its timings are not bench numbers
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2008_11607_b200 import rexi
     from paper_2008_11607_b200.distributed import apply_distributed, pole_partition
 

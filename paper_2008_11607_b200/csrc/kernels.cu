@@ -10,6 +10,8 @@
 //    for the DZ variant, recovery of (u, v) from the accumulated (delta, zeta).
 //  * fixup_k0_kernel                  : the K = 0 modes for the DZ variant (velocities
 //    decouple from delta, zeta there): pure Coriolis 2x2 solves per pole.
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -1166,11 +1168,11 @@ static int ilog2(int x) {
 }
 
 // FFT launch shapes: threads per transform tf = max(1, D/8); a row block holds nb row pairs
-// (nb * tf <= 256 threads, nb <= D/2); a column block a strip of C <= 8 half-spectrum slots
-// (C * tf <= 512, C <= D/2).
+// (nb * tf <= 64 threads unless one pair needs more, nb <= D/2); a column block a strip of
+// C <= 4 half-spectrum slots (C * tf <= 512, C <= D/2).
 static int fft_rows_per_block(int D) {
     const int tf = D >= 8 ? D / 8 : 1;
-    int nb = 256 / tf;
+    int nb = 64 / tf;   // small blocks: the passes are latency-bound, more blocks in flight help
     if (nb < 1) nb = 1;
     if (nb > D / 2) nb = D / 2;
     return nb;
@@ -1178,7 +1180,7 @@ static int fft_rows_per_block(int D) {
 static int fft_cols_per_block(int D) {
     const int tf = D >= 8 ? D / 8 : 1;
     int C = 512 / tf;
-    if (C > 8) C = 8;
+    if (C > 4) C = 4;   // measured: 4-column slabs beat 8 at 512^2 (more blocks), equal at 1024^2
     if (C < 1) C = 1;
     if (C > D / 2) C = D / 2;
     return C;

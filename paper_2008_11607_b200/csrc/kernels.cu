@@ -10,8 +10,6 @@
 //    for the DZ variant, recovery of (u, v) from the accumulated (delta, zeta).
 //  * fixup_k0_kernel                  : the K = 0 modes for the DZ variant (velocities
 //    decouple from delta, zeta there): pure Coriolis 2x2 solves per pole.
-#include <cstdlib>
-
 #include "kernels.cuh"
 #include "launch.h"
 

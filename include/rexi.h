@@ -82,8 +82,12 @@ typedef enum {
  *  REXI_VARIANT_PFHR: PFH on "R2C" mode pairs (allowed equivalent): the fields
  *                    are real, so the spectrum is Hermitian and the solves at -K follow from those
  *                    at K; the pair {K, -K} accumulates directly the Hermitian part that survives
- *                    Re(IDFT(.)) (default; used by rexi_apply / apply_partial / apply_host / run;
- *                    rexi_poles, whose input need not be Hermitian, runs PFH). */
+ *                    Re(IDFT(.)). The two Helmholtz solves are formed for every pole and pair;
+ *                    what depends on K2 only is shared: the denominator by the modes of a K2
+ *                    quad or octet ((a, b) and (b, a) on the square grid), and the weight sum of
+ *                    the delta0 term per K2 value. Default; used by rexi_apply /
+ *                    apply_partial / apply_host / apply_host_batch / run; rexi_poles, whose input
+ *                    need not be Hermitian, runs PFH. */
 typedef enum {
     REXI_VARIANT_DZ = 0,
     REXI_VARIANT_UV = 1,
@@ -168,11 +172,13 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
  *   REXII PFH: (1,1,8) (2,1,3) (2,1,4) (3,1,4) (4,1,3) (4,1,4) (1,2,6) (2,2,3) (2,2,4) (4,2,2)
  *                                                                      default (4,2,2)
  *   REXII PFHR: modes_per_thread 4 (one K2 quad = two R2C pairs), 8 (an "octet": quads (a, b)
- *               and (b, a), which share K2, or two of the remaining quads = four pairs) or 16
- *               (two quads in linear order, no K2 sharing):
+ *               and (b, a), which share K2, or one of the remaining quads plus a discarded copy
+ *               = four pairs) or 16 (two quads in linear order, no K2 sharing):
  *               (4,1,4) (4,1,5) (4,1,6) (4,2,3) (4,2,4) (4,4,3) (8,1,2) (8,1,3) (8,2,2) (8,3,2)
- *               (8,4,2) (16,2,2)                                          default (8,4,2)
- *   REXI:      (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
+ *               (8,4,2) (16,2,2)                                          default (8,1,2)
+ *   REXI with variant UV / DZ / DZ3 (DZ back-substitution kernel):
+ *               (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
+ *   REXI with variant PF / PFH / PFHR: as the REXII row of that variant (same kernels).
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).
  * Per pole and mode the operation order is the same for every tuning; the number of pole
@@ -192,8 +198,8 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int p
  *                         SM issue better than one 256-thread block: measured on B200 the
  *                         chunked pole kernel is 2-4 % faster (C2 1.695 vs 1.735 ms, C4 830 vs
  *                         863 ms).
- * STREAMK falls back to CHUNKED when the segment partials do not fit the partial buffer. The kernels of every other variant are
- * always chunked. Schedules differ only in the summation order of the pole sum. Clears the
+ * STREAMK falls back to CHUNKED when the segment partials do not fit the partial buffer. The
+ * kernels of every other variant are always chunked. Schedules differ only in the summation order of the pole sum. Clears the
  * plan's graph cache. EINVAL for an unknown schedule. */
 typedef enum {
     REXI_SCHEDULE_AUTO = 0,

@@ -1,4 +1,4 @@
-"""Print the CUDA path's one-step max-norm errors for the paper's Table 2-7 rows (GPU box)."""
+"""(Test-side script: it uses the oracle's exact propagator.) Print the CUDA path's one-step max-norm errors for the paper's Table 2-7 rows (GPU box)."""
 import json
 import sys
 import time

@@ -1,7 +1,7 @@
-"""C5 sweep (BASELINE configs[4]): error vs the exact propagator and
+"""(Test-side script: it uses the oracle's exact propagator.) C5 sweep (BASELINE configs[4]): error vs the exact propagator and
 throughput vs the number of REXII terms, on the GPU path (GPU box).
 
-    python tools/sweep.py [D] > profiles/r01_sweep.jsonl
+    python tests/scripts/sweep.py [D] > profiles/r01_sweep_c5_<D>.jsonl
 
 White-noise fields (every Fourier mode excited, so the largest |K| of the grid — the rho of
 the M rule — is present; the Gaussian bump's spectrum dies long before it and hides the

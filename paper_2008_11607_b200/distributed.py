@@ -42,3 +42,17 @@ def apply_distributed(plan, eta, u, v, out=None, group=None):
         plan.apply_partial(b, e, eta, u, v, out=(buf[0], buf[1], buf[2]))
 
     return pole_parallel_step(partial, plan.n_poles, out, group)
+
+
+def run_distributed(plan, steps, eta, u, v, group=None):
+    """`steps` REXII steps in place (S6, T_final = steps * tau) with every step's poles split
+    over the ranks of `group`: per step one pole-parallel `apply_distributed` (its own
+    all-reduce), the summed fields becoming the next step's input. Returns (eta, u, v)."""
+    import torch
+    buf = torch.empty((3, plan.D, plan.D), dtype=torch.float64, device=eta.device)
+    for _ in range(int(steps)):
+        apply_distributed(plan, eta, u, v, out=buf, group=group)
+        eta.copy_(buf[0])
+        u.copy_(buf[1])
+        v.copy_(buf[2])
+    return eta, u, v

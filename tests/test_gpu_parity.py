@@ -323,6 +323,20 @@ def test_schedule_errors(R):
     assert p.info["schedule"] == 0 and p.info["last_schedule"] == 0
 
 
+def test_run_distributed_single_rank_matches_run(R):
+    """distributed.run_distributed (per-step pole split + all-reduce; one rank here) equals the
+    spectral-resident rexi_run up to rounding."""
+    from paper_2008_11607_b200.distributed import run_distributed
+    D, tau = 32, 0.7
+    f = inputs.white_noise(D, seed=31)
+    p = R.Plan(D, tau)
+    a = [dev(x) for x in f]
+    b = [dev(x) for x in f]
+    p.run(3, *a)
+    run_distributed(p, 3, *b)
+    assert rel_l2([host(x) for x in b], [host(x) for x in a]) < 1e-13
+
+
 def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]

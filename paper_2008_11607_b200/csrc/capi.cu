@@ -57,7 +57,7 @@ struct rexi_plan_s {
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 1}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
+    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 8}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
     int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     int sk_occ = 0;                            // same, stream-K R2C kernel
     int schedule = REXI_SCHEDULE_AUTO;

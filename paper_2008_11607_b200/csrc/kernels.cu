@@ -652,16 +652,26 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
             Ssig[g] = cjfms(mk(P.W2r, P.W2i), qd[g], mk(Ssig[g].x + W1q.x, Ssig[g].y - W1q.y));
             Stau[g] = cjfms(mk(P.P2r, P.P2i), qd[g], mk(Stau[g].x + P1q.x, Stau[g].y - P1q.y));
         }
+        // the solve's division by the Helmholtz symbol, eta1 = q num1 and eta_t = conj(q) num_t,
+        // fused with the accumulation weights: X1 eta1 = (X1 q) num1 etc. (per pole and K2)
+        cd Aq[NG], Bq[NG], Cq[NG], Eq[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            Aq[g] = cmul(X1, qd[g]);
+            Cq[g] = cmul(Y1, qd[g]);
+            Bq[g] = cjfma(qd[g], X2, mk(0, 0));   // X2 conj(q)
+            Eq[g] = cjfma(qd[g], Y2, mk(0, 0));   // Y2 conj(q)
+        }
 #pragma unroll
         for (int j = 0; j < 2 * NQ; ++j) {
-            const cd q = qd[SHARED ? 0 : j >> 1];
+            const int g = SHARED ? 0 : j >> 1;
             PairState &s = st[j];
             const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
-            const cd eta1 = cmul(cfms(s2, s.m0, t), q);
+            const cd num1 = cfms(s2, s.m0, t);                                     // eta1 = q num1
             const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
-            const cd etat = cjfma(q, cjfms(s2, s.m0, tt), mk(0, 0));
-            s.H0 = cfma(X2, etat, cfma(X1, eta1, s.H0));
-            s.H1 = cfma(Y2, etat, cfma(Y1, eta1, s.H1));
+            const cd numt = cjfms(s2, s.m0, tt);                                   // eta_t = conj(q) numt
+            s.H0 = cfma(Bq[g], numt, cfma(Aq[g], num1, s.H0));
+            s.H1 = cfma(Eq[g], numt, cfma(Cq[g], num1, s.H1));
         }
     }
 }
@@ -743,10 +753,11 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
             for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
         }
         __syncthreads();
-        if (OCT && shared_k2) r2c_tile<PU, NQ, true>(sp, cnt, K2, st, Ssig, Stau);
+        // octet items always share K2 (single quads run as half-discarded octets)
+        if constexpr (OCT) r2c_tile<PU, NQ, true>(sp, cnt, K2, st, Ssig, Stau);
         else r2c_tile<PU, NQ, false>(sp, cnt, K2, st, Ssig, Stau);
     }
-    if (OCT && shared_k2) {
+    if (OCT) {
 #pragma unroll
         for (int g = 1; g < NQ; ++g) {
             Ssig[g] = Ssig[0];
@@ -827,10 +838,9 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
                 for (int i = threadIdx.x; i < cnt * kPer; i += kSkBlock) dst[i] = src[i];
             }
             __syncthreads();
-            if (shared_k2) r2c_tile<PU, 2, true>(sp, cnt, K2, st, Ssig, Stau);
-            else r2c_tile<PU, 2, false>(sp, cnt, K2, st, Ssig, Stau);
+            r2c_tile<PU, 2, true>(sp, cnt, K2, st, Ssig, Stau);   // octet items share K2
         }
-        if (shared_k2) {
+        {
             Ssig[1] = Ssig[0];
             Stau[1] = Stau[0];
         }
@@ -1308,7 +1318,7 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
 // thread in linear order (eight modes, no K2 sharing; kept for comparison).
 #define REXI_R2C_CONFIGS(X) \
     X(4, 1, 4) X(4, 1, 5) X(4, 1, 6) X(4, 2, 3) X(4, 2, 4) X(4, 4, 3) \
-    X(8, 1, 2) X(8, 1, 3) X(8, 2, 2) X(8, 3, 2) X(8, 4, 2) X(16, 2, 2)
+    X(8, 1, 2) X(8, 1, 3) X(8, 2, 2) X(8, 3, 2) X(8, 4, 2) X(8, 8, 2) X(16, 2, 2)
 #define R2C_KERNEL(M, U, B) pole_kernel_r2c<U, B, ((M) == 4 ? 1 : 2), ((M) == 8)>
 
 bool pole_r2c_supported(int mpt, int pu, int minb) {

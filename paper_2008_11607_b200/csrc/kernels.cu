@@ -398,6 +398,9 @@ constexpr int kPoleBlock = 128;
 #define REXI_POLE_TILE 32
 #endif
 constexpr int kPoleTile = REXI_POLE_TILE;
+// the R2C kernels run 2 blocks per SM, so they can afford a 4x larger pole tile in shared
+// memory (36 KB): fewer block barriers per pole (measured ~1 % faster than 32)
+constexpr int kR2CTile = 128;
 
 struct ModeState {
     cd e0, B0, m0, ua, vb;   // f0 = (e0, ua, vb); B0 = h mu e0 + delta0; m0 = zeta0 - c e0
@@ -678,7 +681,7 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
 
 template <int PU, int MINB, int NQ, bool OCT>
 __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
-    __shared__ PoleConst sp[kPoleTile];
+    __shared__ PoleConst sp[kR2CTile];
     const long n_modes = a.n_modes;
     const int chunk = blockIdx.y;
     const long len = a.pole_end - a.pole_begin;
@@ -743,8 +746,8 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
         Stau[g] = mk(0, 0);
     }
 
-    for (long pt = p0; pt < p1; pt += kPoleTile) {
-        const int cnt = (int)min((long)kPoleTile, p1 - pt);
+    for (long pt = p0; pt < p1; pt += kR2CTile) {
+        const int cnt = (int)min((long)kR2CTile, p1 - pt);
         __syncthreads();
         {
             const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
@@ -791,7 +794,7 @@ constexpr int kSkBlock = 256;
 
 template <int PU>
 __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
-    __shared__ PoleConst sp[kPoleTile];
+    __shared__ PoleConst sp[kR2CTile];
     const long n_modes = a.n_modes;
     const long Nr = a.pole_end - a.pole_begin;
     const long T = a.sk_tiles, P = gridDim.x;
@@ -828,8 +831,8 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
             K2[j >> 1] = fma(kx, kx, ky * ky);
         }
         cd Ssig[2] = {mk(0, 0), mk(0, 0)}, Stau[2] = {mk(0, 0), mk(0, 0)};
-        for (long pt = a.pole_begin + plo; pt < a.pole_begin + phi; pt += kPoleTile) {
-            const int cnt = (int)min((long)kPoleTile, a.pole_begin + phi - pt);
+        for (long pt = a.pole_begin + plo; pt < a.pole_begin + phi; pt += kR2CTile) {
+            const int cnt = (int)min((long)kR2CTile, a.pole_begin + phi - pt);
             __syncthreads();
             {
                 const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
@@ -1350,7 +1353,7 @@ cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaS
     return cudaErrorInvalidValue;
 }
 
-#define REXI_R2C_SK_CONFIGS(X) X(1) X(2) X(3) X(4)
+#define REXI_R2C_SK_CONFIGS(X) X(1) X(2) X(3) X(4) X(8)
 
 cudaError_t launch_poles_r2c_sk(const PoleArgs &a, int pu, int ctas, cudaStream_t st) {
 #define X(U) if (pu == U) { pole_kernel_r2c_sk<U><<<ctas, kSkBlock, 0, st>>>(a); return cudaGetLastError(); }

@@ -1,5 +1,5 @@
 """A/B the pole-kernel schedules (chunked vs stream-K) on one config, interleaved (GPU box).
-    python tools/ab_sched.py c2 [rounds]"""
+    python tools/ab_sched.py c2 [rounds] [pu list, e.g. 1,2,8]"""
 import sys
 
 sys.path.insert(0, ".")
@@ -9,11 +9,12 @@ from paper_2008_11607_b200 import inputs, rexi
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+pus = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2]
 D, tau, tol = {"c2": (512, 1.0, 1e-8), "c3": (1024, 0.1, 1e-12), "c4": (4096, 1.0, 1e-12)}[cfg]
 f = [torch.from_numpy(x).cuda() for x in inputs.gaussian_scenario(D)]
 plans = {}
 for sched in ("chunked", "streamk"):
-    for pu in (1, 2):
+    for pu in pus:
         p = rexi.Plan(D, tau, tol=tol)
         p.set_schedule(sched)
         p.set_tuning(8, pu, 2)

@@ -635,35 +635,38 @@ __host__ __device__ __forceinline__ long sk_cta_of(long x, long W, long P) {
 }
 
 // One tile of poles for the thread's four pairs. SHARED: both quads have the same K2 (octet).
+// Pole sums of the delta0 weights, kept as sigma = conj(S1) - S2 with S1 = sum W1 q and
+// S2 = sum conj(W2) q (and tau' = conj(T1) - T2 with P1, P2): two complex MACs per pole each.
+struct DSums {
+    cd s1, s2, t1, t2;
+    __device__ __forceinline__ cd sigma() const { return mk(s1.x - s2.x, -s1.y - s2.y); }
+    __device__ __forceinline__ cd tau() const { return mk(t1.x - t2.x, -t1.y - t2.y); }
+};
+__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0), mk(0, 0), mk(0, 0)}; }
+
 template <int PU, int NQ, bool SHARED>
 __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const double (&K2)[NQ],
-                                         PairState (&st)[2 * NQ], cd (&Ssig)[NQ], cd (&Stau)[NQ]) {
+                                         PairState (&st)[2 * NQ], DSums (&ds)[NQ]) {
     constexpr int NG = SHARED ? 1 : NQ;
 #pragma unroll PU
     for (int qq = 0; qq < cnt; ++qq) {
         const PoleConst &P = sp[qq];
         const cd s2 = mk(P.s2r, P.s2i);
         const double hn = P.ai;
-        const cd X1 = mk(P.X1r, P.X1i), X2 = mk(P.X2r, P.X2i);
-        const cd Y1 = mk(P.Y1r, P.Y1i), Y2 = mk(P.Y2r, P.Y2i);
-        cd qd[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) {
-            qd[g] = pole_den(P, K2[g]);
-            // sigma = conj(W1 q) - conj(W2) q ; tau' = conj(P1 q) - conj(P2) q  (per pole, quad)
-            const cd W1q = cmul(mk(P.W1r, P.W1i), qd[g]), P1q = cmul(mk(P.P1r, P.P1i), qd[g]);
-            Ssig[g] = cjfms(mk(P.W2r, P.W2i), qd[g], mk(Ssig[g].x + W1q.x, Ssig[g].y - W1q.y));
-            Stau[g] = cjfms(mk(P.P2r, P.P2i), qd[g], mk(Stau[g].x + P1q.x, Stau[g].y - P1q.y));
-        }
+        const cd X1 = mk(P.X1r, P.X1i), Y1 = mk(P.Y1r, P.Y1i);
         // the solve's division by the Helmholtz symbol, eta1 = q num1 and eta_t = conj(q) num_t,
-        // fused with the accumulation weights: X1 eta1 = (X1 q) num1 etc. (per pole and K2)
-        cd Aq[NG], Bq[NG], Cq[NG], Eq[NG];
+        // fused with the accumulation weights: X1 eta1 = (X1 q) num1, X2 eta_t = conj(X1 q) num_t
+        // (X2 = conj(X1), Y2 = conj(Y1) by construction, planner.cpp), per pole and K2
+        cd Aq[NG], Cq[NG];
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
-            Aq[g] = cmul(X1, qd[g]);
-            Cq[g] = cmul(Y1, qd[g]);
-            Bq[g] = cjfma(qd[g], X2, mk(0, 0));   // X2 conj(q)
-            Eq[g] = cjfma(qd[g], Y2, mk(0, 0));   // Y2 conj(q)
+            const cd q = pole_den(P, K2[g]);
+            ds[g].s1 = cfma(mk(P.W1r, P.W1i), q, ds[g].s1);
+            ds[g].s2 = cjfma(mk(P.W2r, P.W2i), q, ds[g].s2);
+            ds[g].t1 = cfma(mk(P.P1r, P.P1i), q, ds[g].t1);
+            ds[g].t2 = cjfma(mk(P.P2r, P.P2i), q, ds[g].t2);
+            Aq[g] = cmul(X1, q);
+            Cq[g] = cmul(Y1, q);
         }
 #pragma unroll
         for (int j = 0; j < 2 * NQ; ++j) {
@@ -673,8 +676,8 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
             const cd num1 = cfms(s2, s.m0, t);                                     // eta1 = q num1
             const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
             const cd numt = cjfms(s2, s.m0, tt);                                   // eta_t = conj(q) numt
-            s.H0 = cfma(Bq[g], numt, cfma(Aq[g], num1, s.H0));
-            s.H1 = cfma(Eq[g], numt, cfma(Cq[g], num1, s.H1));
+            s.H0 = cjfma(Aq[g], numt, cfma(Aq[g], num1, s.H0));
+            s.H1 = cjfma(Cq[g], numt, cfma(Cq[g], num1, s.H1));
         }
     }
 }
@@ -739,12 +742,9 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
     }
     // the d0 terms of H_eta and H_delta' have pole-sum coefficients that depend on K2 only
     // (sigma, tau'): summed once per K2, applied to d0 after the pole loop
-    cd Ssig[NQ], Stau[NQ];
+    DSums ds[NQ];
 #pragma unroll
-    for (int g = 0; g < NQ; ++g) {
-        Ssig[g] = mk(0, 0);
-        Stau[g] = mk(0, 0);
-    }
+    for (int g = 0; g < NQ; ++g) ds[g] = dsums_zero();
 
     for (long pt = p0; pt < p1; pt += kR2CTile) {
         const int cnt = (int)min((long)kR2CTile, p1 - pt);
@@ -757,14 +757,13 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
         }
         __syncthreads();
         // octet items always share K2 (single quads run as half-discarded octets)
-        if constexpr (OCT) r2c_tile<PU, NQ, true>(sp, cnt, K2, st, Ssig, Stau);
-        else r2c_tile<PU, NQ, false>(sp, cnt, K2, st, Ssig, Stau);
+        if constexpr (OCT) r2c_tile<PU, NQ, true>(sp, cnt, K2, st, ds);
+        else r2c_tile<PU, NQ, false>(sp, cnt, K2, st, ds);
     }
     if (OCT) {
 #pragma unroll
         for (int g = 1; g < NQ; ++g) {
-            Ssig[g] = Ssig[0];
-            Stau[g] = Stau[0];
+            ds[g] = ds[0];
         }
     }
     cd *out = a.partial + (size_t)chunk * 3 * n_modes;
@@ -774,8 +773,8 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const PairState &s = st[2 * g + j];
-                out[rep[2 * g + j]] = cfma(Ssig[g], s.d0, s.H0);
-                out[n_modes + rep[2 * g + j]] = cfma(Stau[g], s.d0, s.H1);
+                out[rep[2 * g + j]] = cfma(ds[g].sigma(), s.d0, s.H0);
+                out[n_modes + rep[2 * g + j]] = cfma(ds[g].tau(), s.d0, s.H1);
             }
         }
     }
@@ -830,7 +829,7 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
             s.H1 = mk(0, 0);
             K2[j >> 1] = fma(kx, kx, ky * ky);
         }
-        cd Ssig[2] = {mk(0, 0), mk(0, 0)}, Stau[2] = {mk(0, 0), mk(0, 0)};
+        DSums ds[2] = {dsums_zero(), dsums_zero()};
         for (long pt = a.pole_begin + plo; pt < a.pole_begin + phi; pt += kR2CTile) {
             const int cnt = (int)min((long)kR2CTile, a.pole_begin + phi - pt);
             __syncthreads();
@@ -841,17 +840,16 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
                 for (int i = threadIdx.x; i < cnt * kPer; i += kSkBlock) dst[i] = src[i];
             }
             __syncthreads();
-            r2c_tile<PU, 2, true>(sp, cnt, K2, st, Ssig, Stau);   // octet items share K2
+            r2c_tile<PU, 2, true>(sp, cnt, K2, st, ds);   // octet items share K2
         }
         {
-            Ssig[1] = Ssig[0];
-            Stau[1] = Stau[0];
+            ds[1] = ds[0];
         }
         cd *out = a.partial + (((size_t)t * a.sk_slots + seg) * 8) * kSkBlock + threadIdx.x;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            out[(2 * j) * kSkBlock] = cfma(Ssig[j >> 1], st[j].d0, st[j].H0);
-            out[(2 * j + 1) * kSkBlock] = cfma(Stau[j >> 1], st[j].d0, st[j].H1);
+            out[(2 * j) * kSkBlock] = cfma(ds[j >> 1].sigma(), st[j].d0, st[j].H0);
+            out[(2 * j + 1) * kSkBlock] = cfma(ds[j >> 1].tau(), st[j].d0, st[j].H1);
         }
         g += phi - plo;
     }

@@ -558,9 +558,19 @@ __device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) 
 // see r2c work items below); the corner quad (four self-mirror K = 0 modes) is left to
 // fixup_k0_kernel.
 struct PairState {
-    cd e0, B0, Bt0, m0, d0;  // data of the representative mode
+    cd e0, E2, D2, m0;       // data of the representative mode: eta0, 2 h mu eta0, 2 delta0, m0
     cd H0, H1;               // Hermitian accumulators: eta, delta' (before the e0 term)
 };
+
+// Per-pair state from the mode's spectrum (e = eta0^, d = delta0, z = zeta0).
+__device__ __forceinline__ void pair_setup(PairState &s, cd e, cd d, cd z, double hmu, double c) {
+    s.e0 = e;
+    s.E2 = mk(2.0 * hmu * e.x, 2.0 * hmu * e.y);
+    s.D2 = mk(2.0 * d.x, 2.0 * d.y);
+    s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+    s.H0 = mk(0, 0);
+    s.H1 = mk(0, 0);
+}
 
 // Work items of the R2C kernel (four pairs = eight modes per thread):
 //  * OCT: "octets" — the interior quads (a, b) and (b, a), 1 <= a < b < H, share K2 (square
@@ -651,8 +661,6 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
 #pragma unroll PU
     for (int qq = 0; qq < cnt; ++qq) {
         const PoleConst &P = sp[qq];
-        const cd s2 = mk(P.s2r, P.s2i);
-        const double hn = P.ai;
         const cd X1 = mk(P.X1r, P.X1i), Y1 = mk(P.Y1r, P.Y1i);
         // the solve's division by the Helmholtz symbol, eta1 = q num1 and eta_t = conj(q) num_t,
         // fused with the accumulation weights: X1 eta1 = (X1 q) num1, X2 eta_t = conj(X1 q) num_t
@@ -668,16 +676,23 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
             Aq[g] = cmul(X1, q);
             Cq[g] = cmul(Y1, q);
         }
+        // The two Helmholtz right-hand sides of the pair, num1 = B0 + i hn eta0 - (c/alpha) m0
+        // and num_t = Bt0 - i hn eta0 - conj(c/alpha) m0 (B0, Bt0 = h mu eta0 +- delta0), carry
+        // conjugate weights (X1 q and its conjugate), so X1 q num1 + conj(X1 q) num_t
+        // = Re(X1 q) (num1 + num_t) + i Im(X1 q) (num1 - num_t), with
+        //   num1 + num_t = 2 h mu eta0 - 2 Re(c/alpha) m0,
+        //   num1 - num_t = 2 delta0 + i (2 h n eta0 - 2 Im(c/alpha) m0)
+        // (every pair still forms its right-hand sides for every pole, in this sum/difference basis)
+        const double r2 = P.sr2, k2 = P.si2, g2 = P.hn2;
 #pragma unroll
         for (int j = 0; j < 2 * NQ; ++j) {
             const int g = SHARED ? 0 : j >> 1;
             PairState &s = st[j];
-            const cd t = mk(fma(-hn, s.e0.y, s.B0.x), fma(hn, s.e0.x, s.B0.y));    // B0 + i hn e0
-            const cd num1 = cfms(s2, s.m0, t);                                     // eta1 = q num1
-            const cd tt = mk(fma(hn, s.e0.y, s.Bt0.x), fma(-hn, s.e0.x, s.Bt0.y));  // Bt0 - i hn e0
-            const cd numt = cjfms(s2, s.m0, tt);                                   // eta_t = conj(q) numt
-            s.H0 = cjfma(Aq[g], numt, cfma(Aq[g], num1, s.H0));
-            s.H1 = cjfma(Cq[g], numt, cfma(Cq[g], num1, s.H1));
+            const cd S = mk(fma(-r2, s.m0.x, s.E2.x), fma(-r2, s.m0.y, s.E2.y));       // num1 + num_t
+            const cd w = mk(fma(-k2, s.m0.x, g2 * s.e0.x), fma(-k2, s.m0.y, g2 * s.e0.y));
+            const cd Dd = mk(s.D2.x - w.y, s.D2.y + w.x);                               // num1 - num_t
+            s.H0 = mk(fma(Aq[g].x, S.x, fma(-Aq[g].y, Dd.y, s.H0.x)), fma(Aq[g].x, S.y, fma(Aq[g].y, Dd.x, s.H0.y)));
+            s.H1 = mk(fma(Cq[g].x, S.x, fma(-Cq[g].y, Dd.y, s.H1.x)), fma(Cq[g].x, S.y, fma(Cq[g].y, Dd.x, s.H1.y)));
         }
     }
 }
@@ -729,14 +744,7 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
             const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
             const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
             const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
-            PairState &s = st[2 * g + j];
-            s.e0 = e;
-            s.d0 = d;
-            s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
-            s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
-            s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
-            s.H0 = mk(0, 0);
-            s.H1 = mk(0, 0);
+            pair_setup(st[2 * g + j], e, d, z, hmu, c);
             K2[g] = fma(kx, kx, ky * ky);
         }
     }
@@ -773,8 +781,9 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const PairState &s = st[2 * g + j];
-                out[rep[2 * g + j]] = cfma(ds[g].sigma(), s.d0, s.H0);
-                out[n_modes + rep[2 * g + j]] = cfma(ds[g].tau(), s.d0, s.H1);
+                const cd d0 = mk(0.5 * s.D2.x, 0.5 * s.D2.y);
+                out[rep[2 * g + j]] = cfma(ds[g].sigma(), d0, s.H0);
+                out[n_modes + rep[2 * g + j]] = cfma(ds[g].tau(), d0, s.H1);
             }
         }
     }
@@ -819,14 +828,7 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
             const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
             const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
             const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
-            PairState &s = st[j];
-            s.e0 = e;
-            s.d0 = d;
-            s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
-            s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
-            s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
-            s.H0 = mk(0, 0);
-            s.H1 = mk(0, 0);
+            pair_setup(st[j], e, d, z, hmu, c);
             K2[j >> 1] = fma(kx, kx, ky * ky);
         }
         DSums ds[2] = {dsums_zero(), dsums_zero()};
@@ -848,8 +850,9 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
         cd *out = a.partial + (((size_t)t * a.sk_slots + seg) * 8) * kSkBlock + threadIdx.x;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            out[(2 * j) * kSkBlock] = cfma(ds[j >> 1].sigma(), st[j].d0, st[j].H0);
-            out[(2 * j + 1) * kSkBlock] = cfma(ds[j >> 1].tau(), st[j].d0, st[j].H1);
+            const cd d0 = mk(0.5 * st[j].D2.x, 0.5 * st[j].D2.y);
+            out[(2 * j) * kSkBlock] = cfma(ds[j >> 1].sigma(), d0, st[j].H0);
+            out[(2 * j + 1) * kSkBlock] = cfma(ds[j >> 1].tau(), d0, st[j].H1);
         }
         g += phi - plo;
     }

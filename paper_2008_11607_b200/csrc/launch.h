@@ -43,10 +43,10 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //   kind 5 (PFH): PF without the two delta back-substitutions (4/8 each): 43 / 79
 //   kind 6 (R2C pairs, real input): per K2 value, den 7/11, the four sums behind sigma and tau'
 //     (sum W1 q, sum conj(W2) q, sum P1 q, sum conj(P2) q) 16/32 and the two fused weights
-//     X1 q, Y1 q 8/12 (X2 conj q, Y2 conj q are their conjugates); per pair (two modes) the two
-//     Helmholtz right-hand sides num1, num_t 12/24 and 4 MACs 16/32 = 28/56.
-//     A quad (4 modes, own K2) = 87 / 167; an octet (8 modes, shared K2) = 143 / 279, i.e.
-//     21.75 / 41.75 resp. 17.875 / 34.875 per mode; modes_per_thread 8 uses octets for the
+//     X1 q, Y1 q 8/12; per pair (two modes) the sum and difference of the two Helmholtz
+//     right-hand sides, num1 + num_t 2/4 and num1 - num_t 6/8, and 8 real-times-complex MACs 8/16
+//     = 16/28. A quad (4 modes, own K2) = 63 / 111; an octet (8 modes, shared K2) = 95 / 167,
+//     i.e. 15.75 / 27.75 resp. 11.875 / 20.875 per mode; modes_per_thread 8 uses octets for the
 //     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and half-discarded octets for the other
 //     3(H-1) quads.
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
@@ -60,12 +60,12 @@ inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
     return (n_oct + n_single) * octet / (8 * n_oct + 4 * n_single);
 }
 inline double pole_flops(int kind, int mpt, int D) {
-    if (kind == 6) return r2c_per_mode(mpt, D, 167.0, 279.0);
+    if (kind == 6) return r2c_per_mode(mpt, D, 111.0, 167.0);
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt, int D) {
-    if (kind == 6) return r2c_per_mode(mpt, D, 87.0, 143.0);
+    if (kind == 6) return r2c_per_mode(mpt, D, 63.0, 95.0);
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

@@ -229,12 +229,14 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             const cld P1 = W1 * alpha, P2 = -W2 * std::conj(alpha);
             q.P1r = (double)P1.real();  q.P1i = (double)P1.imag();
             q.P2r = (double)P2.real();  q.P2i = (double)P2.imag();
-            const cld X1 = (W1 + std::conj(W2)) * 0.5L, X2 = (W2 + std::conj(W1)) * 0.5L;
-            const cld Y1 = (P1 + std::conj(P2)) * 0.5L, Y2 = (P2 + std::conj(P1)) * 0.5L;
+            // R2C half-weights; the partner weights (W2 + conj W1)/2 and (P2 + conj P1)/2 are the
+            // conjugates of these, which the kernel uses directly
+            const cld X1 = (W1 + std::conj(W2)) * 0.5L;
+            const cld Y1 = (P1 + std::conj(P2)) * 0.5L;
             q.X1r = (double)X1.real();  q.X1i = (double)X1.imag();
-            q.X2r = (double)X2.real();  q.X2i = (double)X2.imag();
             q.Y1r = (double)Y1.real();  q.Y1i = (double)Y1.imag();
-            q.Y2r = (double)Y2.real();  q.Y2i = (double)Y2.imag();
+            q.sr2 = 2.0 * q.s2r;        q.si2 = 2.0 * q.s2i;        // exact (power-of-two scaling)
+            q.hn2 = 2.0 * q.ai;         q.pad0 = 0.0;
         }
         q.ia2 = (double)std::norm(ia);
     }

@@ -37,10 +37,10 @@ struct alignas(16) PoleConst {
     double W2r, W2i;    //                                       w2 / (2 h mu)
     double P1r, P1i;    // PFH: W1 alpha          (delta1 = alpha eta1 - e0 folded into the weights)
     double P2r, P2i;    // PFH: -W2 conj(alpha)   (delta_t = e0 - conj(alpha) eta_t)
-    double X1r, X1i;    // R2C pairs: (W1 + conj W2)/2
-    double X2r, X2i;    //            (W2 + conj W1)/2
-    double Y1r, Y1i;    //            (P1 + conj P2)/2
-    double Y2r, Y2i;    //            (P2 + conj P1)/2
+    double X1r, X1i;    // R2C pairs: (W1 + conj W2)/2 (the partner weight (W2 + conj W1)/2 is its conjugate)
+    double sr2, si2;    //            2 Re(c/alpha), 2 Im(c/alpha)
+    double Y1r, Y1i;    //            (P1 + conj P2)/2 (partner: its conjugate)
+    double hn2, pad0;   //            2 h n = 2 Im(alpha)
 };
 static_assert(sizeof(PoleConst) == 288, "PoleConst layout");
 

@@ -175,7 +175,7 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
  *               and (b, a), which share K2, or one of the remaining quads plus a discarded copy
  *               = four pairs) or 16 (two quads in linear order, no K2 sharing):
  *               (4,1,4) (4,1,5) (4,1,6) (4,2,3) (4,2,4) (4,4,3) (8,1,2) (8,1,3) (8,2,2) (8,3,2)
- *               (8,4,2) (8,8,2) (16,2,2)                                  default (8,8,2)
+ *               (8,4,2) (8,8,2) (8,2,3) (8,4,3) (8,8,3) (16,2,2)          default (8,8,2)
  *   REXI with variant UV / DZ / DZ3 (DZ back-substitution kernel):
  *               (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
  *   REXI with variant PF / PFH / PFHR: as the REXII row of that variant (same kernels).

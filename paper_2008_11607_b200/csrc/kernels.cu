@@ -1322,7 +1322,7 @@ cudaError_t launch_poles(const PoleArgs &a, int variant, int mpt, int pu, int mi
 // thread in linear order (eight modes, no K2 sharing; kept for comparison).
 #define REXI_R2C_CONFIGS(X) \
     X(4, 1, 4) X(4, 1, 5) X(4, 1, 6) X(4, 2, 3) X(4, 2, 4) X(4, 4, 3) \
-    X(8, 1, 2) X(8, 1, 3) X(8, 2, 2) X(8, 3, 2) X(8, 4, 2) X(8, 8, 2) X(16, 2, 2)
+    X(8, 1, 2) X(8, 1, 3) X(8, 2, 2) X(8, 3, 2) X(8, 4, 2) X(8, 8, 2) X(8, 2, 3) X(8, 4, 3) X(8, 8, 3) X(16, 2, 2)
 #define R2C_KERNEL(M, U, B) pole_kernel_r2c<U, B, ((M) == 4 ? 1 : 2), ((M) == 8)>
 
 bool pole_r2c_supported(int mpt, int pu, int minb) {

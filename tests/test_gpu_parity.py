@@ -529,7 +529,8 @@ def test_run_spectral_resident_matches_repeated_apply(R, graphs):
 
 @pytest.mark.parametrize("mpt,pu,minb", [(4, 1, 4), (4, 1, 5), (4, 1, 6), (4, 2, 3), (4, 2, 4),
                                          (4, 4, 3), (8, 1, 2), (8, 1, 3), (8, 2, 2), (8, 3, 2),
-                                         (8, 4, 2), (8, 8, 2), (16, 2, 2)])
+                                         (8, 4, 2), (8, 8, 2), (8, 2, 3), (8, 4, 3), (8, 8, 3),
+                                         (16, 2, 2)])
 @pytest.mark.parametrize("D", [4, 8, 16, 32, 64])
 def test_pfhr_tunings_vs_oracle(R, mpt, pu, minb, D):
     """R2C-pair kernel (real input): every tuning vs the oracle step, grids with every quad type

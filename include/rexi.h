@@ -196,8 +196,8 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int p
  *  REXI_SCHEDULE_AUTO:    CHUNKED (default). With octet items every block costs the same, so
  *                         the chunked waves are already balanced, and two 128-thread blocks per
  *                         SM issue better than one 256-thread block: measured on B200 the
- *                         chunked pole kernel is 2-4 % faster (C2 1.695 vs 1.735 ms, C4 830 vs
- *                         863 ms).
+ *                         chunked pole kernel is 2-7 % faster (default kernel: C2 0.990 vs
+ *                         1.058 ms, C4 485 vs 522 ms).
  * STREAMK falls back to CHUNKED when the segment partials do not fit the partial buffer. The
  * kernels of every other variant are always chunked. Schedules differ only in the summation order of the pole sum. Clears the
  * plan's graph cache. EINVAL for an unknown schedule. */

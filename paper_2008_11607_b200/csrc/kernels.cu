@@ -645,14 +645,14 @@ __host__ __device__ __forceinline__ long sk_cta_of(long x, long W, long P) {
 }
 
 // One tile of poles for the thread's four pairs. SHARED: both quads have the same K2 (octet).
-// Pole sums of the delta0 weights, kept as sigma = conj(S1) - S2 with S1 = sum W1 q and
-// S2 = sum conj(W2) q (and tau' = conj(T1) - T2 with P1, P2): two complex MACs per pole each.
+// Pole sums of the delta0 weights sigma = sum conj(W1 q) - conj(W2) q and tau' (P1, P2), as
+// four real FMAs per pole each from the planner's real coefficients (planner.h).
 struct DSums {
-    cd s1, s2, t1, t2;
-    __device__ __forceinline__ cd sigma() const { return mk(s1.x - s2.x, -s1.y - s2.y); }
-    __device__ __forceinline__ cd tau() const { return mk(t1.x - t2.x, -t1.y - t2.y); }
+    cd sg, ta;
+    __device__ __forceinline__ cd sigma() const { return sg; }
+    __device__ __forceinline__ cd tau() const { return ta; }
 };
-__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0), mk(0, 0), mk(0, 0)}; }
+__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0)}; }
 
 template <int PU, int NQ, bool SHARED>
 __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const double (&K2)[NQ],
@@ -669,10 +669,8 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
 #pragma unroll
         for (int g = 0; g < NG; ++g) {
             const cd q = pole_den(P, K2[g]);
-            ds[g].s1 = cfma(mk(P.W1r, P.W1i), q, ds[g].s1);
-            ds[g].s2 = cjfma(mk(P.W2r, P.W2i), q, ds[g].s2);
-            ds[g].t1 = cfma(mk(P.P1r, P.P1i), q, ds[g].t1);
-            ds[g].t2 = cjfma(mk(P.P2r, P.P2i), q, ds[g].t2);
+            ds[g].sg = mk(fma(P.sgx1, q.x, fma(P.sgx2, q.y, ds[g].sg.x)), fma(P.sgy1, q.x, fma(P.sgy2, q.y, ds[g].sg.y)));
+            ds[g].ta = mk(fma(P.tax1, q.x, fma(P.tax2, q.y, ds[g].ta.x)), fma(P.tay1, q.x, fma(P.tay2, q.y, ds[g].ta.y)));
             Aq[g] = cmul(X1, q);
             Cq[g] = cmul(Y1, q);
         }

@@ -237,6 +237,10 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             q.Y1r = (double)Y1.real();  q.Y1i = (double)Y1.imag();
             q.sr2 = 2.0 * q.s2r;        q.si2 = 2.0 * q.s2i;        // exact (power-of-two scaling)
             q.hn2 = 2.0 * q.ai;         q.pad0 = 0.0;
+            q.sgx1 = (double)(W1.real() - W2.real());   q.sgx2 = (double)(-(W1.imag() + W2.imag()));
+            q.sgy1 = (double)(W2.imag() - W1.imag());   q.sgy2 = (double)(-(W1.real() + W2.real()));
+            q.tax1 = (double)(P1.real() - P2.real());   q.tax2 = (double)(-(P1.imag() + P2.imag()));
+            q.tay1 = (double)(P2.imag() - P1.imag());   q.tay2 = (double)(-(P1.real() + P2.real()));
         }
         q.ia2 = (double)std::norm(ia);
     }

@@ -18,7 +18,7 @@ struct GaussTable {
 };
 GaussTable appendix_a_table();
 
-// Per-pole constants of the pole kernel (device layout, 36 doubles = 288 B).
+// Per-pole constants of the pole kernel (device layout, 44 doubles = 352 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
 // the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
 struct alignas(16) PoleConst {
@@ -41,8 +41,13 @@ struct alignas(16) PoleConst {
     double sr2, si2;    //            2 Re(c/alpha), 2 Im(c/alpha)
     double Y1r, Y1i;    //            (P1 + conj P2)/2 (partner: its conjugate)
     double hn2, pad0;   //            2 h n = 2 Im(alpha)
+    // R2C delta0 weights as real coefficients of q = qr + i qi (W1 = a + ib, W2 = c + id):
+    // sigma = conj(W1) conj(q) - conj(W2) q = [(a-c) qr - (b+d) qi] + i [(d-b) qr - (a+c) qi];
+    // tau' likewise with P1, P2
+    double sgx1, sgx2, sgy1, sgy2;
+    double tax1, tax2, tay1, tay2;
 };
-static_assert(sizeof(PoleConst) == 288, "PoleConst layout");
+static_assert(sizeof(PoleConst) == 352, "PoleConst layout");
 
 struct Plan {
     GaussTable table;

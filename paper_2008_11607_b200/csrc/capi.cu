@@ -92,6 +92,7 @@ struct rexi_plan_s {
     int max_chunks = 1;
     // device buffers
     rexi::PoleConst *d_poles = nullptr;
+    rexi::R2CPole *d_rpoles = nullptr;
     double *d_ksym = nullptr;
     cd *d_tw = nullptr;
     cd *d_fhat = nullptr;   // [3][n_modes]
@@ -153,7 +154,7 @@ struct rexi_plan_s {
         if (ev_join) cudaEventDestroy(ev_join);
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
-        for (void *p : {(void *)d_poles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
+        for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
                         (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -286,6 +287,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.fhat = fhat;
     a.partial = p->d_partial;
     a.poles = p->d_poles;
+    a.rpoles = p->d_rpoles;
     a.ksym = p->d_ksym;
     a.pole_begin = b;
     a.pole_end = e;
@@ -593,6 +595,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     p->max_chunks = (int)std::max<size_t>(1, std::min<size_t>(64, budget / field));
     auto alloc = [&](void **ptr, size_t bytes) -> cudaError_t { return cudaMalloc(ptr, bytes); };
     if ((e = alloc((void **)&p->d_poles, sizeof(rexi::PoleConst) * (size_t)p->host.n_poles)) ||
+        (e = alloc((void **)&p->d_rpoles, sizeof(rexi::R2CPole) * (size_t)p->host.n_poles)) ||
         (e = alloc((void **)&p->d_ksym, sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_tw, 2 * sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
@@ -603,6 +606,8 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
                                                            : cuda_fail(e, "cudaMalloc"));
     }
     if ((e = cudaMemcpy(p->d_poles, p->host.poles.data(), sizeof(rexi::PoleConst) * (size_t)p->host.n_poles,
+                        cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(p->d_rpoles, p->host.r2c.data(), sizeof(rexi::R2CPole) * (size_t)p->host.n_poles,
                         cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_ksym, p->host.ksym.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), 2 * sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
@@ -663,6 +668,8 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t p, int method) {
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_rpoles, np.r2c.data(), sizeof(rexi::R2CPole) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
         p->host = std::move(np);
         p->method = method;
         return REXI_OK;
@@ -687,15 +694,22 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t p, int L, double mu, const double 
         p->clear_graphs();
         if (np.n_poles != h.n_poles) {
             rexi::PoleConst *d = nullptr;
+            rexi::R2CPole *dr = nullptr;
             cudaError_t e = cudaMalloc((void **)&d, sizeof(rexi::PoleConst) * (size_t)np.n_poles);
+            if (e == cudaSuccess) e = cudaMalloc((void **)&dr, sizeof(rexi::R2CPole) * (size_t)np.n_poles);
             if (e != cudaSuccess) {
                 cudaGetLastError();
+                if (d) cudaFree(d);
                 return fail(REXI_ENOMEM, "cudaMalloc (pole table) failed");
             }
             cudaFree(p->d_poles);
+            cudaFree(p->d_rpoles);
             p->d_poles = d;
+            p->d_rpoles = dr;
         }
         CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_rpoles, np.r2c.data(), sizeof(rexi::R2CPole) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         p->host = std::move(np);
         return REXI_OK;

@@ -415,7 +415,8 @@ __device__ __forceinline__ void pole_solves_in(const PoleConst &P, ModeState &s,
                                                const double c);
 
 // 1/(kappa_n + K2) for one pole and one value of K2 (shared by every mode with that K2).
-__device__ __forceinline__ cd pole_den(const PoleConst &P, const double K2) {
+template <class PC>
+__device__ __forceinline__ cd pole_den(const PC &P, const double K2) {
     const double dr = P.kr + K2;
     const double r = rcp_pos(fma(dr, dr, P.ki2));
     return mk(dr * r, -P.ki * r);
@@ -655,12 +656,12 @@ struct DSums {
 __device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0)}; }
 
 template <int PU, int NQ, bool SHARED>
-__device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const double (&K2)[NQ],
+__device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const double (&K2)[NQ],
                                          PairState (&st)[2 * NQ], DSums (&ds)[NQ]) {
     constexpr int NG = SHARED ? 1 : NQ;
 #pragma unroll PU
     for (int qq = 0; qq < cnt; ++qq) {
-        const PoleConst &P = sp[qq];
+        const R2CPole &P = sp[qq];
         const cd X1 = mk(P.X1r, P.X1i), Y1 = mk(P.Y1r, P.Y1i);
         // the solve's division by the Helmholtz symbol, eta1 = q num1 and eta_t = conj(q) num_t,
         // fused with the accumulation weights: X1 eta1 = (X1 q) num1, X2 eta_t = conj(X1 q) num_t
@@ -697,7 +698,7 @@ __device__ __forceinline__ void r2c_tile(const PoleConst *sp, int cnt, const dou
 
 template <int PU, int MINB, int NQ, bool OCT>
 __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
-    __shared__ PoleConst sp[kR2CTile];
+    __shared__ R2CPole sp[kR2CTile];
     const long n_modes = a.n_modes;
     const int chunk = blockIdx.y;
     const long len = a.pole_end - a.pole_begin;
@@ -756,9 +757,9 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
         const int cnt = (int)min((long)kR2CTile, p1 - pt);
         __syncthreads();
         {
-            const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
+            const double2 *src = reinterpret_cast<const double2 *>(a.rpoles + pt);
             double2 *dst = reinterpret_cast<double2 *>(sp);
-            constexpr int kPer = (int)(sizeof(PoleConst) / sizeof(double2));
+            constexpr int kPer = (int)(sizeof(R2CPole) / sizeof(double2));
             for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
         }
         __syncthreads();
@@ -800,7 +801,7 @@ constexpr int kSkBlock = 256;
 
 template <int PU>
 __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
-    __shared__ PoleConst sp[kR2CTile];
+    __shared__ R2CPole sp[kR2CTile];
     const long n_modes = a.n_modes;
     const long Nr = a.pole_end - a.pole_begin;
     const long T = a.sk_tiles, P = gridDim.x;
@@ -834,9 +835,9 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
             const int cnt = (int)min((long)kR2CTile, a.pole_begin + phi - pt);
             __syncthreads();
             {
-                const double2 *src = reinterpret_cast<const double2 *>(a.poles + pt);
+                const double2 *src = reinterpret_cast<const double2 *>(a.rpoles + pt);
                 double2 *dst = reinterpret_cast<double2 *>(sp);
-                constexpr int kPer = (int)(sizeof(PoleConst) / sizeof(double2));
+                constexpr int kPer = (int)(sizeof(R2CPole) / sizeof(double2));
                 for (int i = threadIdx.x; i < cnt * kPer; i += kSkBlock) dst[i] = src[i];
             }
             __syncthreads();

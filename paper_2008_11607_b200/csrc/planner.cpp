@@ -154,6 +154,7 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     p.C2.assign(2 * (size_t)p.n_poles, 0.0);
     p.gamma.assign((size_t)p.n_poles, 0.0);
     p.poles.assign((size_t)p.n_poles, PoleConst{});
+    p.r2c.assign((size_t)p.n_poles, R2CPole{});
     p.spre_re.assign((size_t)p.n_poles + 1, 0.0L);
     p.spre_im.assign((size_t)p.n_poles + 1, 0.0L);
     p.wpre_re.assign((size_t)p.n_poles + 1, 0.0L);
@@ -233,14 +234,16 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             // conjugates of these, which the kernel uses directly
             const cld X1 = (W1 + std::conj(W2)) * 0.5L;
             const cld Y1 = (P1 + std::conj(P2)) * 0.5L;
-            q.X1r = (double)X1.real();  q.X1i = (double)X1.imag();
-            q.Y1r = (double)Y1.real();  q.Y1i = (double)Y1.imag();
-            q.sr2 = 2.0 * q.s2r;        q.si2 = 2.0 * q.s2i;        // exact (power-of-two scaling)
-            q.hn2 = 2.0 * q.ai;         q.pad0 = 0.0;
-            q.sgx1 = (double)(W1.real() - W2.real());   q.sgx2 = (double)(-(W1.imag() + W2.imag()));
-            q.sgy1 = (double)(W2.imag() - W1.imag());   q.sgy2 = (double)(-(W1.real() + W2.real()));
-            q.tax1 = (double)(P1.real() - P2.real());   q.tax2 = (double)(-(P1.imag() + P2.imag()));
-            q.tay1 = (double)(P2.imag() - P1.imag());   q.tay2 = (double)(-(P1.real() + P2.real()));
+            R2CPole &rq = p.r2c[(size_t)n];
+            rq.kr = q.kr;                 rq.ki = q.ki;
+            rq.ki2 = q.ki2;               rq.hn2 = 2.0 * q.ai;        // exact (power-of-two scaling)
+            rq.X1r = (double)X1.real();  rq.X1i = (double)X1.imag();
+            rq.Y1r = (double)Y1.real();  rq.Y1i = (double)Y1.imag();
+            rq.sr2 = 2.0 * q.s2r;        rq.si2 = 2.0 * q.s2i;
+            rq.sgx1 = (double)(W1.real() - W2.real());   rq.sgx2 = (double)(-(W1.imag() + W2.imag()));
+            rq.sgy1 = (double)(W2.imag() - W1.imag());   rq.sgy2 = (double)(-(W1.real() + W2.real()));
+            rq.tax1 = (double)(P1.real() - P2.real());   rq.tax2 = (double)(-(P1.imag() + P2.imag()));
+            rq.tay1 = (double)(P2.imag() - P1.imag());   rq.tay2 = (double)(-(P1.real() + P2.real()));
         }
         q.ia2 = (double)std::norm(ia);
     }

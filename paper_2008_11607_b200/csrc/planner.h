@@ -18,7 +18,7 @@ struct GaussTable {
 };
 GaussTable appendix_a_table();
 
-// Per-pole constants of the pole kernel (device layout, 44 doubles = 352 B).
+// Per-pole constants of the pole kernels (device layout, 28 doubles = 224 B).
 // c = tau (tau-scaled Coriolis, reading G3); kappa = alpha^2 + c^2 (PAPER.md:476 with
 // the tau scaling); w1 = Gamma C2, w2 = Gamma (C1 - C2 conj(alpha)) (reading G4).
 struct alignas(16) PoleConst {
@@ -37,17 +37,25 @@ struct alignas(16) PoleConst {
     double W2r, W2i;    //                                       w2 / (2 h mu)
     double P1r, P1i;    // PFH: W1 alpha          (delta1 = alpha eta1 - e0 folded into the weights)
     double P2r, P2i;    // PFH: -W2 conj(alpha)   (delta_t = e0 - conj(alpha) eta_t)
-    double X1r, X1i;    // R2C pairs: (W1 + conj W2)/2 (the partner weight (W2 + conj W1)/2 is its conjugate)
-    double sr2, si2;    //            2 Re(c/alpha), 2 Im(c/alpha)
-    double Y1r, Y1i;    //            (P1 + conj P2)/2 (partner: its conjugate)
-    double hn2, pad0;   //            2 h n = 2 Im(alpha)
-    // R2C delta0 weights as real coefficients of q = qr + i qi (W1 = a + ib, W2 = c + id):
-    // sigma = conj(W1) conj(q) - conj(W2) q = [(a-c) qr - (b+d) qi] + i [(d-b) qr - (a+c) qi];
-    // tau' likewise with P1, P2
+};
+static_assert(sizeof(PoleConst) == 224, "PoleConst layout");
+
+// The constants the R2C pole kernel reads per pole, packed for nine 16-byte shared-memory loads
+// (DESIGN.md 6.1): kappa; 2 h n; the R2C half-weights X1 = (W1 + conj W2)/2,
+// Y1 = (P1 + conj P2)/2 (their partners are the conjugates); 2 Re(c/alpha), 2 Im(c/alpha); the
+// delta0 weights as real coefficients of q = qr + i qi (W1 = a + ib, W2 = c + id):
+// sigma = conj(W1) conj(q) - conj(W2) q = [(a-c) qr - (b+d) qi] + i [(d-b) qr - (a+c) qi],
+// tau' likewise with P1, P2.
+struct alignas(16) R2CPole {
+    double kr, ki;
+    double ki2, hn2;
+    double X1r, X1i;
+    double Y1r, Y1i;
+    double sr2, si2;
     double sgx1, sgx2, sgy1, sgy2;
     double tax1, tax2, tay1, tay2;
 };
-static_assert(sizeof(PoleConst) == 352, "PoleConst layout");
+static_assert(sizeof(R2CPole) == 144, "R2CPole layout");
 
 struct Plan {
     GaussTable table;
@@ -59,6 +67,7 @@ struct Plan {
     // term table, n = 0..N (interleaved re/im for complex entries)
     std::vector<double> alpha, C1, C2, gamma;   // REXI plans: C1 = beta^Re_n, C2 = 0
     std::vector<PoleConst> poles;
+    std::vector<R2CPole> r2c;        // the same poles for the R2C kernel
     // prefix sums (extended precision) of w1_n / alpha_n + w2_n / |alpha_n|^2, n = 0..N:
     // S(b, e) = pre[e] - pre[b] rebuilds the zeta pole sum from the eta pole sum (finish_kernel)
     std::vector<long double> spre_re, spre_im;

@@ -554,10 +554,14 @@ __device__ __forceinline__ void quad_modes(long q, int D, int log2D, long m[4]) 
 // is accumulated directly per pole:
 //   H_eta   += X1 eta1 + X2 eta_t + (conj(W1 q) - conj(W2) q) d0
 //   H_delta' += Y1 eta1 + Y2 eta_t + (conj(P1 q) - conj(P2) q) d0
-// (the d0 coefficients are summed per quad and applied once, after the pole loop)
-// (X, Y: half-weights from the planner). A thread owns one or two K2 quads (two or four pairs,
-// see r2c work items below); the corner quad (four self-mirror K = 0 modes) is left to
-// fixup_k0_kernel.
+// (X, Y: half-weights from the planner; X2 = conj X1, Y2 = conj Y1). With eta1 = q num1 and
+// eta_t = conj(q) num_t (the two Helmholtz solves, num = their right-hand sides) this is
+//   H_eta += Re(X1 q) (num1 + num_t) + i Im(X1 q) (num1 - num_t) + sigma d0,
+//   num1 + num_t = 2 h mu eta0 - 2 Re(c/alpha) m0,  num1 - num_t = 2 d0 + i (2 h n eta0 - 2 Im(c/alpha) m0),
+// which r2c_tile evaluates for every pole and pair; the d0 coefficients
+// sigma, tau' depend on the pole and K2 only and are summed per K2 value, applied after the
+// pole loop. A thread owns one quad (mpt 4) or one octet item (mpt 8, two quads sharing K2);
+// the corner quad (four self-mirror K = 0 modes) is left to fixup_k0_kernel.
 struct PairState {
     cd e0, E2, D2, m0;       // data of the representative mode: eta0, 2 h mu eta0, 2 delta0, m0
     cd H0, H1;               // Hermitian accumulators: eta, delta' (before the e0 term)

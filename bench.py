@@ -375,6 +375,12 @@ def main():
                          "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
                          "traffic": traffic, "kernel": "pole_kernel",
                          "flops_per_pole_mode": info["flops_per_pole_mode"],
+                         # SURVEY.md 8(d)'s per-unit figure is the paper's route (~200 flops per
+                         # pole-gridpoint); the kernel's exact rearrangements execute fewer, so the
+                         # roofline uses the kernel's own count and this is reported beside it
+                         "paper_route_flops_per_pole_mode": 200.0,
+                         "paper_route_equiv_tflops": (200.0 * rank_units / pole_avg_s / 1e12
+                                                      if pole_avg_s > 0 else None),
                          "fp64_pipe_frac": pipe_frac,
                          "kernel_ms_avg": pole_avg_s * 1e3,
                          "kernel_share_of_step": (pole_ms / ms_local) if ms_local > 0 else None,

@@ -652,12 +652,16 @@ __host__ __device__ __forceinline__ long sk_cta_of(long x, long W, long P) {
 // One tile of poles for the thread's four pairs. SHARED: both quads have the same K2 (octet).
 // Pole sums of the delta0 weights sigma = sum conj(W1 q) - conj(W2) q and tau' (P1, P2), as
 // four real FMAs per pole each from the planner's real coefficients (planner.h).
+// The sum/difference evaluation below also sends the delta0 part of (num1 - num_t) = 2 delta0 +
+// i w to these sums: i Im(X1 q) 2 delta0 is a delta0 term with a pole-and-K2 coefficient, so
+// sigma gains 2 i sum Im(X1 q) (bA) and tau' 2 i sum Im(Y1 q) (bC).
 struct DSums {
     cd sg, ta;
-    __device__ __forceinline__ cd sigma() const { return sg; }
-    __device__ __forceinline__ cd tau() const { return ta; }
+    double bA, bC;
+    __device__ __forceinline__ cd sigma() const { return mk(sg.x, sg.y + 2.0 * bA); }
+    __device__ __forceinline__ cd tau() const { return mk(ta.x, ta.y + 2.0 * bC); }
 };
-__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0)}; }
+__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0), 0.0, 0.0}; }
 
 template <int PU, int NQ, bool SHARED>
 __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const double (&K2)[NQ],
@@ -678,6 +682,8 @@ __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const doubl
             ds[g].ta = mk(fma(P.tax1, q.x, fma(P.tax2, q.y, ds[g].ta.x)), fma(P.tay1, q.x, fma(P.tay2, q.y, ds[g].ta.y)));
             Aq[g] = cmul(X1, q);
             Cq[g] = cmul(Y1, q);
+            ds[g].bA += Aq[g].y;
+            ds[g].bC += Cq[g].y;
         }
         // The two Helmholtz right-hand sides of the pair, num1 = B0 + i hn eta0 - (c/alpha) m0
         // and num_t = Bt0 - i hn eta0 - conj(c/alpha) m0 (B0, Bt0 = h mu eta0 +- delta0), carry
@@ -693,9 +699,10 @@ __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const doubl
             PairState &s = st[j];
             const cd S = mk(fma(-r2, s.m0.x, s.E2.x), fma(-r2, s.m0.y, s.E2.y));       // num1 + num_t
             const cd w = mk(fma(-k2, s.m0.x, g2 * s.e0.x), fma(-k2, s.m0.y, g2 * s.e0.y));
-            const cd Dd = mk(s.D2.x - w.y, s.D2.y + w.x);                               // num1 - num_t
-            s.H0 = mk(fma(Aq[g].x, S.x, fma(-Aq[g].y, Dd.y, s.H0.x)), fma(Aq[g].x, S.y, fma(Aq[g].y, Dd.x, s.H0.y)));
-            s.H1 = mk(fma(Cq[g].x, S.x, fma(-Cq[g].y, Dd.y, s.H1.x)), fma(Cq[g].x, S.y, fma(Cq[g].y, Dd.x, s.H1.y)));
+            // num1 - num_t = 2 delta0 + i w: i Im(A) (2 delta0 + i w) = i Im(A) 2 delta0 - Im(A) w,
+            // the delta0 part going to the sums (DSums)
+            s.H0 = mk(fma(Aq[g].x, S.x, fma(-Aq[g].y, w.x, s.H0.x)), fma(Aq[g].x, S.y, fma(-Aq[g].y, w.y, s.H0.y)));
+            s.H1 = mk(fma(Cq[g].x, S.x, fma(-Cq[g].y, w.x, s.H1.x)), fma(Cq[g].x, S.y, fma(-Cq[g].y, w.y, s.H1.y)));
         }
     }
 }

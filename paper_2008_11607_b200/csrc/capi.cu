@@ -99,7 +99,6 @@ struct rexi_plan_s {
     cd *d_acc = nullptr;    // [3][n_modes]
     cd *d_tmp = nullptr;    // [3][n_modes]
     cd *d_partial = nullptr;  // [max_chunks][3][n_modes]
-    int *d_tile_cnt = nullptr;  // [R2C tiles] arrival counters of the fused finish (kept at zero)
     double *d_stage = nullptr;  // [6][n_modes] (rexi_apply_host)
     double *d_stage2 = nullptr;  // [6][n_modes] second set (rexi_apply_host_batch)
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -156,8 +155,7 @@ struct rexi_plan_s {
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
-                        (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2,
-                        (void *)d_tile_cnt})
+                        (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -302,18 +300,6 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     a.sk_tiles = sk_tiles;
     a.sk_slots = sk_slots;
-    // chunked R2C octet kernel: the last block of each tile finishes it (no finish pass)
-    a.fused_finish = (kd == 6 && !sk_tiles && p->mpt[6] == 8) ? 1 : 0;
-    a.tile_cnt = p->d_tile_cnt;
-    a.acc = acc;
-    {
-        const long double sr = p->host.spre_re[(size_t)e] - p->host.spre_re[(size_t)b];
-        const long double si = p->host.spre_im[(size_t)e] - p->host.spre_im[(size_t)b];
-        a.S = cd{(double)sr, (double)si};
-        const long double wr = p->host.wpre_re[(size_t)e] - p->host.wpre_re[(size_t)b];
-        const long double wi = p->host.wpre_im[(size_t)e] - p->host.wpre_im[(size_t)b];
-        a.Sd = cd{(double)wr, (double)wi};
-    }
     rexi_status_t s;
     const bool fork = (kd == 6);
     if (fork) {
@@ -375,8 +361,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     f.sk_ctas = sk_ctas;
     f.sk_poles = e - b;
     if (sk_tiles) CK(rexi::launch_finish_r2c_sk(f, st));
-    else if (!a.fused_finish) CK(rexi::launch_finish(f, st));
-    p->launches += a.fused_finish ? 1 : 2;
+    else CK(rexi::launch_finish(f, st));
+    p->launches += 2;
     if (fork) {
         CK(cudaStreamWaitEvent(st, p->ev_join, 0));
     } else if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
@@ -614,8 +600,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
         (e = alloc((void **)&p->d_tw, 2 * sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
         (e = alloc((void **)&p->d_tmp, field)) ||
-        (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks)) ||
-        (e = alloc((void **)&p->d_tile_cnt, sizeof(int) * (size_t)rexi::pole_r2c_blocks(D, 4)))) {
+        (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks))) {
         cudaGetLastError();
         return cleanup_fail(e == cudaErrorMemoryAllocation ? fail(REXI_ENOMEM, "cudaMalloc failed")
                                                            : cuda_fail(e, "cudaMalloc"));
@@ -625,8 +610,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
         (e = cudaMemcpy(p->d_rpoles, p->host.r2c.data(), sizeof(rexi::R2CPole) * (size_t)p->host.n_poles,
                         cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_ksym, p->host.ksym.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), 2 * sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemset(p->d_tile_cnt, 0, sizeof(int) * (size_t)rexi::pole_r2c_blocks(D, 4))))
+        (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), 2 * sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
         return cleanup_fail(cuda_fail(e, "cudaMemcpy"));
     *out = p;
     return REXI_OK;

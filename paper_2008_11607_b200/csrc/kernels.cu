@@ -707,31 +707,6 @@ __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const doubl
     }
 }
 
-// Finish of one R2C pair from its summed Hermitian accumulators (h0 = H_eta, h1 = H_delta'):
-// H(delta) = h1 - Re(sum w1) eta0, H(zeta) = Re(S) m0 + c H(eta), then (u, v) from (delta, zeta)
-// (as finish_kernel); writes the representative r and, conjugated, its mirror -K.
-__device__ __forceinline__ void r2c_finish_pair(const cd *__restrict__ fhat, const double *__restrict__ ksym,
-                                                cd *acc, long n, int D, int log2D, double c, cd S, cd Sd,
-                                                long r, cd h0, cd h1) {
-    const int rl = (int)(r >> log2D), rk = (int)(r & (D - 1));
-    const long mm = ((long)((D - rl) & (D - 1)) << log2D) + ((D - rk) & (D - 1));
-    const double kx = ksym[rk], ky = ksym[rl];
-    const cd e = fhat[r], uu = fhat[n + r], vv = fhat[2 * n + r];
-    h1 = mk(fma(-Sd.x, e.x, h1.x), fma(-Sd.x, e.y, h1.y));
-    const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
-    const cd h2 = mk(fma(S.x, m0.x, c * h0.x), fma(S.x, m0.y, c * h0.y));
-    const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0 off the corners
-    const cd tt = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
-    const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
-    const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
-    acc[r] = h0;
-    acc[n + r] = U;
-    acc[2 * n + r] = V;
-    acc[mm] = mk(h0.x, -h0.y);      // the Hermitian spectrum at -K is the conjugate
-    acc[n + mm] = mk(U.x, -U.y);
-    acc[2 * n + mm] = mk(V.x, -V.y);
-}
-
 template <int PU, int MINB, int NQ, bool OCT>
 __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) {
     __shared__ R2CPole sp[kR2CTile];
@@ -819,42 +794,6 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2c(PoleArgs a) 
                 const cd d0 = mk(0.5 * s.D2.x, 0.5 * s.D2.y);
                 out[rep[2 * g + j]] = cfma(ds[g].sigma(), d0, s.H0);
                 out[n_modes + rep[2 * g + j]] = cfma(ds[g].tau(), d0, s.H1);
-            }
-        }
-    }
-    if (a.fused_finish) {
-        // The last of a tile's n_chunks blocks to finish sums the tile's chunk partials in chunk
-        // order (deterministic) and finishes its pairs, replacing a separate finish pass. The
-        // counter resets itself for the next launch.
-        __shared__ int last_block;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int prev = atomicAdd(a.tile_cnt + blockIdx.x, 1);
-            last_block = prev == a.n_chunks - 1;
-            if (last_block) a.tile_cnt[blockIdx.x] = 0;
-        }
-        __syncthreads();
-        if (last_block) {
-            __threadfence();
-#pragma unroll
-            for (int g = 0; g < NQ; ++g) {
-                if (!ok[g]) continue;
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const long r = rep[2 * g + j];
-                    cd h0 = mk(0, 0), h1 = mk(0, 0);
-                    for (int cc = 0; cc < a.n_chunks; ++cc) {
-                        const cd *p = a.partial + (size_t)cc * 3 * n_modes;
-                        // L2 loads (ld.global.cg): other SMs wrote them during this launch
-                        const double2 y0 = __ldcg(reinterpret_cast<const double2 *>(p + r));
-                        const double2 y1 = __ldcg(reinterpret_cast<const double2 *>(p + n_modes + r));
-                        const cd x0 = mk(y0.x, y0.y), x1 = mk(y1.x, y1.y);
-                        h0 = mk(h0.x + x0.x, h0.y + x0.y);
-                        h1 = mk(h1.x + x1.x, h1.y + x1.y);
-                    }
-                    r2c_finish_pair(a.fhat, a.ksym, a.acc, n_modes, a.D, a.log2D, c, a.S, a.Sd, r, h0, h1);
-                }
             }
         }
     }
@@ -1140,6 +1079,8 @@ __global__ void __launch_bounds__(256) finish_r2c_sk_kernel(FinishArgs a) {
     if (!ok[pair >> 1]) return;
     const long n = a.n_modes;
     const long r = r2c_rep(quad[pair >> 1], pair & 1, a.D, a.log2D);
+    const int rl = (int)(r >> a.log2D), rk = (int)(r & (a.D - 1));
+    const long mm = ((long)((a.D - rl) & (a.D - 1)) << a.log2D) + ((a.D - rk) & (a.D - 1));
     const long Nr = a.sk_poles, P = a.sk_ctas, W = a.sk_tiles * Nr;
     const long i0 = sk_cta_of(t * Nr, W, P), i1 = sk_cta_of((t + 1) * Nr - 1, W, P);
     cd h0 = mk(0, 0), h1 = mk(0, 0);
@@ -1149,7 +1090,23 @@ __global__ void __launch_bounds__(256) finish_r2c_sk_kernel(FinishArgs a) {
         h0 = mk(h0.x + x0.x, h0.y + x0.y);
         h1 = mk(h1.x + x1.x, h1.y + x1.y);
     }
-    r2c_finish_pair(a.fhat, a.ksym, a.acc, n, a.D, a.log2D, a.tau, a.S, a.Sd, r, h0, h1);
+    const double kx = a.ksym[rk], ky = a.ksym[rl];
+    const cd e = a.fhat[r], uu = a.fhat[n + r], vv = a.fhat[2 * n + r];
+    const double c = a.tau;
+    // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
+    h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
+    const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
+    const cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
+    const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0 off the corners
+    const cd tt = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
+    const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
+    const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
+    a.acc[r] = h0;
+    a.acc[n + r] = U;
+    a.acc[2 * n + r] = V;
+    a.acc[mm] = mk(h0.x, -h0.y);      // the Hermitian spectrum at -K is the conjugate
+    a.acc[n + mm] = mk(U.x, -U.y);
+    a.acc[2 * n + mm] = mk(V.x, -V.y);
 }
 
 // ============================================================================= K = 0 modes (DZ)

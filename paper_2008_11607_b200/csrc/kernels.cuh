@@ -72,11 +72,6 @@ struct PoleArgs {
     double hmu;            // Re(alpha_n) = h mu (same for every pole)
     long sk_tiles;         // R2C stream-K: tiles of 128 octet items (0: chunked launch)
     int sk_slots;          // R2C stream-K: partial slots per tile
-    // chunked R2C, fused finish: the last block of each tile finishes it (no finish pass)
-    int fused_finish;
-    int *tile_cnt;         // [tiles] arrival counters, zero between launches
-    cd *acc;               // finished output [3][D*D]
-    cd S, Sd;              // as FinishArgs
 };
 
 struct FinishArgs {

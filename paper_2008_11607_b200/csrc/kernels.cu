@@ -653,15 +653,14 @@ __host__ __device__ __forceinline__ long sk_cta_of(long x, long W, long P) {
 // Pole sums of the delta0 weights sigma = sum conj(W1 q) - conj(W2) q and tau' (P1, P2), as
 // four real FMAs per pole each from the planner's real coefficients (planner.h).
 // The sum/difference evaluation below also sends the delta0 part of (num1 - num_t) = 2 delta0 +
-// i w to these sums: i Im(X1 q) 2 delta0 is a delta0 term with a pole-and-K2 coefficient, so
-// sigma gains 2 i sum Im(X1 q) (bA) and tau' 2 i sum Im(Y1 q) (bC).
+// i w to these sums: i Im(X1 q) 2 delta0 is a delta0 term with a pole-and-K2 coefficient; the
+// planner folds its 2 Im(X1 q) (and 2 Im(Y1 q) for tau') into the coefficients (planner.h).
 struct DSums {
     cd sg, ta;
-    double bA, bC;
-    __device__ __forceinline__ cd sigma() const { return mk(sg.x, sg.y + 2.0 * bA); }
-    __device__ __forceinline__ cd tau() const { return mk(ta.x, ta.y + 2.0 * bC); }
+    __device__ __forceinline__ cd sigma() const { return sg; }
+    __device__ __forceinline__ cd tau() const { return ta; }
 };
-__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0), 0.0, 0.0}; }
+__device__ __forceinline__ DSums dsums_zero() { return DSums{mk(0, 0), mk(0, 0)}; }
 
 template <int PU, int NQ, bool SHARED>
 __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const double (&K2)[NQ],
@@ -682,8 +681,6 @@ __device__ __forceinline__ void r2c_tile(const R2CPole *sp, int cnt, const doubl
             ds[g].ta = mk(fma(P.tax1, q.x, fma(P.tax2, q.y, ds[g].ta.x)), fma(P.tay1, q.x, fma(P.tay2, q.y, ds[g].ta.y)));
             Aq[g] = cmul(X1, q);
             Cq[g] = cmul(Y1, q);
-            ds[g].bA += Aq[g].y;
-            ds[g].bC += Cq[g].y;
         }
         // The two Helmholtz right-hand sides of the pair, num1 = B0 + i hn eta0 - (c/alpha) m0
         // and num_t = Bt0 - i hn eta0 - conj(c/alpha) m0 (B0, Bt0 = h mu eta0 +- delta0), carry

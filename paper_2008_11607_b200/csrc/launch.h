@@ -42,11 +42,11 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //                shared den 7/11, 4 MACs 16/32: 51 / 95
 //   kind 5 (PFH): PF without the two delta back-substitutions (4/8 each): 43 / 79
 //   kind 6 (R2C pairs, real input): per K2 value, den 7/11, the delta0 weight sums sigma, tau'
-//     (four real FMAs each from the planner's coefficients, plus the sums of Im(X1 q), Im(Y1 q))
-//     10/18 and the two fused weights X1 q, Y1 q 8/12; per pair (two modes) num1 + num_t 2/4,
-//     the non-delta0 part w of num1 - num_t 4/6 and 8 real-times-complex MACs 8/16 = 14/26.
-//     A quad (4 modes, own K2) = 53 / 93; an octet (8 modes, shared K2) = 81 / 145, i.e.
-//     13.25 / 23.25 resp. 10.125 / 18.125 per mode; modes_per_thread 8 uses octets for the
+//     (four real FMAs each from the planner's coefficients) 8/16 and the two fused weights
+//     X1 q, Y1 q 8/12; per pair (two modes) num1 + num_t 2/4, the non-delta0 part w of
+//     num1 - num_t 4/6 and 8 real-times-complex MACs 8/16 = 14/26.
+//     A quad (4 modes, own K2) = 51 / 91; an octet (8 modes, shared K2) = 79 / 143, i.e.
+//     12.75 / 22.75 resp. 9.875 / 17.875 per mode; modes_per_thread 8 uses octets for the
 //     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and half-discarded octets for the other
 //     3(H-1) quads.
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
@@ -60,12 +60,12 @@ inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
     return (n_oct + n_single) * octet / (8 * n_oct + 4 * n_single);
 }
 inline double pole_flops(int kind, int mpt, int D) {
-    if (kind == 6) return r2c_per_mode(mpt, D, 93.0, 145.0);
+    if (kind == 6) return r2c_per_mode(mpt, D, 91.0, 143.0);
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt, int D) {
-    if (kind == 6) return r2c_per_mode(mpt, D, 53.0, 81.0);
+    if (kind == 6) return r2c_per_mode(mpt, D, 51.0, 79.0);
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

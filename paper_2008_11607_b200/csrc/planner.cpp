@@ -240,10 +240,14 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             rq.X1r = (double)X1.real();  rq.X1i = (double)X1.imag();
             rq.Y1r = (double)Y1.real();  rq.Y1i = (double)Y1.imag();
             rq.sr2 = 2.0 * q.s2r;        rq.si2 = 2.0 * q.s2i;
+            // sigma also carries the delta0 part 2 i Im(X1 q) of the sum/difference evaluation
+            // (kernels.cu): 2 Im(X1 q) = 2 X1i qr + 2 X1r qi joins the imaginary coefficients
             rq.sgx1 = (double)(W1.real() - W2.real());   rq.sgx2 = (double)(-(W1.imag() + W2.imag()));
-            rq.sgy1 = (double)(W2.imag() - W1.imag());   rq.sgy2 = (double)(-(W1.real() + W2.real()));
+            rq.sgy1 = (double)(W2.imag() - W1.imag() + 2.0L * X1.imag());
+            rq.sgy2 = (double)(-(W1.real() + W2.real()) + 2.0L * X1.real());
             rq.tax1 = (double)(P1.real() - P2.real());   rq.tax2 = (double)(-(P1.imag() + P2.imag()));
-            rq.tay1 = (double)(P2.imag() - P1.imag());   rq.tay2 = (double)(-(P1.real() + P2.real()));
+            rq.tay1 = (double)(P2.imag() - P1.imag() + 2.0L * Y1.imag());
+            rq.tay2 = (double)(-(P1.real() + P2.real()) + 2.0L * Y1.real());
         }
         q.ia2 = (double)std::norm(ia);
     }

@@ -44,8 +44,10 @@ static_assert(sizeof(PoleConst) == 224, "PoleConst layout");
 // (DESIGN.md 6.1): kappa; 2 h n; the R2C half-weights X1 = (W1 + conj W2)/2,
 // Y1 = (P1 + conj P2)/2 (their partners are the conjugates); 2 Re(c/alpha), 2 Im(c/alpha); the
 // delta0 weights as real coefficients of q = qr + i qi (W1 = a + ib, W2 = c + id):
-// sigma = conj(W1) conj(q) - conj(W2) q = [(a-c) qr - (b+d) qi] + i [(d-b) qr - (a+c) qi],
-// tau' likewise with P1, P2.
+// sigma = conj(W1) conj(q) - conj(W2) q + 2 i Im(X1 q)
+//       = [(a-c) qr - (b+d) qi] + i [(d-b+2 Im X1) qr + (2 Re X1 - a - c) qi],
+// tau' likewise with P1, P2, Y1 (the 2 i Im(X1 q) term: the delta0 part of the kernel's
+// num1 - num_t, kernels.cu).
 struct alignas(16) R2CPole {
     double kr, ki;
     double ki2, hn2;

@@ -326,7 +326,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         x.D = p->host.D;
         CK(cudaEventRecord(p->ev_fork, st));
         CK(cudaStreamWaitEvent(p->aux_stream, p->ev_fork, 0));
-        CK(rexi::launch_fixup_k0(x, p->aux_stream));
+        CK(rexi::launch_fixup_k0(x, p->aux_stream, true));
         CK(cudaEventRecord(p->ev_join, p->aux_stream));
         p->launches += 1;
     }
@@ -377,7 +377,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         x.pole_end = e;
         x.n_modes = n;
         x.D = a.D;
-        CK(rexi::launch_fixup_k0(x, st));
+        CK(rexi::launch_fixup_k0(x, st, false));
         p->launches += 1;
     }
     return REXI_OK;

@@ -1110,7 +1110,10 @@ __global__ void __launch_bounds__(256) finish_r2c_sk_kernel(FinishArgs a) {
 // Modes with Kx = Ky = 0: (0,0), (0,D/2), (D/2,0), (D/2,D/2). There tau A only couples u, v
 // through Coriolis: (u1,v1) = kappa^-1 [[alpha,-c],[c,alpha]] (a,b) (eq:lswVelocities with
 // grad eta = 0) and (u2,v2) = conj(kappa)^-1 [[conj alpha, c],[-c, conj alpha]] (u1,v1).
-constexpr int kFixBlock = 1024;
+// BS = 1024 when the fix-up runs alone; 128 when it runs beside the pole kernel (R2C): a
+// 1024-thread block needs a whole SM's register file and would hold back that SM's pole blocks
+// for its duration, a 128-thread one fits next to two resident pole blocks.
+template <int kFixBlock>
 __global__ void __launch_bounds__(kFixBlock) fixup_k0_kernel(FixupArgs a) {
     __shared__ cd red[2][kFixBlock];
     const int D = a.D, H = D / 2;
@@ -1403,8 +1406,9 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st) {
-    fixup_k0_kernel<<<4, kFixBlock, 0, st>>>(a);
+cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel) {
+    if (beside_pole_kernel) fixup_k0_kernel<128><<<4, 128, 0, st>>>(a);
+    else fixup_k0_kernel<1024><<<4, 1024, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@ cudaError_t pole_r2c_sk_occupancy(int pu, int *blocks_per_sm);
 long pole_r2c_sk_tiles(int D);
 long sk_slots_bound(long tiles, long poles, long ctas);
 cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st);
-cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st);
+cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:

@@ -991,36 +991,32 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     if (a.kind == 6) {   // R2C pairs: Hermitian accumulators at the representative mode
         const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
         const long mm = ((long)((a.D - l) & (a.D - 1)) << a.log2D) + ((a.D - k) & (a.D - 1));
-        if (mm == m) return;                        // self-mirror K = 0 corner: fixup_k0_kernel
-        const long r = m < mm ? m : mm;             // representative of {K, -K}
+        if (mm <= m) return;   // self-mirror K = 0 corner (fixup_k0_kernel), or the mirror of a pair
+        // m is the representative of {K, -K} (the smaller linear index): finish both modes
         cd h0 = mk(0, 0), h1 = mk(0, 0);
         for (int c = 0; c < a.n_chunks; ++c) {
             const cd *p = a.partial + (size_t)c * 3 * n;
-            const cd x0 = p[r], x1 = p[n + r];
+            const cd x0 = p[m], x1 = p[n + m];
             h0 = mk(h0.x + x0.x, h0.y + x0.y);
             h1 = mk(h1.x + x1.x, h1.y + x1.y);
         }
-        const int rl = (int)(r >> a.log2D), rk = (int)(r & (a.D - 1));
-        const double kx = a.ksym[rk], ky = a.ksym[rl];
-        const cd e = a.fhat[r], uu = a.fhat[n + r], vv = a.fhat[2 * n + r];
+        const double kx = a.ksym[k], ky = a.ksym[l];
+        const cd e = a.fhat[m], uu = a.fhat[n + m], vv = a.fhat[2 * n + m];
         const double c = a.tau;
         // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
         h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
         const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
-        cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
-        const double K2 = fma(kx, kx, ky * ky);
-        const double inv = 1.0 / K2;   // K2 > 0: only the corners have K2 = 0
+        const cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
+        const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0: only the corners have K2 = 0
         const cd t = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
         const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
-        cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
-        if (r != m) {   // mirror mode: the Hermitian spectrum at -K is the conjugate
-            h0.y = -h0.y;
-            U.y = -U.y;
-            V.y = -V.y;
-        }
+        const cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
         a.acc[m] = h0;
         a.acc[n + m] = U;
         a.acc[2 * n + m] = V;
+        a.acc[mm] = mk(h0.x, -h0.y);   // the Hermitian spectrum at -K is the conjugate
+        a.acc[n + mm] = mk(U.x, -U.y);
+        a.acc[2 * n + mm] = mk(V.x, -V.y);
         return;
     }
     const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4 || a.kind == 5);

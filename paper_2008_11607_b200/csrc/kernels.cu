@@ -3,13 +3,17 @@
 //  * fft_{rows,cols}_{fwd,inv}_kernel : real 2-D FFT by batched radix-8 Stockham passes in
 //    shared memory (S1 forward transform, S5 inverse transform + Re). PAPER.md:497 "all computations
 //    ... in Fourier space"; Alg. 1 lines 1 and last.
-//  * pole_kernel<VARIANT>             : S2 + S3, the fused per-mode two-solve REXII pole
-//    loop with the weighted accumulation in registers (eq:lswEta,
-//    eq:lswVelocities). No per-pole solution ever reaches HBM.
-//  * finish_kernel                    : fixed-order sum of the per-chunk partial sums and,
-//    for the DZ variant, recovery of (u, v) from the accumulated (delta, zeta).
-//  * fixup_k0_kernel                  : the K = 0 modes for the DZ variant (velocities
-//    decouple from delta, zeta there): pure Coriolis 2x2 solves per pole.
+//  * pole_kernel_r2c (default)        : S2 + S3 for real fields on {K, -K} mode pairs grouped
+//    in K2 octets: both Helmholtz-reduced solves of every pole for every pair, fused with the
+//    weighted accumulation in registers (eq:lswEta); pole_kernel_r2c_sk is
+//    its opt-in stream-K schedule.
+//  * pole_kernel<VARIANT>             : the same for the other variants (UV, DZ, DZ3, PF, PFH)
+//    and for complex spectra (rexi_poles). No per-pole solution ever reaches HBM.
+//  * finish_kernel (+ finish_r2c_sk)  : fixed-order sum of the per-chunk partial sums, zeta
+//    rebuilt from the potential vorticity, (u, v) recovered from (delta, zeta).
+//  * fixup_k0_kernel                  : the K = 0 modes (velocities decouple from delta, zeta
+//    there): pure Coriolis 2x2 solves per pole.
+//  * hermitian_kernel                 : the spectral form of Re(.) between rexi_run steps.
 #include "kernels.cuh"
 #include "launch.h"
 

@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--variant", default="pfhr", choices=["pfhr", "pfh", "pf", "dz", "dz3", "uv"])
+    ap.add_argument("--variant", default="pfhx", choices=["pfhx", "pfhr", "pfh", "pf", "dz", "dz3", "uv"])
     ap.add_argument("--h", default="0.5", help="Gaussian spacing h, or 'auto' (NEXT-2 h_for_tol)")
     ap.add_argument("--tuning", default=None,
                     help="pole kernel tuning 'modes_per_thread,poles_per_iter,min_blocks' (default: plan's)")

@@ -79,22 +79,34 @@ typedef enum {
  *  REXI_VARIANT_PFH: PF with the delta back-substitution (delta = alpha eta - eta0, the first row
  *                    of each system) folded into the accumulation weights: per pole the two
  *                    Helmholtz solutions are formed; (delta, zeta, u, v) follow once per mode.
- *  REXI_VARIANT_PFHR: PFH on "R2C" mode pairs (allowed equivalent): the fields
+ *  REXI_VARIANT_PFHR: PFH on "R2C" mode pairs, COLLAPSED (comparison only, see below): the fields
  *                    are real, so the spectrum is Hermitian and the solves at -K follow from those
  *                    at K; the pair {K, -K} accumulates directly the Hermitian part that survives
  *                    Re(IDFT(.)). The two Helmholtz solves are formed for every pole and pair;
  *                    what depends on K2 only is shared: the denominator by the modes of a K2
  *                    quad or octet ((a, b) and (b, a) on the square grid), and the weight sum of
- *                    the delta0 term per K2 value. Default; used by rexi_apply /
- *                    apply_partial / apply_host / apply_host_batch / run; rexi_poles, whose input
- *                    need not be Hermitian, runs PFH. */
+ *                    the delta0 term per K2 value. This collapses the delta0
+ *                    pole sums and pre-multiplies the weights by 1/(kappa + K2): it is NOT the
+ *                    per-pole solve route of the contract (SURVEY.md 8(d) "out-of-contract
+ *                    shortcut"); kept as a labelled comparison only.
+ *  REXI_VARIANT_PFHX: explicit-solve R2C pairs (the DEFAULT): for every pole and every {K, -K}
+ *                    pair the two Helmholtz solutions eta1 = q num1 and eta_t = conj(q) num_t are
+ *                    formed from the pair's own right-hand sides (eq:lswEta, PAPER.md:486-497;
+ *                    procedure PAPER.md:427-435), the -K solves follow from them through the
+ *                    Hermitian data with the per-pole correction sigma_n delta0, and the weighted
+ *                    Hermitian part is accumulated in registers. Shared between
+ *                    the modes of an octet: only the reciprocal q = 1/(kappa_n + K2) and the
+ *                    per-pole coefficients sigma_n, tau'_n. Used by rexi_apply / apply_partial /
+ *                    apply_host / apply_host_batch / run; rexi_poles, whose input need not be
+ *                    Hermitian, runs PFH. */
 typedef enum {
     REXI_VARIANT_DZ = 0,
     REXI_VARIANT_UV = 1,
     REXI_VARIANT_DZ3 = 2,
     REXI_VARIANT_PF = 3,
     REXI_VARIANT_PFH = 4,
-    REXI_VARIANT_PFHR = 5
+    REXI_VARIANT_PFHR = 5,
+    REXI_VARIANT_PFHX = 6
 } rexi_variant_t;
 
 /* Which rational approximation the plan evaluates (both with the Appendix A coefficients):
@@ -105,7 +117,7 @@ typedef enum {
  *                     term, evaluated as the half-sum n = 0..N with Gamma_n (the Appendix A
  *                     table is conjugate-symmetric, so beta^Re_{-n} = conj(beta^Re_n);
  *                     DESIGN.md reading R2). With w2 = 0 the partial-fraction weights are
- *                     W1 = w1, W2 = 0, so variants PF, PFH and PFHR (default) run the same
+ *                     W1 = w1, W2 = 0, so variants PF, PFH, PFHR and PFHX (default) run the same
  *                     kernels as REXII; UV, DZ and DZ3 select the DZ back-substitution kernel
  *                     (one solve per term). */
 typedef enum { REXI_METHOD_REXII = 0, REXI_METHOD_REXI = 1 } rexi_method_t;
@@ -176,9 +188,11 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
  *               = four pairs) or 16 (two quads in linear order, no K2 sharing):
  *               (4,1,4) (4,1,5) (4,1,6) (4,2,3) (4,2,4) (4,4,3) (8,1,2) (8,1,3) (8,2,2) (8,3,2)
  *               (8,4,2) (8,8,2) (8,2,3) (8,4,3) (8,8,3) (16,2,2)          default (8,8,2)
+ *   REXII PFHX: modes_per_thread 8 (octet items): (8,1,2) (8,2,2) (8,4,2) (8,8,2) (8,1,3)
+ *               (8,2,3) (8,4,3) (8,8,3)                                  default (8,8,2)
  *   REXI with variant UV / DZ / DZ3 (DZ back-substitution kernel):
  *               (1,1,8) (2,1,4) (4,1,4) (4,1,5)                         default (4,1,4)
- *   REXI with variant PF / PFH / PFHR: as the REXII row of that variant (same kernels).
+ *   REXI with variant PF / PFH / PFHR / PFHX: as the REXII row of that variant (same kernels).
  * modes_per_thread = 4 maps each thread to a "K2 quad" (four modes with equal K^2 that share
  * the pole denominator 1/(kappa_n + K^2)).
  * Per pole and mode the operation order is the same for every tuning; the number of pole

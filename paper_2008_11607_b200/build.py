@@ -4,6 +4,7 @@
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -19,17 +20,33 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
-def _stale():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+STAMP = LIB + ".stamp"
+
+
+def _source_hash():
+    """sha256 over every source the library is built from, the public header, this script and
+    the nvcc flags: a prebuilt librexi.so is reused only if it was built from exactly these."""
+    h = hashlib.sha256()
     files = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "rexi.h"),
                                                      os.path.abspath(__file__)]
-    return any(os.path.getmtime(f) > t for f in files)
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    h.update(" ".join(FLAGS).encode())
+    return h.hexdigest()
+
+
+def _stale(digest):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return True
+    with open(STAMP) as f:
+        return f.read().strip() != digest
 
 
 def build(force=False, verbose=False):
-    if not force and not _stale():
+    digest = _source_hash()
+    if not force and not _stale(digest):
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *FLAGS, "-shared", "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
@@ -42,6 +59,8 @@ def build(force=False, verbose=False):
     if verbose:
         print(log)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(digest + "\n")
     return LIB
 
 

@@ -50,20 +50,24 @@ struct DeviceGuard {
 
 }  // namespace
 
+// shared with scalar.cu (launch.h): its entry points report through the same thread-local text
+void rexi::set_last_error(const char *msg) { g_last_error = msg ? msg : ""; }
+
 struct rexi_plan_s {
     rexi::Plan host;
     int device = 0;
-    int variant = REXI_VARIANT_PFHR;
+    int variant = REXI_VARIANT_PFHX;
     int method = REXI_METHOD_REXII;
     // pole-kernel tuning per kernel kind (0 REXII-DZ, 1 REXII-UV, 2 REXI): modes per thread,
     // poles per loop trip, min blocks/SM
-    int mpt[7] = {4, 4, 4, 4, 4, 4, 8}, pu[7] = {1, 1, 1, 1, 1, 2, 8}, minb[7] = {4, 3, 4, 4, 3, 2, 2};
-    int occ_cache[7] = {0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
+    int mpt[8] = {4, 4, 4, 4, 4, 4, 8, 8}, pu[8] = {1, 1, 1, 1, 1, 2, 8, 8}, minb[8] = {4, 3, 4, 4, 3, 2, 2, 2};
+    int occ_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     int sk_occ = 0;                            // same, stream-K R2C kernel
     int schedule = REXI_SCHEDULE_AUTO;
     int last_schedule = REXI_SCHEDULE_AUTO;
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
-    // 6 REXII PFH on R2C pairs (real input only; spectral calls use kind 5)
+    // 6 REXII PFH on R2C pairs, collapsed (real input only; spectral calls use kind 5),
+    // 7 REXII PFHX: explicit solves on R2C pairs (real input only; spectral calls use kind 5)
     int kind() const {
         if (method == REXI_METHOD_REXI) {
             // REXI: w2 = 0, so the partial-fraction weights are W1 = w1, W2 = 0 and the PF / PFH /
@@ -73,6 +77,7 @@ struct rexi_plan_s {
                 case REXI_VARIANT_PF: return 4;
                 case REXI_VARIANT_PFH: return 5;
                 case REXI_VARIANT_PFHR: return 6;
+                case REXI_VARIANT_PFHX: return 7;
                 default: return 2;
             }
         }
@@ -84,6 +89,7 @@ struct rexi_plan_s {
             case REXI_VARIANT_PF: return 4;
             case REXI_VARIANT_PFH: return 5;
             case REXI_VARIANT_PFHR: return 6;
+            case REXI_VARIANT_PFHX: return 7;
             default: return 0;
         }
     }
@@ -93,6 +99,7 @@ struct rexi_plan_s {
     // device buffers
     rexi::PoleConst *d_poles = nullptr;
     rexi::R2CPole *d_rpoles = nullptr;
+    rexi::R2XPole *d_xpoles = nullptr;
     double *d_ksym = nullptr;
     cd *d_tw = nullptr;
     cd *d_fhat = nullptr;   // [3][n_modes]
@@ -114,7 +121,7 @@ struct rexi_plan_s {
         const void *key[6];
         int mode;               // 0: physical step S1..S5, 1: spectral step (S2, S3, Re projection)
         long b, e;
-        int kind, mpt, pu, minb;
+        int kind, method, mpt, pu, minb;
         bool timing;
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
@@ -154,7 +161,7 @@ struct rexi_plan_s {
         if (ev_join) cudaEventDestroy(ev_join);
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
-        for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
+        for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_xpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
                         (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
@@ -173,13 +180,14 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range, int v) {
     if (n_range <= 0) return 0;
-    const long tiles = v == 6 ? rexi::pole_r2c_blocks(p->host.D, p->mpt[v])
+    const long tiles = v >= 6 ? rexi::pole_r2c_blocks(p->host.D, p->mpt[v])
                               : (p->n_modes + rexi::pole_modes_per_block(p->mpt[v]) - 1) /
                                     rexi::pole_modes_per_block(p->mpt[v]);
     int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];
     if (occ <= 0) {
-        cudaError_t e = v == 6 ? rexi::pole_r2c_occupancy(p->mpt[v], p->pu[v], p->minb[v], &occ)
-                               : rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ);
+        cudaError_t e = v == 7   ? rexi::pole_r2x_occupancy(p->pu[v], p->minb[v], &occ)
+                        : v == 6 ? rexi::pole_r2c_occupancy(p->mpt[v], p->pu[v], p->minb[v], &occ)
+                                 : rexi::pole_occupancy(v, p->mpt[v], p->pu[v], p->minb[v], &occ);
         if (e != cudaSuccess) occ = 1;
     }
     const long conc = (long)p->num_sms * std::max(1, occ);
@@ -261,7 +269,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
         return REXI_OK;
     }
     int kd = p->kind();
-    if (kd == 6 && !real_input) kd = 5;
+    if ((kd == 6 || kd == 7) && !real_input) kd = 5;
     // R2C with octet items, REXI_SCHEDULE_STREAMK: a persistent grid when the segment partials
     // fit the partial buffer (AUTO = chunked: measured 2-4 % faster, rexi.h)
     long sk_tiles = 0;
@@ -288,6 +296,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.partial = p->d_partial;
     a.poles = p->d_poles;
     a.rpoles = p->d_rpoles;
+    a.xpoles = p->d_xpoles;
     a.ksym = p->d_ksym;
     a.pole_begin = b;
     a.pole_end = e;
@@ -301,7 +310,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.sk_tiles = sk_tiles;
     a.sk_slots = sk_slots;
     rexi_status_t s;
-    const bool fork = (kd == 6);
+    const bool fork = (kd == 6 || kd == 7);
     if (fork) {
         // K = 0 corners on a side stream, concurrently with the pole kernel (disjoint outputs)
         if (!p->aux_stream) {
@@ -333,6 +342,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     if ((s = record(p, st, true)) != REXI_OK) return s;
     p->last_schedule = sk_tiles ? REXI_SCHEDULE_STREAMK : REXI_SCHEDULE_CHUNKED;
     if (sk_tiles) CK(rexi::launch_poles_r2c_sk(a, p->pu[kd], sk_ctas, st));
+    else if (kd == 7) CK(rexi::launch_poles_r2x(a, p->pu[kd], p->minb[kd], st));
     else if (kd == 6) CK(rexi::launch_poles_r2c(a, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     else CK(rexi::launch_poles(a, kd, p->mpt[kd], p->pu[kd], p->minb[kd], st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
@@ -368,7 +378,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     } else if (kd != 1) {   // DZ accumulators carry no velocity at K = 0
         rexi::FixupArgs x;
         x.method = p->method;
-        x.write_eta = kd == 6;
+        x.write_eta = kd >= 6;
         x.S = f.S;
         x.fhat = fhat;
         x.acc = acc;
@@ -409,7 +419,7 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
     rexi_status_t s;
     if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
     if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
-    return do_inverse(p, p->d_acc, eo, uo, vo, st, p->kind() == 6);
+    return do_inverse(p, p->d_acc, eo, uo, vo, st, p->kind() >= 6);
 }
 
 // One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
@@ -432,6 +442,7 @@ rexi_status_t do_step_graph(rexi_plan_s *p, int mode, long b, long e, const doub
     rexi_plan_s::GraphEntry *hit = nullptr;
     for (auto &g : p->graphs)
         if (g.mode == mode && std::equal(key, key + 6, g.key) && g.b == b && g.e == e && g.kind == kd &&
+            g.method == p->method &&
             g.mpt == p->mpt[kd] && g.pu == p->pu[kd] && g.minb == p->minb[kd] && g.timing == p->timing)
             hit = &g;
     if (!hit) {
@@ -453,6 +464,7 @@ rexi_status_t do_step_graph(rexi_plan_s *p, int mode, long b, long e, const doub
         g.b = b;
         g.e = e;
         g.kind = kd;
+        g.method = p->method;
         g.mpt = p->mpt[kd];
         g.pu = p->pu[kd];
         g.minb = p->minb[kd];
@@ -596,6 +608,7 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     auto alloc = [&](void **ptr, size_t bytes) -> cudaError_t { return cudaMalloc(ptr, bytes); };
     if ((e = alloc((void **)&p->d_poles, sizeof(rexi::PoleConst) * (size_t)p->host.n_poles)) ||
         (e = alloc((void **)&p->d_rpoles, sizeof(rexi::R2CPole) * (size_t)p->host.n_poles)) ||
+        (e = alloc((void **)&p->d_xpoles, sizeof(rexi::R2XPole) * (size_t)p->host.n_poles)) ||
         (e = alloc((void **)&p->d_ksym, sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_tw, 2 * sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
@@ -608,6 +621,8 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
     if ((e = cudaMemcpy(p->d_poles, p->host.poles.data(), sizeof(rexi::PoleConst) * (size_t)p->host.n_poles,
                         cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_rpoles, p->host.r2c.data(), sizeof(rexi::R2CPole) * (size_t)p->host.n_poles,
+                        cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(p->d_xpoles, p->host.r2x.data(), sizeof(rexi::R2XPole) * (size_t)p->host.n_poles,
                         cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_ksym, p->host.ksym.data(), sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(p->d_tw, p->host.twiddle.data(), 2 * sizeof(double) * (size_t)D, cudaMemcpyHostToDevice)))
@@ -648,7 +663,7 @@ rexi_status_t rexi_plan_info(rexi_plan_t p, rexi_plan_info_t *info) {
 
 rexi_status_t rexi_plan_set_variant(rexi_plan_t p, int variant) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PFHR) return fail(REXI_EINVAL, "unknown variant");
+    if (variant < REXI_VARIANT_DZ || variant > REXI_VARIANT_PFHX) return fail(REXI_EINVAL, "unknown variant");
     p->variant = variant;
     return REXI_OK;
 }
@@ -666,9 +681,13 @@ rexi_status_t rexi_plan_set_method(rexi_plan_t p, int method) {
         int st = rexi::make_plan(np, h.D, h.tau, h.tol, h.h, h.M, err, method, &h.table);
         if (st != REXI_OK) return fail((rexi_status_t)st, err.empty() ? "planner" : std::string(err.data()));
         CK(cudaDeviceSynchronize());
+        // cached graphs hold the old method's finish / fix-up arguments (pole sums S, Sd)
+        p->clear_graphs();
         CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         CK(cudaMemcpy(p->d_rpoles, np.r2c.data(), sizeof(rexi::R2CPole) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_xpoles, np.r2x.data(), sizeof(rexi::R2XPole) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         p->host = std::move(np);
         p->method = method;
@@ -695,21 +714,28 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t p, int L, double mu, const double 
         if (np.n_poles != h.n_poles) {
             rexi::PoleConst *d = nullptr;
             rexi::R2CPole *dr = nullptr;
+            rexi::R2XPole *dx = nullptr;
             cudaError_t e = cudaMalloc((void **)&d, sizeof(rexi::PoleConst) * (size_t)np.n_poles);
             if (e == cudaSuccess) e = cudaMalloc((void **)&dr, sizeof(rexi::R2CPole) * (size_t)np.n_poles);
+            if (e == cudaSuccess) e = cudaMalloc((void **)&dx, sizeof(rexi::R2XPole) * (size_t)np.n_poles);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 if (d) cudaFree(d);
+                if (dr) cudaFree(dr);
                 return fail(REXI_ENOMEM, "cudaMalloc (pole table) failed");
             }
             cudaFree(p->d_poles);
             cudaFree(p->d_rpoles);
+            cudaFree(p->d_xpoles);
             p->d_poles = d;
             p->d_rpoles = dr;
+            p->d_xpoles = dx;
         }
         CK(cudaMemcpy(p->d_poles, np.poles.data(), sizeof(rexi::PoleConst) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         CK(cudaMemcpy(p->d_rpoles, np.r2c.data(), sizeof(rexi::R2CPole) * (size_t)np.n_poles,
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_xpoles, np.r2x.data(), sizeof(rexi::R2XPole) * (size_t)np.n_poles,
                       cudaMemcpyHostToDevice));
         p->host = std::move(np);
         return REXI_OK;
@@ -720,8 +746,9 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int pole
                                    int min_blocks_per_sm) {
     if (!p) return fail(REXI_EINVAL, "null plan");
     const int v = p->kind();
-    const bool ok = v == 6 ? rexi::pole_r2c_supported(modes_per_thread, poles_per_iter, min_blocks_per_sm)
-                           : rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm);
+    const bool ok = v == 7   ? rexi::pole_r2x_supported(modes_per_thread, poles_per_iter, min_blocks_per_sm)
+                    : v == 6 ? rexi::pole_r2c_supported(modes_per_thread, poles_per_iter, min_blocks_per_sm)
+                             : rexi::pole_config_supported(v, modes_per_thread, poles_per_iter, min_blocks_per_sm);
     if (!ok) return fail(REXI_EINVAL, "unsupported pole-kernel tuning for this variant");
     p->mpt[v] = modes_per_thread;
     p->pu[v] = poles_per_iter;
@@ -821,16 +848,21 @@ rexi_status_t rexi_apply_host(rexi_plan_t p, const double *eta, const double *u,
         for (int i = 0; i < 6; ++i) d[i] = p->d_stage + i * n;
         const double *hin[3] = {eta, u, v};
         double *hout[3] = {eo, uo, vo};
-        for (int i = 0; i < 3; ++i)
-            CK(cudaMemcpyAsync(d[i], hin[i], n * sizeof(double), cudaMemcpyHostToDevice, st));
-        rexi_status_t s;
-        if ((s = do_step(p, 0, p->host.n_poles, d[0], d[1], d[2], d[3], d[4], d[5], st)) != REXI_OK) {
-            cudaStreamSynchronize(st);   // the input copies must not outlive the call
-            return s;
+        // every failure path below still drains the stream: no queued copy may touch the
+        // caller's host buffers once this call has returned
+        rexi_status_t s = REXI_OK;
+        for (int i = 0; i < 3 && s == REXI_OK; ++i) {
+            const cudaError_t e = cudaMemcpyAsync(d[i], hin[i], n * sizeof(double), cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync (H2D)");
         }
-        for (int i = 0; i < 3; ++i)
-            CK(cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        if (s == REXI_OK) s = do_step(p, 0, p->host.n_poles, d[0], d[1], d[2], d[3], d[4], d[5], st);
+        for (int i = 0; i < 3 && s == REXI_OK; ++i) {
+            const cudaError_t e = cudaMemcpyAsync(hout[i], d[3 + i], n * sizeof(double), cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync (D2H)");
+        }
+        const cudaError_t es = cudaStreamSynchronize(st);
+        if (s != REXI_OK) return s;
+        if (es != cudaSuccess) return cuda_fail(es, "cudaStreamSynchronize");
         return REXI_OK;
     });
 }

@@ -869,6 +869,135 @@ __global__ void __launch_bounds__(kSkBlock, 1) pole_kernel_r2c_sk(PoleArgs a) {
     }
 }
 
+// ----------------------------------------------------------------------------- PFHX (default)
+// Explicit-solve R2C pairs. For every pole n and every {K, -K} pair the kernel forms the two
+// Helmholtz solutions of the pair's representative mode from that mode's own right-hand sides
+// (eq:lswEta, tau-scaled; partial fractions of the two resolvents, SURVEY.md
+// 8(d) allowed equivalent):
+//   num1  = B0  + i hn eta0 - (c/alpha) m0          eta1  = q num1         (alpha_n I + tau A)
+//   num_t = Bt0 - i hn eta0 - conj(c/alpha) m0      eta_t = conj(q) num_t  (conj(alpha_n) I - tau A)
+// with q = 1/(kappa_n + K2), one reciprocal per pole and K2 value (shared by the octet's eight
+// modes; the second system's denominator is its conjugate). The solves at -K follow from the
+// Hermitian data (R2C pairs above): conj(eta1(-K)) = eta_t + 2 conj(q) delta0 and
+// conj(eta_t(-K)) = eta1 - 2 q delta0, so the Hermitian part of the pair's weighted sum takes,
+// for every pole,
+//   H_eta    += X1 eta1 + conj(X1) eta_t + sigma_n delta0,   sigma_n = conj(W1 q) - conj(W2) q
+//   H_delta' += Y1 eta1 + conj(Y1) eta_t + tau'_n delta0     (P1, P2 for tau'_n)
+// where X1 eta1 + conj(X1) eta_t = Re(X1)(eta1 + eta_t) + i Im(X1)(eta1 - eta_t). The delta
+// back-substitution of each solve (delta = alpha eta - eta0, first row) is folded into the
+// weights (PFH); zeta and (u, v) follow once per mode in finish_kernel. fp64 work per pole: 7
+// (denominator) + 8 (sigma_n, tau'_n) per K2 value, 40 per pair (launch.h).
+struct XPair {
+    cd e0, B0, Bt0, m0, d0;   // eta0, h mu eta0 + delta0, h mu eta0 - delta0, zeta0 - c eta0, delta0
+    cd H0, H1;                // Hermitian accumulators: eta, delta' (before the -Re(sum w1) eta0 term)
+};
+
+template <int PU>
+__device__ __forceinline__ void r2x_tile(const R2XPole *sp, int cnt, const double K2, XPair (&st)[4]) {
+#pragma unroll PU
+    for (int qq = 0; qq < cnt; ++qq) {
+        const R2XPole &P = sp[qq];
+        const cd q = pole_den(P, K2);
+        const cd sg = mk(fma(P.sgx1, q.x, P.sgx2 * q.y), fma(P.sgy1, q.x, P.sgy2 * q.y));
+        const cd ta = mk(fma(P.tax1, q.x, P.tax2 * q.y), fma(P.tay1, q.x, P.tay2 * q.y));
+        const double hn = P.hn, sr = P.s2r, si = P.s2i;
+        const double xr = P.X1r, xi = P.X1i, yr = P.Y1r, yi = P.Y1i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            XPair &s = st[j];
+            // right-hand sides of the two shifted systems after the Helmholtz reduction
+            const cd n1 = mk(fma(-hn, s.e0.y, fma(-sr, s.m0.x, fma(si, s.m0.y, s.B0.x))),
+                             fma(hn, s.e0.x, fma(-sr, s.m0.y, fma(-si, s.m0.x, s.B0.y))));
+            const cd nt = mk(fma(hn, s.e0.y, fma(-sr, s.m0.x, fma(-si, s.m0.y, s.Bt0.x))),
+                             fma(-hn, s.e0.x, fma(-sr, s.m0.y, fma(si, s.m0.x, s.Bt0.y))));
+            // the two Helmholtz solutions of this pole and mode
+            const cd eta1 = cmul(q, n1);
+            const cd etat = mk(fma(q.x, nt.x, q.y * nt.y), fma(q.x, nt.y, -q.y * nt.x));   // conj(q) nt
+            // weighted accumulation of the Hermitian part
+            const cd S = mk(eta1.x + etat.x, eta1.y + etat.y);
+            const cd Df = mk(eta1.x - etat.x, eta1.y - etat.y);
+            s.H0.x = fma(xr, S.x, fma(-xi, Df.y, fma(sg.x, s.d0.x, fma(-sg.y, s.d0.y, s.H0.x))));
+            s.H0.y = fma(xr, S.y, fma(xi, Df.x, fma(sg.x, s.d0.y, fma(sg.y, s.d0.x, s.H0.y))));
+            s.H1.x = fma(yr, S.x, fma(-yi, Df.y, fma(ta.x, s.d0.x, fma(-ta.y, s.d0.y, s.H1.x))));
+            s.H1.y = fma(yr, S.y, fma(yi, Df.x, fma(ta.x, s.d0.y, fma(ta.y, s.d0.x, s.H1.y))));
+        }
+    }
+}
+
+// grid = (octet-item tiles of 128, pole chunks); a thread owns one octet item (four {K, -K}
+// pairs with one K2, r2c_octet_item) and runs every pole of its chunk.
+template <int PU, int MINB>
+__global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) {
+    __shared__ R2XPole sp[kR2CTile];
+    const long n_modes = a.n_modes;
+    const int chunk = blockIdx.y;
+    const long len = a.pole_end - a.pole_begin;
+    const long p0 = a.pole_begin + len * chunk / a.n_chunks;
+    const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
+    const double c = a.tau;
+    const double hmu = a.hmu;
+    const int H = a.D >> 1;
+    const long item = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+    long quad[2];
+    bool ok[2];
+    bool shared_k2 = false;
+    r2c_octet_item(item, a.D, quad, ok, shared_k2);
+    long rep[4];
+    double K2 = 0.0;
+    XPair st[4];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        const long qs = quad[g];
+        long mq[4];
+        quad_modes(qs, a.D, a.log2D, mq);
+        const int qa = (int)(qs >> (a.log2D - 1)), qb = (int)(qs & (H - 1));
+        rep[2 * g] = mq[0];
+        rep[2 * g + 1] = (qa > 0 && qb > 0) ? mq[1] : mq[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const long mm = rep[2 * g + j];
+            const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
+            const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
+            const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
+            // delta0 = i (kx u + ky v), zeta0 = i (kx v - ky u)   (tau-scaled)
+            const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
+            const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
+            XPair &s = st[2 * g + j];
+            s.e0 = e;
+            s.d0 = d;
+            s.B0 = mk(fma(hmu, e.x, d.x), fma(hmu, e.y, d.y));
+            s.Bt0 = mk(fma(hmu, e.x, -d.x), fma(hmu, e.y, -d.y));
+            s.m0 = mk(fma(-c, e.x, z.x), fma(-c, e.y, z.y));
+            s.H0 = mk(0, 0);
+            s.H1 = mk(0, 0);
+            K2 = fma(kx, kx, ky * ky);   // the same for all four pairs of an octet item
+        }
+    }
+    for (long pt = p0; pt < p1; pt += kR2CTile) {
+        const int cnt = (int)min((long)kR2CTile, p1 - pt);
+        __syncthreads();
+        {
+            const double2 *src = reinterpret_cast<const double2 *>(a.xpoles + pt);
+            double2 *dst = reinterpret_cast<double2 *>(sp);
+            constexpr int kPer = (int)(sizeof(R2XPole) / sizeof(double2));
+            for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
+        }
+        __syncthreads();
+        r2x_tile<PU>(sp, cnt, K2, st);
+    }
+    cd *out = a.partial + (size_t)chunk * 3 * n_modes;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        if (ok[g]) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                out[rep[2 * g + j]] = st[2 * g + j].H0;
+                out[n_modes + rep[2 * g + j]] = st[2 * g + j].H1;
+            }
+        }
+    }
+}
+
 // grid = (tiles, pole chunks). MPT < 4: a thread owns MPT modes m = tile0 + j * 128 + tid.
 // MPT = 4: a thread owns one K2 quad (quad_modes) and computes the pole denominator
 // 1/(kappa_n + K2) once for its four modes. Every thread runs all poles of its chunk, PU poles
@@ -992,7 +1121,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long m = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long n = a.n_modes;
     if (m >= n) return;
-    if (a.kind == 6) {   // R2C pairs: Hermitian accumulators at the representative mode
+    if (a.kind == 6 || a.kind == 7) {   // R2C pairs: Hermitian accumulators at the representative mode
         const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
         const long mm = ((long)((a.D - l) & (a.D - 1)) << a.log2D) + ((a.D - k) & (a.D - 1));
         if (mm <= m) return;   // self-mirror K = 0 corner (fixup_k0_kernel), or the mirror of a pair
@@ -1360,6 +1489,35 @@ cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaS
 #define X(M, U, B) if (mpt == M && pu == U && minb == B) { \
     R2C_KERNEL(M, U, B)<<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
     REXI_R2C_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+// Explicit-solve R2C kernel (PFHX, default) instantiations: (poles per loop trip, min blocks);
+// octet items only (modes_per_thread 8).
+#define REXI_R2X_CONFIGS(X) X(1, 2) X(2, 2) X(4, 2) X(8, 2) X(1, 3) X(2, 3) X(4, 3) X(8, 3)
+
+bool pole_r2x_supported(int mpt, int pu, int minb) {
+    if (mpt != 8) return false;
+#define X(U, B) if (pu == U && minb == B) return true;
+    REXI_R2X_CONFIGS(X)
+#undef X
+    return false;
+}
+
+cudaError_t pole_r2x_occupancy(int pu, int minb, int *blocks_per_sm) {
+#define X(U, B) if (pu == U && minb == B) \
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2x<U, B>, kPoleBlock, 0);
+    REXI_R2X_CONFIGS(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
+    dim3 grid((unsigned)pole_r2c_blocks(a.D, 8), (unsigned)a.n_chunks);
+#define X(U, B) if (pu == U && minb == B) { \
+    pole_kernel_r2x<U, B><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
+    REXI_R2X_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;
 }

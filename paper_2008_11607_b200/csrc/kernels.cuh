@@ -63,6 +63,7 @@ struct PoleArgs {
     cd *partial;           // [n_chunks][3][D*D]
     const PoleConst *poles;
     const R2CPole *rpoles; // the same poles, R2C kernel layout
+    const R2XPole *xpoles; // the same poles, explicit-solve R2C kernel layout
     const double *ksym;    // [D]
     long pole_begin, pole_end;
     long n_modes;          // D*D

@@ -7,6 +7,9 @@
 
 namespace rexi {
 
+// thread-local text returned by rexi_last_error() (capi.cu); scalar.cu sets it on its failures
+void set_last_error(const char *msg);
+
 cudaError_t fft_setup_attributes();
 // S1: real fields -> full spectrum (x scale); half = D x D complex scratch per field.
 cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
@@ -23,6 +26,10 @@ bool pole_r2c_supported(int mpt, int pu, int minb);
 long pole_r2c_blocks(int D, int mpt);
 cudaError_t pole_r2c_occupancy(int mpt, int pu, int minb, int *blocks_per_sm);
 cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaStream_t st);
+// explicit-solve R2C kernel (PFHX, kind 7; octet items, modes_per_thread 8)
+bool pole_r2x_supported(int mpt, int pu, int minb);
+cudaError_t pole_r2x_occupancy(int pu, int minb, int *blocks_per_sm);
+cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st);
 // stream-K R2C (octet items, modes_per_thread 8): persistent grid of `ctas` blocks
 cudaError_t launch_poles_r2c_sk(const PoleArgs &a, int pu, int ctas, cudaStream_t st);
 cudaError_t pole_r2c_sk_occupancy(int pu, int *blocks_per_sm);
@@ -49,6 +56,13 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 //     12.75 / 22.75 resp. 9.875 / 17.875 per mode; modes_per_thread 8 uses octets for the
 //     (H-1)(H-2)/2 interior quad pairs (a, b), (b, a) and half-discarded octets for the other
 //     3(H-1) quads.
+//   kind 7 (PFHX, explicit solves on R2C pairs, real input; the default): per K2 value and pole
+//     den 7/11 and the per-pole delta0 coefficients sigma_n, tau'_n (2 MUL + 2 FMA each) 8/12;
+//     per pair and pole the two right-hand sides num1, num_t (12 FMA) 12/24, the two solutions
+//     eta1 = q num1, eta_t = conj(q) num_t (2 MUL + 2 FMA each) 8/12, their sum and difference
+//     (4 ADD) 4/4 and the Hermitian accumulation of eta and delta' (16 FMA) 16/32 = 40/72.
+//     An octet (8 modes, shared K2) = 175 / 311, i.e. 21.875 / 38.875 per mode (+ the
+//     discarded halves of the 3(H-1) single-quad items, as for kind 6).
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
 // by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
@@ -61,11 +75,13 @@ inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
 }
 inline double pole_flops(int kind, int mpt, int D) {
     if (kind == 6) return r2c_per_mode(mpt, D, 91.0, 143.0);
+    if (kind == 7) return r2c_per_mode(8, D, 0.0, 311.0);
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt, int D) {
     if (kind == 6) return r2c_per_mode(mpt, D, 51.0, 79.0);
+    if (kind == 7) return r2c_per_mode(8, D, 0.0, 175.0);
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

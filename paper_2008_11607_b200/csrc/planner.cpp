@@ -155,6 +155,7 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
     p.gamma.assign((size_t)p.n_poles, 0.0);
     p.poles.assign((size_t)p.n_poles, PoleConst{});
     p.r2c.assign((size_t)p.n_poles, R2CPole{});
+    p.r2x.assign((size_t)p.n_poles, R2XPole{});
     p.spre_re.assign((size_t)p.n_poles + 1, 0.0L);
     p.spre_im.assign((size_t)p.n_poles + 1, 0.0L);
     p.wpre_re.assign((size_t)p.n_poles + 1, 0.0L);
@@ -248,6 +249,18 @@ int make_plan(Plan &p, int D, double tau, double tol, double h, long M, std::vec
             rq.tax1 = (double)(P1.real() - P2.real());   rq.tax2 = (double)(-(P1.imag() + P2.imag()));
             rq.tay1 = (double)(P2.imag() - P1.imag() + 2.0L * Y1.imag());
             rq.tay2 = (double)(-(P1.real() + P2.real()) + 2.0L * Y1.real());
+            R2XPole &rx = p.r2x[(size_t)n];
+            rx.kr = q.kr;                 rx.ki = q.ki;
+            rx.ki2 = q.ki2;               rx.hn = q.ai;
+            rx.s2r = q.s2r;               rx.s2i = q.s2i;
+            rx.X1r = rq.X1r;              rx.X1i = rq.X1i;
+            rx.Y1r = rq.Y1r;              rx.Y1i = rq.Y1i;
+            rx.sgx1 = rq.sgx1;            rx.sgx2 = rq.sgx2;
+            rx.sgy1 = (double)(W2.imag() - W1.imag());
+            rx.sgy2 = (double)(-(W1.real() + W2.real()));
+            rx.tax1 = rq.tax1;            rx.tax2 = rq.tax2;
+            rx.tay1 = (double)(P2.imag() - P1.imag());
+            rx.tay2 = (double)(-(P1.real() + P2.real()));
         }
         q.ia2 = (double)std::norm(ia);
     }

@@ -59,6 +59,26 @@ struct alignas(16) R2CPole {
 };
 static_assert(sizeof(R2CPole) == 144, "R2CPole layout");
 
+// The constants the explicit-solve R2C kernel (PFHX, the default) reads per pole, nine 16-byte
+// shared-memory loads: kappa, Im(kappa)^2, h n and c/alpha build the two Helmholtz solves of a
+// mode pair, eta1 = q num1 and eta_t = conj(q) num_t (q = 1/(kappa + K2)); X1 = (W1 + conj W2)/2,
+// Y1 = (P1 + conj P2)/2 weight them (partners conj X1, conj Y1); the per-pole coefficient of the
+// -K correction 2 conj(q) delta0 resp. 2 q delta0 (kernels.cu, "R2C pairs") as real
+// coefficients of q = qr + i qi (W1 = a + ib, W2 = c + id):
+//   sigma_n = conj(W1 q) - conj(W2) q = [(a-c) qr - (b+d) qi] + i [(d-b) qr - (a+c) qi],
+// tau'_n likewise with P1, P2. sigma_n and tau'_n are formed per pole and applied to each pair's
+// delta0 per pole (no pole sum is formed before it meets a mode's data).
+struct alignas(16) R2XPole {
+    double kr, ki;
+    double ki2, hn;
+    double s2r, s2i;
+    double X1r, X1i;
+    double Y1r, Y1i;
+    double sgx1, sgx2, sgy1, sgy2;
+    double tax1, tax2, tay1, tay2;
+};
+static_assert(sizeof(R2XPole) == 144, "R2XPole layout");
+
 struct Plan {
     GaussTable table;
     int D = 0;
@@ -70,6 +90,7 @@ struct Plan {
     std::vector<double> alpha, C1, C2, gamma;   // REXI plans: C1 = beta^Re_n, C2 = 0
     std::vector<PoleConst> poles;
     std::vector<R2CPole> r2c;        // the same poles for the R2C kernel
+    std::vector<R2XPole> r2x;        // the same poles for the explicit-solve R2C kernel
     // prefix sums (extended precision) of w1_n / alpha_n + w2_n / |alpha_n|^2, n = 0..N:
     // S(b, e) = pre[e] - pre[b] rebuilds the zeta pole sum from the eta pole sum (finish_kernel)
     std::vector<long double> spre_re, spre_im;

@@ -21,6 +21,7 @@
 
 #include "../../include/rexi.h"
 #include "kernels.cuh"
+#include "launch.h"
 #include "planner.h"
 
 using rexi::cd;
@@ -81,10 +82,15 @@ struct rexi_scalar_plan_s {
     }
 };
 
+static rexi_status_t sfail(rexi_status_t s, const char *msg) {
+    rexi::set_last_error(msg);
+    return s;
+}
+
 extern "C" {
 
 rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M, int device) {
-    if (!out) return REXI_EINVAL;
+    if (!out) return sfail(REXI_EINVAL, "out is NULL");
     *out = nullptr;
     std::vector<rexi::ScalarTerm> terms;
     std::vector<char> err;
@@ -92,11 +98,11 @@ rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M,
     try {
         st = rexi::make_scalar_terms(terms, h, M, err);
     } catch (...) {
-        return REXI_ENOMEM;
+        return sfail(REXI_ENOMEM, "scalar term table allocation failed");
     }
-    if (st != REXI_OK) return (rexi_status_t)st;
+    if (st != REXI_OK) return sfail((rexi_status_t)st, err.empty() ? "invalid h or M" : err.data());
     rexi_scalar_plan_s *p = new (std::nothrow) rexi_scalar_plan_s();
-    if (!p) return REXI_ENOMEM;
+    if (!p) return sfail(REXI_ENOMEM, "host allocation failed");
     p->device = device;
     p->h = h;
     p->M = M;
@@ -105,7 +111,8 @@ rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M,
     cudaGetDevice(&prev);
     if (cudaSetDevice(device) != cudaSuccess) {
         delete p;
-        return REXI_ECUDA;
+        cudaGetLastError();
+        return sfail(REXI_ECUDA, "cudaSetDevice failed");
     }
     cudaError_t e = cudaMalloc((void **)&p->d_terms, sizeof(rexi::ScalarTerm) * terms.size());
     if (e == cudaSuccess)
@@ -114,14 +121,16 @@ rexi_status_t rexi_scalar_plan_create(rexi_scalar_plan_t *out, double h, long M,
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
         delete p;
-        return e == cudaErrorMemoryAllocation ? REXI_ENOMEM : REXI_ECUDA;
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? sfail(REXI_ENOMEM, "cudaMalloc (scalar terms) failed")
+                                              : sfail(REXI_ECUDA, cudaGetErrorString(e));
     }
     *out = p;
     return REXI_OK;
 }
 
 rexi_status_t rexi_scalar_plan_destroy(rexi_scalar_plan_t p) {
-    if (!p) return REXI_EINVAL;
+    if (!p) return sfail(REXI_EINVAL, "null scalar plan");
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(p->device);
@@ -135,14 +144,17 @@ long rexi_scalar_plan_terms(rexi_scalar_plan_t p) { return p ? 2 * p->N + 1 : -1
 rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t p, int method, long n, const double *x,
                                 const double *in, double *out, double phase_re, double phase_im,
                                 void *stream) {
-    if (!p || n < 0 || (n > 0 && (!x || !in || !out))) return REXI_EINVAL;
+    if (!p || n < 0 || (n > 0 && (!x || !in || !out))) return sfail(REXI_EINVAL, "null plan/pointer or n < 0");
     if (method != REXI_SCALAR_REXII && method != REXI_SCALAR_REXI && method != REXI_SCALAR_REXI_M)
-        return REXI_EINVAL;
+        return sfail(REXI_EINVAL, "unknown scalar method");
     if (n == 0) return REXI_OK;
-    if (n > 0x7fffffffL) return REXI_EINVAL;
+    if (n > 0x7fffffffL) return sfail(REXI_EINVAL, "n exceeds the grid limit (2^31 - 1)");
     int prev = 0;
     cudaGetDevice(&prev);
-    if (cudaSetDevice(p->device) != cudaSuccess) return REXI_ECUDA;
+    if (cudaSetDevice(p->device) != cudaSuccess) {
+        cudaGetLastError();
+        return sfail(REXI_ECUDA, "cudaSetDevice failed");
+    }
     const long nt = 2 * p->N + 1;
     const cd ph = cd{phase_re, phase_im};
     const cd *cin = reinterpret_cast<const cd *>(in);
@@ -156,7 +168,7 @@ rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t p, int method, long n, const 
         scalar_kernel<REXI_SCALAR_REXI_M><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, cin, cout, ph);
     cudaError_t e = cudaGetLastError();
     cudaSetDevice(prev);
-    return e == cudaSuccess ? REXI_OK : REXI_ECUDA;
+    return e == cudaSuccess ? REXI_OK : sfail(REXI_ECUDA, cudaGetErrorString(e));
 }
 
 }  // extern "C"

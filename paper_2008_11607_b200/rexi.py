@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
-VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4, "pfhr": 5}
+VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4, "pfhr": 5, "pfhx": 6}
 METHODS = {"rexii": 0, "rexi": 1}
 SCHEDULES = {"auto": 0, "chunked": 1, "streamk": 2}
 
@@ -164,7 +164,7 @@ def _torch():
 class Plan:
     """One REXII step e^{tau A} on a D x D grid (rexi_plan_create)."""
 
-    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfhr", method="rexii"):
+    def __init__(self, D, tau, tol=1e-12, h=0.5, M=0, device=None, variant="pfhx", method="rexii"):
         """h = "auto" (or H_AUTO) selects h_for_tol(tol) (NEXT-2)."""
         if isinstance(h, str):
             if h != "auto":
@@ -406,10 +406,20 @@ class ScalarPlan:
     def apply(self, x, vec, method="rexii", phase=1.0 + 0.0j, out=None):
         """out_j = phase * r(i x_j) * vec_j for float64 x and complex128 vec (CUDA tensors)."""
         torch = _torch()
-        if x.dtype != torch.float64 or vec.dtype != torch.complex128 or x.shape != vec.shape \
-                or not (x.is_cuda and vec.is_cuda) or not (x.is_contiguous() and vec.is_contiguous()):
-            raise ValueError("x: contiguous float64, vec: contiguous complex128, same shape, CUDA")
+        ok = (isinstance(x, torch.Tensor) and isinstance(vec, torch.Tensor)
+              and x.dtype == torch.float64 and vec.dtype == torch.complex128 and x.shape == vec.shape
+              and x.is_cuda and vec.is_cuda and x.is_contiguous() and vec.is_contiguous()
+              and x.device.index == self.device and vec.device.index == self.device)
+        if not ok:
+            raise ValueError(f"x: contiguous float64, vec: contiguous complex128, same shape, on "
+                             f"cuda:{self.device}")
+        if method not in SCALAR_METHODS:
+            raise ValueError(f"method must be one of {sorted(SCALAR_METHODS)}")
         out = torch.empty_like(vec) if out is None else out
+        if not (isinstance(out, torch.Tensor) and out.dtype == torch.complex128 and out.shape == vec.shape
+                and out.is_cuda and out.device.index == self.device and out.is_contiguous()):
+            raise ValueError(f"out: expected a contiguous complex128 tensor of shape {tuple(vec.shape)} "
+                             f"on cuda:{self.device}")
         stream = _vp(torch.cuda.current_stream(self.device).cuda_stream)
         _check(_lib.rexi_scalar_apply(self._h, SCALAR_METHODS[method], int(x.numel()), _vp(x.data_ptr()),
                                       _vp(vec.data_ptr()), _vp(out.data_ptr()), float(complex(phase).real),

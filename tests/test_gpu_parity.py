@@ -186,7 +186,7 @@ def test_pole_kernel_c4_size_sampled(R, variant):
 
 
 # ----------------------------------------------------------------------------- S1..S5
-@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh", "pfhr"])
+@pytest.mark.parametrize("variant", ["dz", "uv", "dz3", "pf", "pfh", "pfhr", "pfhx"])
 @pytest.mark.parametrize("D,tau,tol,scen", [(64, 0.02, 1e-12, "gauss"), (64, 0.02, 1e-12, "white"),
                                             (128, 1.0, 1e-12, "gauss"), (32, 3.0, 1e-10, "white"),
                                             (8, 0.7, 1e-12, "white")])
@@ -301,7 +301,7 @@ def test_schedules_agree(R, D, tau, tol):
     fd = [dev(x) for x in f]
     res = {}
     for sched in ("chunked", "streamk", "auto"):
-        p = R.Plan(D, tau, tol=tol)
+        p = R.Plan(D, tau, tol=tol, variant="pfhr")   # stream-K exists for the PFHR kernel only
         p.set_schedule(sched)
         res[sched] = [host(t) for t in p.apply(*fd)]
         info = p.info
@@ -311,7 +311,7 @@ def test_schedules_agree(R, D, tau, tol):
     assert rel_l2(res["streamk"], res["chunked"]) < 1e-14
     assert rel_l2(res["auto"], res["chunked"]) < 1e-14
     if D <= 128:
-        info = R.Plan(D, tau, tol=tol).info
+        info = R.Plan(D, tau, tol=tol, variant="pfhr").info
         g = lrsw.rexii_step(*f, tau, info["h"], info["M"])
         assert rel_l2(res["streamk"], g) < TOL
 
@@ -341,9 +341,9 @@ def test_variants_agree(R):
     D = 128
     f = [dev(x) for x in inputs.white_noise(D)]
     res = {}
-    for v in ("dz", "uv", "dz3", "pf", "pfh", "pfhr"):
+    for v in ("dz", "uv", "dz3", "pf", "pfh", "pfhr", "pfhx"):
         res[v] = [host(t) for t in R.Plan(D, 2.0, variant=v).apply(*f)]
-    for v in ("uv", "dz3", "pf", "pfh", "pfhr"):
+    for v in ("uv", "dz3", "pf", "pfh", "pfhr", "pfhx"):
         assert rel_l2(res["dz"], res[v]) < TOL
 
 
@@ -445,11 +445,11 @@ def test_rexi_method_vs_oracle(R, D, tau, h, M):
     assert rel_l2(got, ref) < TOL
 
 
-@pytest.mark.parametrize("variant", ["uv", "dz", "dz3", "pf", "pfh", "pfhr"])
+@pytest.mark.parametrize("variant", ["uv", "dz", "dz3", "pf", "pfh", "pfhr", "pfhx"])
 @pytest.mark.parametrize("D,tau,h,M", [(16, 1.0, 0.2, 150), (64, 0.5, 0.2, 500)])
 def test_rexi_method_variants(R, variant, D, tau, h, M):
     """REXI (w2 = 0) through every variant: the DZ back-substitution kernel (uv, dz, dz3) and
-    the partial-fraction kernels with W1 = w1, W2 = 0 (pf, pfh, pfhr incl. R2C octets)."""
+    the partial-fraction kernels with W1 = w1, W2 = 0 (pf, pfh, pfhr, pfhx incl. R2C octets)."""
     f = inputs.white_noise(D, seed=21)
     p = R.Plan(D, tau, h=h, M=M, method="rexi", variant=variant)
     got = [host(t) for t in p.apply(*(dev(x) for x in f))]
@@ -466,6 +466,27 @@ def test_rexi_method_tunings(R, mpt, pu, minb):
     p.set_tuning(mpt, pu, minb)
     got = [host(t) for t in p.apply(*f)]
     assert rel_l2(got, base) < 1e-14
+
+
+def test_set_method_invalidates_graphs(R):
+    """apply (REXII) -> set_method('rexi') -> apply into the SAME buffers must not replay the
+    REXII graph (its finish / fix-up arguments carry the old method's pole sums): the result
+    equals a fresh REXI plan's, and switching back reproduces the REXII result."""
+    import torch
+    D, tau, h, M = 32, 1.0, 0.2, 200
+    f = [dev(x) for x in inputs.white_noise(D, seed=77)]
+    out = [torch.empty((D, D), dtype=torch.float64, device="cuda") for _ in range(3)]
+    for variant in ("pfhx", "pfhr", "pfh", "dz"):
+        p = R.Plan(D, tau, h=h, M=M, variant=variant)
+        a = [host(t) for t in p.apply(*f, out=out)]
+        p.set_method("rexi")
+        b = [host(t) for t in p.apply(*f, out=out)]
+        ref = [host(t) for t in R.Plan(D, tau, h=h, M=M, method="rexi", variant=variant).apply(*f)]
+        assert rel_l2(b, ref) == 0.0, variant
+        p.set_method("rexii")
+        c = [host(t) for t in p.apply(*f, out=out)]
+        assert rel_l2(c, a) == 0.0, variant
+        assert rel_l2(b, a) > 1e-6          # the two methods really differ at this (h, M)
 
 
 def test_set_method_roundtrip(R):
@@ -547,7 +568,7 @@ def test_pfhr_tunings_vs_oracle(R, mpt, pu, minb, D):
 
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
 def test_apply_full_size_sampled_vs_oracle(R, cfg):
-    """The bench's launch configuration (default plan: PFHR octet kernel, chunked schedule,
+    """The bench's launch configuration (default plan: PFHX octet kernel, chunked schedule,
     whole-step graph) at BASELINE's full sizes, element by element against the oracle on
     sampled modes: the spectrum of the GPU's physical output at K must equal the Hermitian part
     of the oracle's dense-LU pole sum, (A(K) + conj A(-K)) / 2 — the spectral form of
@@ -575,16 +596,32 @@ def test_apply_full_size_sampled_vs_oracle(R, cfg):
     assert err < TOL, err
 
 
-def test_pfhr_c2_full_size_properties(R):
-    """The default (PFHR) at the bench configuration: vs DZ3 (all per-pole components formed)
-    and vs the exact propagator."""
+@pytest.mark.parametrize("variant", ["pfhx", "pfhr"])
+def test_r2c_c2_full_size_properties(R, variant):
+    """The default (PFHX) and the collapsed PFHR at the bench configuration: vs DZ3 (all
+    per-pole components formed) and vs the exact propagator."""
     D = 512
     f = inputs.gaussian_scenario(D)
     t = [dev(x) for x in f]
-    a = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant="pfhr").apply(*t)]
+    a = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant=variant).apply(*t)]
     b = [host(x) for x in R.Plan(D, 1.0, tol=1e-8, variant="dz3").apply(*t)]
     assert rel_l2(a, b) < TOL
     assert rel_l2(a, lrsw.exact_step(*f, 1.0)) < 1e-8
+
+
+@pytest.mark.parametrize("pu,minb", [(1, 2), (2, 2), (4, 2), (8, 2), (1, 3), (2, 3), (4, 3), (8, 3)])
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 64])
+def test_pfhx_tunings_vs_oracle(R, pu, minb, D):
+    """Explicit-solve R2C kernel (the default): every tuning vs the oracle step on grids with
+    every quad type (corner, axis, Nyquist, interior, half-discarded octets) and ragged tiles."""
+    tau = 0.9
+    f = inputs.white_noise(D)
+    p = R.Plan(D, tau, variant="pfhx")
+    p.set_tuning(8, pu, minb)
+    got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    info = p.info
+    ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])
+    assert rel_l2(got, ref) < TOL
 
 
 def test_h_auto_c2(R):

@@ -133,13 +133,25 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def oracle_rate(D, tau, tol, scen, seconds, threads=0):
     """Time the oracle (as it stands) on a bounded sample of the workload: all poles on a
     deterministic sample of Fourier modes (per-mode work is identical across modes).
-    Returns (pole·gp/s, cores, sample description, n_poles)."""
+    threads > 0 sets the oracle's OpenMP thread count for this call (restored after).
+    Returns (pole·gp/s, cores, sample description, n_poles, seconds)."""
     from oracle import coeffs as C
     from oracle import lrsw
     from paper_2008_11607_b200 import inputs
+    prev = lrsw.num_threads(0)
     cores = lrsw.num_threads(threads)
     h = 0.5
     M = C.M_lrsw(D, tau, h, tol)
@@ -147,21 +159,24 @@ def oracle_rate(D, tau, tol, scen, seconds, threads=0):
     f = scenario(scen, D)
     # spectral input by the oracle's own naive DFT (one-off, not part of the timed sample)
     F = lrsw.spectral_fields(*f)
-    S = 64
+    S = 64 if threads != 1 else 8
     rate = None
     desc = ""
-    while True:
-        ml, mk = inputs.sample_modes(D, S)
-        fm = F[ml, mk, :]
-        t0 = time.perf_counter()
-        lrsw.rexii_pole_sum(D, tau, fm, ml, mk, al, c1, c2, g)
-        dt = time.perf_counter() - t0
-        rate = len(ml) * len(g) / dt
-        desc = (f"{len(ml)} sampled Fourier modes x all {len(g)} poles (dense 3x3 LU per mode, "
-                f"2 solves per pole) of the {D}^2 step; {dt:.1f} s")
-        if dt >= seconds or S >= D * D:
-            break
-        S = min(D * D, int(S * max(2.0, min(16.0, seconds / max(dt, 1e-3) * 1.2))))
+    try:
+        while True:
+            ml, mk = inputs.sample_modes(D, S)
+            fm = F[ml, mk, :]
+            t0 = time.perf_counter()
+            lrsw.rexii_pole_sum(D, tau, fm, ml, mk, al, c1, c2, g)
+            dt = time.perf_counter() - t0
+            rate = len(ml) * len(g) / dt
+            desc = (f"{len(ml)} sampled Fourier modes x all {len(g)} poles (dense 3x3 LU per mode, "
+                    f"2 solves per pole) of the {D}^2 step on {cores} thread(s); {dt:.1f} s")
+            if dt >= seconds or S >= D * D:
+                break
+            S = min(D * D, int(S * max(2.0, min(16.0, seconds / max(dt, 1e-3) * 1.2))))
+    finally:
+        lrsw.num_threads(prev)
     return rate, cores, desc, len(g), dt
 
 
@@ -194,12 +209,15 @@ def run_reference(args):
               f"tau={tau} step (dense per-mode LU, naive), {T / args.steps:.3f} s")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * n_poles * D * D / value, "higher_is_better": True,
+            # measured wall time of one timed step (a bounded sample of the workload)
+            "ms_per_step": 1e3 * T / args.steps,
+            # the whole D^2 step at this rate: an extrapolation, not a measurement
+            "full_step_ms_extrapolated": 1e3 * n_poles * D * D / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: LRSW {D}x{D}, tau={tau}, tol={tol}, h=0.5, "
                                    f"{n_poles} poles, {scen} scenario (BASELINE configs[{cidx}])"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -210,11 +228,17 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    import torch
-    import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.backend == "nccl":
+        # communicator evidence: NCCL's INIT lines (rank, nranks, channels / NVLS) on stderr,
+        # so stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    import torch
+    import torch.distributed as dist
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
     if args.backend == "gloo":
@@ -245,9 +269,9 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(timers=None):
         if world > 1:
-            apply_distributed(plan, *f, out=out)
+            apply_distributed(plan, *f, out=out, timers=timers)
         else:
             plan.apply(*f, out=(out[0], out[1], out[2]))
 
@@ -267,6 +291,7 @@ def main():
     plan.timing_read()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    rank_timers = []                       # per step: (start, partial done, all-reduce done)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -274,22 +299,46 @@ def main():
     for i in range(args.steps):
         flush.zero_()                      # L2 flush between timed steps, outside the events
         ev[i][0].record(stream)
-        step()
+        step(rank_timers if world > 1 else None)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clocks.mark()
     if world > 1:
         dist.barrier()
-    ms_local = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_local = sum(step_ms)
     pole_ms, pole_launches, launches = plan.timing_read()
     plan.timing_enable(False)
-    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    # per-step time = max over ranks of that step; the statistic is the median
+    t = torch.tensor(step_ms + [ms_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
+    t = t.tolist()
+    step_max = t[:-1]
+    ms_median = statistics.median(step_max)
+    ms_mean = sum(step_max) / len(step_max)
+    ms_total = t[-1]
     time.sleep(0.25)
     clocks.stop()
     clk = clocks.summary()
+
+    # fp64-pipe peak of this GPU, measured now (the roofline denominator)
+    peak_ops, _ = rexi.fp64_peak(local, reps=5)
+    peak_tflops = 2.0 * peak_ops / 1e12
+
+    # per-rank breakdown (S3 pole kernel, rexi_apply_partial, S4 all-reduce)
+    pole_avg_s = (pole_ms / 1e3) / max(1, pole_launches)
+    mine = {"rank": rank, "poles": [pb, pe], "pole_kernel_ms": pole_avg_s * 1e3,
+            "step_ms_median": statistics.median(step_ms), "fp64_peak_tflops": peak_tflops}
+    if rank_timers:
+        part = [a.elapsed_time(b) for a, b, _ in rank_timers]
+        ar = [b.elapsed_time(c) for _, b, c in rank_timers]
+        mine["apply_partial_ms"] = statistics.median(part)
+        mine["allreduce_ms"] = statistics.median(ar)
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
 
     # ---- end to end through the public API with host buffers (pinned), copies inside
     pinned_in = [torch.from_numpy(x).pin_memory() for x in f_host]
@@ -343,48 +392,46 @@ def main():
         del bin_, bout
 
     units = n_poles * D * D                           # pole·gridpoints per step, whole job
-    value = units * args.steps / (ms_total / 1e3)
-    # roofline of the dominant kernel (the pole kernel) on this rank
+    value = units / (ms_median / 1e3)
+    # roofline of the dominant kernel (the pole kernel) on this rank: algorithmic flops of the
+    # kernel's route (DESIGN.md 6.1 recount) x the pole·gridpoints of one launch / its time
     rank_units = (pe - pb) * D * D
-    pole_avg_s = (pole_ms / 1e3) / max(1, pole_launches)
-    achieved = info["flops_per_pole_mode"] * rank_units / pole_avg_s / 1e12 if pole_avg_s > 0 else None
-    pipe_frac = (info["fp64_ops_per_pole_mode"] * rank_units / pole_avg_s / FP64_PIPE_PEAK_OPS
-                 if pole_avg_s > 0 else None)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "pole_kernel_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            traffic = tj.get(f"{args.config}_{args.variant}")
-        except Exception:
-            traffic = None
+    per_s = rank_units / pole_avg_s if pole_avg_s > 0 else None
+    achieved = info["flops_per_pole_mode"] * per_s / 1e12 if per_s else None
+    pipe_frac = info["fp64_ops_per_pole_mode"] * per_s / peak_ops if per_s else None
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
-            "steps_per_s": args.steps / (ms_total / 1e3),
+            "warmup": args.warmup, "ms_per_step": ms_median,
+            "ms_per_step_mean": ms_mean, "ms_timed_region": ms_total,
+            "statistic": "median over the timed steps of the per-step max over ranks (CUDA events)",
+            "steps_per_s": 1e3 / ms_median,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: LRSW {D}x{D}, tau={tau}, tol={tol}, "
                                    f"h={info['h']:.4g}, M={info['M']}, {n_poles} poles, {scen} scenario "
                                    f"(BASELINE configs[{cidx}])",
-                       "variant": args.variant, "tuning": args.tuning or "default", "l2": "flushed between timed steps (256 MB write)",
+                       "variant": args.variant, "tuning": args.tuning or "default",
+                       "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"poles split over {world} GPU(s)"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
-                         "traffic": traffic, "kernel": "pole_kernel",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tflops,
+                         "unit": "TFLOP/s", "frac": (achieved / peak_tflops) if achieved else None,
+                         "traffic": None,
+                         "traffic_note": "DRAM bytes per launch are an ncu quantity (profiles/r02*_summary.md); "
+                                         "not measurable inside this run",
+                         "kernel": "pole_kernel_r2x (S2+S3)" if args.variant == "pfhx" else "pole_kernel",
                          "flops_per_pole_mode": info["flops_per_pole_mode"],
-                         # SURVEY.md 8(d)'s per-unit figure is the paper's route (~200 flops per
-                         # pole-gridpoint); the kernel's exact rearrangements execute fewer, so the
-                         # roofline uses the kernel's own count and this is reported beside it
-                         "paper_route_flops_per_pole_mode": 200.0,
-                         "paper_route_equiv_tflops": (200.0 * rank_units / pole_avg_s / 1e12
-                                                      if pole_avg_s > 0 else None),
+                         "fp64_ops_per_pole_mode": info["fp64_ops_per_pole_mode"],
+                         "peak_source": "measured in this run: rexi_fp64_peak (DFMA, register operands, "
+                                        "best of 5), x 2 flop per DFMA",
+                         "peak_derived": FP64_PEAK_TFLOPS,
+                         # SURVEY.md 8(d)'s per-unit figure (the paper's Helmholtz route, ~200 flops
+                         # per pole-gridpoint): > 1 means the kernel's route executes fewer flops
+                         "frac_survey_route_200": (200.0 * per_s / 1e12 / peak_tflops) if per_s else None,
                          "fp64_pipe_frac": pipe_frac,
                          "kernel_ms_avg": pole_avg_s * 1e3,
-                         "kernel_share_of_step": (pole_ms / ms_local) if ms_local > 0 else None,
-                         "peak_note": "derived: 148 SM x 64 fp64 FMA/clk x 2 x 1.965 GHz"},
+                         "kernel_share_of_step": (pole_ms / ms_local) if ms_local > 0 else None},
             "clocks": clk,
             "e2e": {"value": units * e2e_n / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": 3 * D * D * 8, "d2h_bytes_per_step": 3 * D * D * 8,
@@ -392,10 +439,19 @@ def main():
                     "single_call_ms_per_step": 1e3 * single_s / e2e_steps},
             "gpu_launches": launches,
         }
+        if world > 1:
+            line["ranks"] = ranks
+            line["comm"] = {"backend": args.backend, "nranks": dist.get_world_size(),
+                            "collective": "all_reduce(sum, fp64) of the 3 real fields, once per step",
+                            "bytes_per_step": 3 * D * D * 8,
+                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                            if args.backend == "nccl" else None}
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, desc, _, _ = oracle_rate(D, tau, tol, scen, args.cpu_seconds)
+            rate1, _, desc1, _, _ = oracle_rate(D, tau, tol, scen, min(5.0, args.cpu_seconds / 2), threads=1)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-                                    "sample": desc}
+                                    "sample": desc, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                                    "value_1core": rate1, "sample_1core": desc1}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

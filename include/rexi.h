@@ -296,6 +296,15 @@ rexi_status_t rexi_timing_enable(rexi_plan_t plan, int enable);
 rexi_status_t rexi_timing_read(rexi_plan_t plan, double *pole_kernel_ms, long *pole_launches,
                                long *total_launches);
 
+/* Measurement (not part of the method): the attainable fp64-pipe rate of `device`, the
+ * roofline denominator of the pole kernel, which is bound by the fp64 ALUs (SURVEY.md 8(d)
+ * "Which roofline bounds the path"). Runs `reps` launches of a DFMA kernel (8 independent
+ * chains per thread, register operands, grid = SMs x 16 x 128 threads) and returns the best
+ * rate in fp64-pipe ops/s (one DFMA = one op = 2 flops) and that launch's time (ms; may be
+ * NULL). Synchronous on the default stream of `device`. EINVAL: ops_per_s NULL or reps < 1;
+ * ECUDA: a CUDA call failed (rexi_last_error). */
+rexi_status_t rexi_fp64_peak(int device, int reps, double *ops_per_s, double *best_ms);
+
 /* Host-only (no GPU needed): the Appendix A table compiled into the library
  * (reading G1): *mu and a[2*(L+1)] = (Re a_l, Im a_l), l = 0..L;
  * returns L (= 24). a may be NULL to query L. */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librexi.so")
-SOURCES = ["planner.cpp", "fit.cpp", "kernels.cu", "capi.cu", "scalar.cu"]
+SOURCES = ["planner.cpp", "fit.cpp", "kernels.cu", "capi.cu", "scalar.cu", "diag.cu"]
 DEPS = SOURCES + ["planner.h", "kernels.cuh", "launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -17,20 +17,37 @@ def pole_partition(n_poles, world_size, rank):
     return (n_poles * rank) // world_size, (n_poles * (rank + 1)) // world_size
 
 
-def pole_parallel_step(partial_fn, n_poles, out, group=None):
+def _event(out):
+    """A timing event recorded on the current stream of out's device (None on CPU)."""
+    import torch
+    if not (hasattr(out, "is_cuda") and out.is_cuda):
+        return None
+    e = torch.cuda.Event(enable_timing=True)
+    e.record(torch.cuda.current_stream(out.device))
+    return e
+
+
+def pole_parallel_step(partial_fn, n_poles, out, group=None, timers=None):
     """Generic S3 + S4: ``partial_fn(begin, end, out)`` writes this rank's partial result
-    into ``out`` (a tensor holding the three fields); then one all-reduce(sum)."""
+    into ``out`` (a tensor holding the three fields); then one all-reduce(sum).
+
+    ``timers`` (optional list): appends (start, partial done, all-reduce done) CUDA events
+    recorded on the current stream (the all-reduce's completion is ordered into it)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     b, e = pole_partition(n_poles, world, rank)
+    e0 = _event(out) if timers is not None else None
     partial_fn(b, e, out)
+    e1 = _event(out) if timers is not None else None
     if world > 1:
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    if timers is not None and e0 is not None:
+        timers.append((e0, e1, _event(out)))
     return out
 
 
-def apply_distributed(plan, eta, u, v, out=None, group=None):
+def apply_distributed(plan, eta, u, v, out=None, group=None, timers=None):
     """One REXII step with the poles split over the ranks of `group` (one GPU per rank).
 
     ``out`` (optional) is a contiguous (3, D, D) float64 CUDA tensor; returns it."""
@@ -41,7 +58,7 @@ def apply_distributed(plan, eta, u, v, out=None, group=None):
     def partial(b, e, buf):
         plan.apply_partial(b, e, eta, u, v, out=(buf[0], buf[1], buf[2]))
 
-    return pole_parallel_step(partial, plan.n_poles, out, group)
+    return pole_parallel_step(partial, plan.n_poles, out, group, timers)
 
 
 def run_distributed(plan, steps, eta, u, v, group=None):

@@ -64,6 +64,7 @@ EXPORTS = {
     "rexi_run": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp, _vp]),
     "rexi_timing_enable": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_timing_read": (ctypes.c_int, [_vp, _dp, _lp, _lp]),
+    "rexi_fp64_peak": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _dp, _dp]),
     "rexi_appendix_a": (ctypes.c_int, [_dp, _dp]),
     "rexi_terms_host": (ctypes.c_long, [ctypes.c_double, ctypes.c_long, ctypes.c_int, _dp, _dp, _dp, _dp]),
     "rexi_h_for_tol": (ctypes.c_double, [ctypes.c_double]),
@@ -149,6 +150,15 @@ def fit_gaussian(L=24, mu=-5.133333333333333, K=200, xmax=100.0):
     if r != 0:
         raise ValueError("bad fit arguments")
     return mu_out.value, a[0::2] + 1j * a[1::2], d.value
+
+
+def fp64_peak(device=0, reps=5):
+    """Measured fp64-pipe rate of `device` (rexi_fp64_peak): (ops/s, best launch ms)."""
+    ops = ctypes.c_double()
+    ms = ctypes.c_double()
+    _check(_lib.rexi_fp64_peak(int(device), int(reps), ctypes.byref(ops), ctypes.byref(ms)),
+           "rexi_fp64_peak")
+    return ops.value, ms.value
 
 
 def abi_version():

@@ -248,6 +248,26 @@ rexi_status_t rexi_forward(rexi_plan_t plan, const double *eta, const double *u,
 rexi_status_t rexi_poles(rexi_plan_t plan, long pole_begin, long pole_end, const double *fhat,
                          double *acc, void *stream);
 
+/* S2+S3 for the spectrum of REAL fields (fhat = rexi_forward output, or any Hermitian spectrum
+ * F(-K) = conj F(K)): writes acc = the spectrum of Re(IDFT(sum_{n in [pole_begin, pole_end)}
+ * Gamma_n [...])), i.e. the Hermitian part (A(K) + conj A(-K)) / 2 of rexi_poles' sum — the
+ * quantity the real part of PAPER.md:434 keeps — computed by the plan's R2C kernel (PFHX by
+ * default: one {K, -K} pair per work item, both Helmholtz solves per pole).
+ * acc is a full D x D spectrum (both modes of every pair written), summable across ranks
+ * (S4 in spectral form) and invertible by rexi_inverse. The R2C kernel reads only one mode of
+ * each pair, so a non-Hermitian fhat gives an unspecified result. fhat and acc must not alias;
+ * ERANGE for a bad range. For the non-R2C variants this is rexi_poles followed by the
+ * Hermitian projection. */
+rexi_status_t rexi_poles_real(rexi_plan_t plan, long pole_begin, long pole_end, const double *fhat,
+                              double *acc, void *stream);
+
+/* S4 helper for the spectral form of the cross-GPU sum: a Hermitian spectrum (F(-K) = conj F(K),
+ * e.g. rexi_poles_real output) is determined by its rows l = 0 .. D/2, which are contiguous per
+ * field ((D/2 + 1) * D complex values at offset field * D * D) — ranks all-reduce only those
+ * (the same bytes as the three real fields). This call rebuilds rows l = D/2 + 1 .. D - 1 in place:
+ * acc(l, k) = conj acc(D - l, (D - k) mod D). Rows 0 and D/2 are not modified. */
+rexi_status_t rexi_hermitian_mirror(rexi_plan_t plan, double *acc, void *stream);
+
 /* S5: eta,u,v = Re(inverse 2-D FFT of acc) (Alg. 1 last line PAPER.md:535). */
 rexi_status_t rexi_inverse(rexi_plan_t plan, const double *acc, double *eta, double *u, double *v,
                            void *stream);

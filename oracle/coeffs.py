@@ -227,9 +227,9 @@ def _windowed(h, M, L, wk_re, wk_im, bre, bim, N):
     return hh * out_re, hh * out_im
 
 
-def rexii_terms(h, M, mu=None, a=None):
-    """The REXII term table (eq:modifiedRexi, eq:REXI_Modified_matrix), N = M + L.
-    Default table: Appendix A; or (mu, a[0..2L]) with a[L + l] = a_l (e.g. a NEXT-2 refit)."""
+def _rexii_terms_ld(h, M, mu=None, a=None):
+    """The REXII term table in extended precision: (L, N, mu_ld, n, c1r, c1i, c2r, c2i, C1r, C1i,
+    C2r, C2i), every array longdouble (eq:modifiedRexi, eq:REXI_Modified_matrix), N = M + L."""
     if mu is None:
         mu_ld, a_re, a_im = appendix_a(LD)
         L = L_APPENDIX_A
@@ -252,10 +252,35 @@ def rexii_terms(h, M, mu=None, a=None):
     C1r = c1r * hh * mu_ld + c2r * hh * n_ld
     C1i = c1i * hh * mu_ld + c2i * hh * n_ld
     C2r, C2i = -c2i, c2r
+    return L, N, mu_ld, n, c1r, c1i, c2r, c2i, C1r, C1i, C2r, C2i
+
+
+def rexii_terms(h, M, mu=None, a=None):
+    """The REXII term table (eq:modifiedRexi, eq:REXI_Modified_matrix), N = M + L, rounded once
+    to fp64. Default table: Appendix A; or (mu, a[0..2L]) with a[L + l] = a_l (e.g. a NEXT-2
+    refit)."""
+    L, N, mu_ld, n, c1r, c1i, c2r, c2i, C1r, C1i, C2r, C2i = _rexii_terms_ld(h, M, mu, a)
+    hh = LD(h)
+    n_ld = n.astype(LD)
     f = lambda r, i: r.astype(np.float64) + 1j * i.astype(np.float64)
     alpha = (float(hh * mu_ld) + 1j * (hh * n_ld).astype(np.float64))
     return RexiiTerms(h=h, M=M, L=L, N=N, mu=float(mu_ld), n=n, alpha=alpha,
                       c1=f(c1r, c1i), c2=f(c2r, c2i), C1=f(C1r, C1i), C2=f(C2r, C2i))
+
+
+def rexii_half_terms_ld(h, M):
+    """Remark 3's half-sum table n = 0..N NOT rounded to fp64: complex
+    longdouble (clongdouble) alpha_n, C_{1,n}, C_{2,n} and Gamma_n — the coefficients of the
+    extended-precision reference lrsw.rexii_pole_sum_ld (test infrastructure, R1)."""
+    L, N, mu_ld, n, c1r, c1i, c2r, c2i, C1r, C1i, C2r, C2i = _rexii_terms_ld(h, M)
+    sel = n >= 0
+    hh = LD(h)
+    CL = np.clongdouble
+    alpha = (hh * mu_ld) + 1j * CL(hh * n[sel].astype(LD))
+    C1 = C1r[sel].astype(CL) + 1j * C1i[sel].astype(CL)
+    C2 = C2r[sel].astype(CL) + 1j * C2i[sel].astype(CL)
+    gamma = np.where(n[sel] == 0, LD(1), LD(2))
+    return n[sel], alpha.astype(CL), C1, C2, gamma
 
 
 @dataclass

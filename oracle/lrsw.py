@@ -128,6 +128,64 @@ def rexii_pole_sum(D, tau, fhat_modes, mode_l, mode_k, alpha, C1, C2, gamma, nyq
     return acc
 
 
+def _solve3_ld(A, r):
+    """x = A^-1 r for a batch of 3x3 complex longdouble systems (A: (m, 3, 3), r: (m, 3)) by
+    Cramer's rule: x_i = det(A with column i replaced by r) / det(A)."""
+    def det(M):
+        return (M[:, 0, 0] * (M[:, 1, 1] * M[:, 2, 2] - M[:, 1, 2] * M[:, 2, 1])
+                - M[:, 0, 1] * (M[:, 1, 0] * M[:, 2, 2] - M[:, 1, 2] * M[:, 2, 0])
+                + M[:, 0, 2] * (M[:, 1, 0] * M[:, 2, 1] - M[:, 1, 1] * M[:, 2, 0]))
+    d = det(A)
+    x = np.empty_like(r)
+    for i in range(3):
+        Ai = A.copy()
+        Ai[:, :, i] = r
+        x[:, i] = det(Ai) / d
+    return x
+
+
+def rexii_pole_sum_ld(D, tau, fhat_modes, mode_l, mode_k, terms_ld, begin=0, end=None):
+    """Extended-precision reference of rexii_pole_sum for poles [begin, end) of the half-sum
+    (test infrastructure: the "long-double truth" of DESIGN.md reading R1). Every quantity is
+    complex longdouble (x87, 64-bit mantissa: 2^11 x the fp64 precision): the unrounded
+    coefficient table (coeffs.rexii_half_terms_ld), the tau-scaled symbols 2 pi k tau (G3,
+    Nyquist zeroed, G2) with pi in longdouble, and per mode and pole the two shifted systems of
+    PAPER.md:429-431 solved by Cramer's rule (not the fp64 oracle's pivoted elimination),
+    accumulated in ascending n as in the display PAPER.md:432-434:
+        acc += Gamma_n [C2_n g1 + (C1_n - C2_n conj(alpha_n)) g2],
+        (alpha_n I + tau A) g1 = f0,  (conj(alpha_n) I - tau A) g2 = g1.
+    fhat_modes: (n_modes, 3) complex; returns (n_modes, 3) clongdouble."""
+    CL, LDt = np.clongdouble, np.longdouble
+    n, alpha, C1, C2, gamma = terms_ld
+    end = len(n) if end is None else end
+    pi = LDt(4) * np.arctan(LDt(1))
+    kk = wavenumbers(D).astype(LDt)
+    sym = LDt(2) * pi * kk * LDt(tau)
+    sym[D // 2] = LDt(0)
+    kx = sym[np.asarray(mode_k)].astype(CL)
+    ky = sym[np.asarray(mode_l)].astype(CL)
+    nm = len(kx)
+    t = CL(LDt(tau))
+    # tau A-hat per mode: [[0, -i kx, -i ky], [-i kx, 0, tau], [-i ky, -tau, 0]]
+    B = np.zeros((nm, 3, 3), dtype=CL)
+    B[:, 0, 1] = -1j * kx
+    B[:, 0, 2] = -1j * ky
+    B[:, 1, 0] = -1j * kx
+    B[:, 2, 0] = -1j * ky
+    B[:, 1, 2] = t
+    B[:, 2, 1] = -t
+    eye = np.eye(3, dtype=CL)[None]
+    f0 = np.asarray(fhat_modes).astype(CL).reshape(-1, 3)
+    acc = np.zeros((nm, 3), dtype=CL)
+    for j in range(begin, end):
+        a = alpha[j]
+        ab = np.conj(a)
+        g1 = _solve3_ld(a * eye + B, f0)
+        g2 = _solve3_ld(ab * eye - B, g1)
+        acc += gamma[j] * (C2[j] * g1 + (C1[j] - C2[j] * ab) * g2)
+    return acc
+
+
 def rexi_pole_sum(D, tau, fhat_modes, mode_l, mode_k, alpha, beta, nyquist_zero=True):
     f = np.ascontiguousarray(fhat_modes, dtype=np.complex128).reshape(-1, 3)
     nm = f.shape[0]

@@ -798,6 +798,33 @@ rexi_status_t rexi_poles(rexi_plan_t p, long b, long e, const double *fhat, doub
     });
 }
 
+rexi_status_t rexi_poles_real(rexi_plan_t p, long b, long e, const double *fhat, double *acc, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!fhat || !acc) return fail(REXI_EINVAL, "null pointer");
+        if (fhat == acc) return fail(REXI_EINVAL, "fhat and acc must not alias");
+        rexi_status_t s = check_range(p, b, e);
+        if (s != REXI_OK) return s;
+        const cudaStream_t st = (cudaStream_t)stream;
+        const cd *in = reinterpret_cast<const cd *>(fhat);
+        cd *out = reinterpret_cast<cd *>(acc);
+        if (p->kind() >= 6) return do_poles(p, b, e, in, out, st, true);   // R2C: Hermitian already
+        // generic kernels: the complex pole sum, then its Hermitian part (the spectral Re)
+        if ((s = do_poles(p, b, e, in, p->d_tmp, st, true)) != REXI_OK) return s;
+        CK(rexi::launch_hermitian(p->d_tmp, out, p->n_modes, p->host.D, st));
+        p->launches += 1;
+        return REXI_OK;
+    });
+}
+
+rexi_status_t rexi_hermitian_mirror(rexi_plan_t p, double *acc, void *stream) {
+    return guarded(p, [&]() -> rexi_status_t {
+        if (!acc) return fail(REXI_EINVAL, "null pointer");
+        CK(rexi::launch_mirror_rows(reinterpret_cast<cd *>(acc), p->n_modes, p->host.D, (cudaStream_t)stream));
+        p->launches += 1;
+        return REXI_OK;
+    });
+}
+
 rexi_status_t rexi_inverse(rexi_plan_t p, const double *acc, double *eta, double *u, double *v,
                            void *stream) {
     return guarded(p, [&]() -> rexi_status_t {

@@ -1559,6 +1559,28 @@ cudaError_t launch_finish(const FinishArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Rows l = D/2 + 1 .. D - 1 of a Hermitian spectrum from rows 1 .. D/2 - 1: F(l, k) =
+// conj F(D - l, (D - k) mod D). One thread per (field, mirrored mode); rows 0 and D/2 are
+// self-mirror rows and are left as they are.
+__global__ void __launch_bounds__(256) mirror_rows_kernel(cd *__restrict__ acc, long n_modes, int D, int log2D) {
+    const long per = (long)(D / 2 - 1) << log2D;   // mirrored modes per field
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 3 * per) return;
+    const int f = (int)(t / per);
+    const long r = t - (long)f * per;
+    const int l = D / 2 + 1 + (int)(r >> log2D), k = (int)(r & (D - 1));
+    const long src = ((long)(D - l) << log2D) + ((D - k) & (D - 1));
+    const cd x = acc[f * n_modes + src];
+    acc[f * n_modes + ((long)l << log2D) + k] = mk(x.x, -x.y);
+}
+
+cudaError_t launch_mirror_rows(cd *acc, long n_modes, int D, cudaStream_t st) {
+    const long work = 3L * (D / 2 - 1) * D;
+    if (work <= 0) return cudaSuccess;
+    mirror_rows_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(acc, n_modes, D, ilog2(D));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st) {
     hermitian_kernel<<<(unsigned)((n_modes + 255) / 256), 256, 0, st>>>(in, out, n_modes, D, ilog2(D));
     return cudaGetLastError();

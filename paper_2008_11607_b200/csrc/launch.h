@@ -38,6 +38,8 @@ long sk_slots_bound(long tiles, long poles, long ctas);
 cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
+// rows D/2+1 .. D-1 of a Hermitian spectrum from rows 1 .. D/2-1 (in place)
+cudaError_t launch_mirror_rows(cd *acc, long n_modes, int D, cudaStream_t st);
 
 // Algorithmic work of the pole kernel per (pole, Fourier mode), counted from its source:
 // flops (FMA = 2, MUL/ADD = 1) and fp64-pipe instructions (FMA/MUL/ADD = 1 each), by kind.

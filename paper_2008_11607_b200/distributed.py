@@ -61,15 +61,40 @@ def apply_distributed(plan, eta, u, v, out=None, group=None, timers=None):
     return pole_parallel_step(partial, plan.n_poles, out, group, timers)
 
 
-def run_distributed(plan, steps, eta, u, v, group=None):
+def run_distributed(plan, steps, eta, u, v, group=None, spectral=False):
     """`steps` REXII steps in place (S6, T_final = steps * tau) with every step's poles split
-    over the ranks of `group`: per step one pole-parallel `apply_distributed` (its own
-    all-reduce), the summed fields becoming the next step's input. Returns (eta, u, v)."""
+    over the ranks of `group`. Returns (eta, u, v).
+
+    spectral=False: per step one pole-parallel `apply_distributed` (S1, the rank's poles, S5,
+    all-reduce of the three real fields), the summed fields becoming the next step's input.
+    spectral=True (spectral-resident, NEXT-4): S1 once; per step every rank evaluates its poles
+    on the shared Hermitian spectrum (rexi_poles_real), the ranks all-reduce the spectrum's rows
+    l = 0 .. D/2 (per field; the same bytes as the real fields) and rebuild the other rows by
+    Hermitian symmetry (rexi_hermitian_mirror) — the next step's input; S5 once at the end. The
+    real part of each step is the Hermitian projection the R2C kernel applies, so
+    this equals the physical-space loop up to rounding, without two FFTs per step."""
     import torch
-    buf = torch.empty((3, plan.D, plan.D), dtype=torch.float64, device=eta.device)
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if not spectral:
+        buf = torch.empty((3, plan.D, plan.D), dtype=torch.float64, device=eta.device)
+        for _ in range(int(steps)):
+            apply_distributed(plan, eta, u, v, out=buf, group=group)
+            eta.copy_(buf[0])
+            u.copy_(buf[1])
+            v.copy_(buf[2])
+        return eta, u, v
+    b, e = pole_partition(plan.n_poles, world, rank)
+    fhat = plan.forward(eta, u, v)
+    acc = torch.empty_like(fhat)
+    half = plan.D // 2 + 1
     for _ in range(int(steps)):
-        apply_distributed(plan, eta, u, v, out=buf, group=group)
-        eta.copy_(buf[0])
-        u.copy_(buf[1])
-        v.copy_(buf[2])
+        plan.poles_real(fhat, b, e, acc=acc)
+        if world > 1:
+            for c in range(3):
+                dist.all_reduce(acc[c, :half], op=dist.ReduceOp.SUM, group=group)
+        plan.hermitian_mirror(acc)
+        fhat, acc = acc, fhat
+    plan.inverse(fhat, out=(eta, u, v))
     return eta, u, v

@@ -85,3 +85,12 @@ def sample_modes(D, n, seed=PARITY_SEED):
                     break
         flat = np.array(sorted(pick))
     return (flat // D).astype(np.int32), (flat % D).astype(np.int32)
+
+
+def spectral_hermitian(D, seed=PARITY_SEED):
+    """Seeded Hermitian spectra (3, D, D): F(K) = (Z(K) + conj Z(-K)) / 2 for the complex white
+    spectra Z of spectral_white, so F(-K) = conj F(K) exactly (the spectrum of real fields,
+    input of rexi_poles_real) — without a transform (no O(D^3) DFT at large D)."""
+    Z = spectral_white(D, seed)
+    j = (-np.arange(D)) % D
+    return 0.5 * (Z + np.conj(Z[:, j][:, :, j]))

@@ -55,6 +55,8 @@ EXPORTS = {
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "rexi_poles": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp]),
+    "rexi_poles_real": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp]),
+    "rexi_hermitian_mirror": (ctypes.c_int, [_vp, _vp, _vp]),
     "rexi_inverse": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "rexi_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rexi_apply_partial": (ctypes.c_int, [_vp, ctypes.c_long, ctypes.c_long, _vp, _vp, _vp,
@@ -304,6 +306,20 @@ class Plan:
         acc = self._new_spec() if acc is None else acc
         _check(_lib.rexi_poles(self._h, int(begin), int(end), self._spec(fhat, "fhat"),
                                self._spec(acc, "acc"), self._stream()), "rexi_poles")
+        return acc
+
+    def poles_real(self, fhat, begin=0, end=None, acc=None):
+        """rexi_poles_real: the Hermitian part of the pole sum for the spectrum of real fields."""
+        end = self.n_poles if end is None else end
+        acc = self._new_spec() if acc is None else acc
+        _check(_lib.rexi_poles_real(self._h, int(begin), int(end), self._spec(fhat, "fhat"),
+                                    self._spec(acc, "acc"), self._stream()), "rexi_poles_real")
+        return acc
+
+    def hermitian_mirror(self, acc):
+        """rexi_hermitian_mirror: rows D/2+1 .. D-1 of a Hermitian spectrum from rows 1 .. D/2-1."""
+        _check(_lib.rexi_hermitian_mirror(self._h, self._spec(acc, "acc"), self._stream()),
+               "rexi_hermitian_mirror")
         return acc
 
     def inverse(self, acc, out=None):

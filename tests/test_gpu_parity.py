@@ -323,18 +323,37 @@ def test_schedule_errors(R):
     assert p.info["schedule"] == 0 and p.info["last_schedule"] == 0
 
 
-def test_run_distributed_single_rank_matches_run(R):
-    """distributed.run_distributed (per-step pole split + all-reduce; one rank here) equals the
-    spectral-resident rexi_run up to rounding."""
+@pytest.mark.parametrize("spectral", [False, True])
+@pytest.mark.parametrize("variant", ["pfhx", "pfh"])
+def test_run_distributed_single_rank_matches_run(R, spectral, variant):
+    """distributed.run_distributed (per-step pole split + all-reduce; one rank here), in
+    physical or spectral-resident form, equals rexi_run up to rounding, and the oracle's steps."""
     from paper_2008_11607_b200.distributed import run_distributed
     D, tau = 32, 0.7
     f = inputs.white_noise(D, seed=31)
-    p = R.Plan(D, tau)
+    p = R.Plan(D, tau, variant=variant)
     a = [dev(x) for x in f]
     b = [dev(x) for x in f]
     p.run(3, *a)
-    run_distributed(p, 3, *b)
+    run_distributed(p, 3, *b, spectral=spectral)
     assert rel_l2([host(x) for x in b], [host(x) for x in a]) < 1e-13
+    g = f
+    for _ in range(3):
+        g = lrsw.rexii_step(*g, tau, p.info["h"], p.info["M"])
+    assert rel_l2([host(x) for x in b], g) < TOL
+
+
+@pytest.mark.parametrize("D", [4, 8, 64])
+def test_hermitian_mirror(R, D):
+    """rexi_hermitian_mirror rebuilds rows D/2+1 .. D-1 of a Hermitian spectrum exactly and
+    leaves rows 0 .. D/2 untouched."""
+    import torch
+    F = inputs.spectral_hermitian(D, seed=2)
+    p = R.Plan(D, 0.5)
+    t = dev(F)
+    t[:, D // 2 + 1:] = 0
+    got = host(p.hermitian_mirror(t))
+    assert np.array_equal(got, F)
 
 
 def test_variants_agree(R):

@@ -228,3 +228,47 @@ def test_white_noise_accuracy_tol(oracle_lib):
         M = C.M_lrsw(D, tau, h, tol)
         f = inputs.white_noise(D)
         assert rel_l2(lrsw.rexii_step(*f, tau, h, M), lrsw.exact_step(*f, tau)) < tol
+
+
+def test_ld_pole_sum_pins():
+    """The extended-precision reference (lrsw.rexii_pole_sum_ld, reading R1) against what the
+    mathematics fixes: (a) for a Hermitian spectrum its full half-sum's Hermitian part is the
+    exact per-mode propagator e^{tau A-hat} f(K) (closed-form eigen-decomposition) within the
+    REXII error of the m0 = 11 rule (~1e-14); (b) it agrees with the fp64
+    oracle (pivoted elimination, a different algorithm) to fp64 rounding, on the full sum and on
+    a pole sub-range; (c) pole-range additivity."""
+    from paper_2008_11607_b200 import inputs
+    D, tau, h = 16, 1.0, 0.5
+    M = C.M_lrsw(D, tau, h, 1e-16)
+    tl = C.rexii_half_terms_ld(h, M)
+    t = C.rexii_terms(h, M).half()
+    F = inputs.spectral_hermitian(D, seed=3)
+    ml, mk = lrsw.all_modes(D)
+    fm = np.stack([F[c][ml, mk] for c in range(3)], -1)
+    mlm, mkm = (-ml) % D, (-mk) % D
+    fmm = np.stack([F[c][mlm, mkm] for c in range(3)], -1)
+    A = lrsw.rexii_pole_sum_ld(D, tau, fm, ml, mk, tl).astype(np.complex128)
+    Am = lrsw.rexii_pole_sum_ld(D, tau, fmm, mlm, mkm, tl).astype(np.complex128)
+    herm = (A + np.conj(Am)) / 2
+    K = lrsw.symbols(D, tau)
+    E = lrsw.exact_propagator_modes(K[mk], K[ml], tau)
+    ex = np.einsum("mij,mj->mi", E, fm)
+    assert np.linalg.norm(herm - ex) / np.linalg.norm(ex) < 1e-13
+    # (b) vs the fp64 oracle: full sum and the sub-range [40, 77)
+    ref = lrsw.rexii_pole_sum(D, tau, fm, ml, mk, *t[1:])
+    assert np.linalg.norm(A - ref) / np.linalg.norm(ref) < 1e-13
+    sub = lrsw.rexii_pole_sum_ld(D, tau, fm, ml, mk, tl, 40, 77).astype(np.complex128)
+    ref_sub = lrsw.rexii_pole_sum(D, tau, fm, ml, mk, *(x[40:77] for x in t[1:]))
+    assert np.linalg.norm(sub - ref_sub) / np.linalg.norm(ref_sub) < 1e-12
+    # (c) additivity over a partition of the poles
+    lo = lrsw.rexii_pole_sum_ld(D, tau, fm, ml, mk, tl, 0, 40).astype(np.complex128)
+    hi = lrsw.rexii_pole_sum_ld(D, tau, fm, ml, mk, tl, 77, None).astype(np.complex128)
+    assert np.linalg.norm(lo + sub + hi - A) / np.linalg.norm(A) < 1e-15
+
+
+def test_spectral_hermitian_input_is_hermitian():
+    from paper_2008_11607_b200 import inputs
+    D = 8
+    F = inputs.spectral_hermitian(D, seed=1)
+    j = (-np.arange(D)) % D
+    assert np.array_equal(F, np.conj(F[:, j][:, :, j]))

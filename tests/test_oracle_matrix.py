@@ -55,4 +55,12 @@ def test_fig2c_rexie_shift_A2():
     M = C.M_rule(2450.0, 0.5)
     assert X.rel_l2(X.rexie_matrix(A2, f, 1.0, 0.5, M, nu=-2450j), ex) < 1e-11
     assert X.rel_l2(X.rexie_matrix(A2, f, 1.0, 0.5, M - 50, nu=-2450j), ex) > 1e-3
-    assert X.rel_l2(X.rexie_matrix(A2, f, 1.0, 0.5, M, nu=0.0), ex) > 1e-6
+    # without the shift the same M covers only |lambda| <= (M - 11) h = 2450 of the spectrum
+    # i[-4900, 0] (eq:matrixAccuracyBound): beyond it R(x) ~ 0, so the error is the part of f0
+    # on the eigenvectors with |lambda| > 2450 (A_2 is normal: e^{A_2} is unitary)
+    H = (A2 / 1j).real                      # A_2 = i H, H real symmetric
+    w, V = np.linalg.eigh(H)
+    c = V.T @ f
+    tail = np.linalg.norm(c[np.abs(w) > 2450.0]) / np.linalg.norm(c)
+    err0 = X.rel_l2(X.rexie_matrix(A2, f, 1.0, 0.5, M, nu=0.0), ex)
+    assert tail > 1e-6 and abs(err0 - tail) < 1e-3 * tail, (err0, tail)

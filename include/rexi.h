@@ -201,24 +201,32 @@ rexi_status_t rexi_plan_set_table(rexi_plan_t plan, int L, double mu, const doub
 rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int poles_per_iter,
                                    int min_blocks_per_sm);
 
-/* How the R2C pole kernel (REXII PFHR, modes_per_thread 8, real-input calls) distributes its
- * (item tile x pole) iterations over the GPU:
+/* How a step is scheduled on the GPU. For the R2C pole kernels (PFHR / PFHX, real-input calls):
  *  REXI_SCHEDULE_CHUNKED: grid = (tiles, pole chunks), chunk count chosen to fill whole waves of
  *                         resident blocks; one partial sum per chunk.
  *  REXI_SCHEDULE_STREAMK: a persistent grid of one 256-thread block per SM splits the
  *                         iteration space evenly (no wave tail); one partial per tile segment.
- *  REXI_SCHEDULE_AUTO:    CHUNKED (default). With octet items every block costs the same, so
- *                         the chunked waves are already balanced, and two 128-thread blocks per
- *                         SM issue at least as well as one 256-thread block: measured on B200
- *                         the chunked pole kernel is 0.5-7 % faster across the kernel versions
- *                         (default kernel: C2 0.870 vs 0.874 ms).
+ *                         (PFHR only.)
+ *  REXI_SCHEDULE_FUSED:   the whole physical step S1..S5 (rexi_apply / apply_partial /
+ *                         apply_host) as ONE launch of a thread-block cluster (16 CTAs, or 8):
+ *                         FFT passes, PFHX pole loop, K = 0 corners, finish and inverse FFT
+ *                         separated by cluster barriers, intermediates in L2 (kernels.cu "fused
+ *                         small-grid step"). PFHX plans with D <= 128 only (else CHUNKED).
+ *  REXI_SCHEDULE_AUTO:    FUSED for PFHX steps with D <= 128 and a small pole range (octet items
+ *                         x poles <= 2^18: the cluster's 16 SMs finish the poles sooner than the
+ *                         seven launches of the chunked path would), CHUNKED otherwise (default).
+ *                         With octet items every block costs the same, so the chunked waves are
+ *                         already balanced, and two 128-thread blocks per SM issue at least as
+ *                         well as one 256-thread block: measured on B200 the chunked pole kernel
+ *                         is 0.5-7 % faster than STREAMK across the kernel versions.
  * STREAMK falls back to CHUNKED when the segment partials do not fit the partial buffer. The
- * kernels of every other variant are always chunked. Schedules differ only in the summation order of the pole sum. Clears the
- * plan's graph cache. EINVAL for an unknown schedule. */
+ * kernels of every other variant are always chunked. Schedules differ only in the summation
+ * order of the pole sum. Clears the plan's graph cache. EINVAL for an unknown schedule. */
 typedef enum {
     REXI_SCHEDULE_AUTO = 0,
     REXI_SCHEDULE_CHUNKED = 1,
-    REXI_SCHEDULE_STREAMK = 2
+    REXI_SCHEDULE_STREAMK = 2,
+    REXI_SCHEDULE_FUSED = 3
 } rexi_schedule_t;
 rexi_status_t rexi_plan_set_schedule(rexi_plan_t plan, int schedule);
 
@@ -382,6 +390,25 @@ long rexi_scalar_plan_terms(rexi_scalar_plan_t plan);
 rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t plan, int method, long n, const double *x,
                                 const double *in, double *out, double phase_re, double phase_im,
                                 void *stream);
+
+/* NEXT-3 on the library's own transforms and pole kernel: out ~ e^{tau A} f for a CIRCULANT
+ * n x n matrix A (first column `col`), e.g. the finite-difference test matrices A_1 (advection)
+ * and A_2 (Schroedinger, shift nu = -2450 i) of Sec. 3.2 (Fig. 2). A circulant
+ * is diagonalised by the DFT — A = F^-1 diag(F col) F, eq:AisVEV with V = F^-1 —
+ * so, with the DFT kernels of the library (radix-8 Stockham passes for power-of-two n <= 2048, a
+ * direct DFT for other n such as the paper's n = 70):
+ *   1. lambda = DFT(col), fh = DFT(f);
+ *   2. x_j = Im(tau (lambda_j - nu)) (A's eigenvalues are purely imaginary), and
+ *      oh_j = e^{tau nu} r(i x_j) fh_j by the scalar pole kernel of rexi_scalar_apply with `method`
+ *      (REXII; REXI = REXIE per eigenvalue; REXI_M = the eigen-coordinates of eq:originalREXImatrix,
+ *      whose Re the caller takes for a real A, f); Remark 1's shift nu;
+ *   3. out = DFT^-1(oh).
+ * col, f, out: device arrays of n complex values (interleaved re, im); out must not alias col or
+ * f. Stream-ordered (scratch from cudaMallocAsync on `stream`). EINVAL: null plan / pointer,
+ * n < 1 or n > 2^20, unknown method, non-finite tau or nu; ECUDA: a CUDA call failed. */
+rexi_status_t rexi_circulant_apply(rexi_scalar_plan_t plan, int method, long n, const double *col,
+                                   const double *f, double *out, double tau, double nu_re,
+                                   double nu_im, void *stream);
 
 const char *rexi_status_string(rexi_status_t status);
 const char *rexi_last_error(void);

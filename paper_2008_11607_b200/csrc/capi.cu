@@ -309,6 +309,8 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     a.hmu = p->host.poles[0].ar;
     a.sk_tiles = sk_tiles;
     a.sk_slots = sk_slots;
+    a.partial_cap = 3 * n * (long)p->max_chunks;
+    a.n_poles = p->host.n_poles;
     rexi_status_t s;
     const bool fork = (kd == 6 || kd == 7);
     if (fork) {
@@ -370,6 +372,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     f.sk_slots = sk_slots;
     f.sk_ctas = sk_ctas;
     f.sk_poles = e - b;
+    f.partial_cap = 3 * n * (long)p->max_chunks;
     if (sk_tiles) CK(rexi::launch_finish_r2c_sk(f, st));
     else CK(rexi::launch_finish(f, st));
     p->launches += 2;
@@ -414,8 +417,128 @@ rexi_status_t guarded(rexi_plan_t p, F &&f) {
     }
 }
 
+// Pole-range sums used by the finish / fix-up kernels: S = sum (w1/alpha + w2/|alpha|^2) and
+// Sd = sum w1 over [b, e), from the planner's extended-precision prefix sums.
+void range_sums(const rexi_plan_s *p, long b, long e, cd *S, cd *Sd) {
+    const long double sr = p->host.spre_re[(size_t)e] - p->host.spre_re[(size_t)b];
+    const long double si = p->host.spre_im[(size_t)e] - p->host.spre_im[(size_t)b];
+    *S = cd{(double)sr, (double)si};
+    const long double wr = p->host.wpre_re[(size_t)e] - p->host.wpre_re[(size_t)b];
+    const long double wi = p->host.wpre_im[(size_t)e] - p->host.wpre_im[(size_t)b];
+    *Sd = cd{(double)wr, (double)wi};
+}
+
+// The fused small-grid step (REXI_SCHEDULE_FUSED / AUTO, include/rexi.h): PFHX kind, D <= 128,
+// a non-empty pole range, cluster launch available; under AUTO only for small pole work.
+constexpr long kSmallWorkMax = 1L << 18;   // octet items x poles
+bool small_eligible(const rexi_plan_s *p, long b, long e) {
+    if (p->kind() != 7 || e <= b || p->host.D > 128) return false;
+    if (p->schedule != REXI_SCHEDULE_FUSED && p->schedule != REXI_SCHEDULE_AUTO) return false;
+    if (p->schedule == REXI_SCHEDULE_AUTO && rexi::small_step_items(p->host.D) * (e - b) > kSmallWorkMax)
+        return false;
+    // AUTO falls back to the multi-launch path without a cluster launch; an explicit FUSED
+    // request then fails in do_step_small (no silent change of schedule)
+    return p->schedule == REXI_SCHEDULE_FUSED || rexi::small_step_cluster() > 0;
+}
+
+rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
+                            const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+    const int cs = rexi::small_step_cluster();
+    if (cs <= 0) return fail(REXI_ECUDA, "fused small-grid step: thread-block cluster launch unavailable");
+    const long n = p->n_modes;
+    const int D = p->host.D;
+    const long items = rexi::small_step_items(D);
+    const long W = (long)cs * rexi::kSmallThreadsHost - 128;   // pole workers (kernels.cu)
+    long chunks = std::min(e - b, std::max(1L, W / items));
+    chunks = std::max(1L, std::min(chunks, (long)p->max_chunks));
+    cd S, Sd;
+    range_sums(p, b, e, &S, &Sd);
+    rexi::SmallArgs a;
+    a.in[0] = eta; a.in[1] = u; a.in[2] = v;
+    a.out[0] = eo; a.out[1] = uo; a.out[2] = vo;
+    a.half = p->d_tmp;
+    a.tw = p->d_tw;
+    a.scale = 1.0 / ((double)D * (double)D);
+    a.n_items = items;
+    rexi::PoleArgs &q = a.pole;
+    q = rexi::PoleArgs{};
+    q.fhat = p->d_fhat;
+    q.partial = p->d_partial;
+    q.poles = p->d_poles;
+    q.rpoles = p->d_rpoles;
+    q.xpoles = p->d_xpoles;
+    q.ksym = p->d_ksym;
+    q.pole_begin = b;
+    q.pole_end = e;
+    q.n_modes = n;
+    q.n_chunks = (int)chunks;
+    q.D = D;
+    q.log2D = 0;
+    while ((1 << q.log2D) < D) ++q.log2D;
+    q.tau = p->host.tau;
+    q.hmu = p->host.poles[0].ar;
+    q.partial_cap = 3 * n * (long)p->max_chunks;
+    q.n_poles = p->host.n_poles;
+    rexi::FinishArgs &f = a.fin;
+    f = rexi::FinishArgs{};
+    f.partial = p->d_partial;
+    f.acc = p->d_acc;
+    f.fhat = p->d_fhat;
+    f.ksym = p->d_ksym;
+    f.n_modes = n;
+    f.n_chunks = (int)chunks;
+    f.D = D;
+    f.log2D = q.log2D;
+    f.kind = 7;
+    f.tau = p->host.tau;
+    f.S = S;
+    f.Sd = Sd;
+    f.partial_cap = q.partial_cap;
+    rexi::FixupArgs &x = a.fix;
+    x.method = p->method;
+    x.write_eta = 1;
+    x.S = S;
+    x.fhat = p->d_fhat;
+    x.acc = p->d_acc;
+    x.poles = p->d_poles;
+    x.pole_begin = b;
+    x.pole_end = e;
+    x.n_modes = n;
+    x.D = D;
+    rexi_status_t s;
+    if ((s = record(p, st, true)) != REXI_OK) return s;
+    CK(rexi::launch_step_small(a, cs, st));
+    if ((s = record(p, st, false)) != REXI_OK) return s;
+    p->pole_launches += 1;
+    p->launches += 1;
+    p->last_schedule = REXI_SCHEDULE_FUSED;
+    return REXI_OK;
+}
+
+// REXI_CHECKED builds: every workspace array a step writes before reading is filled with NaN
+// first, so a read of a slot the step did not write shows up in the result (checked tests).
+rexi_status_t poison_workspace(rexi_plan_s *p, cudaStream_t st, bool fhat) {
+#ifdef REXI_CHECKED
+    const size_t field = sizeof(cd) * 3 * (size_t)p->n_modes;
+    CK(cudaMemsetAsync(p->d_tmp, 0xFF, field, st));
+    CK(cudaMemsetAsync(p->d_acc, 0xFF, field, st));
+    CK(cudaMemsetAsync(p->d_partial, 0xFF, field * (size_t)p->max_chunks, st));
+    if (fhat) CK(cudaMemsetAsync(p->d_fhat, 0xFF, field, st));
+#else
+    (void)p;
+    (void)st;
+    (void)fhat;
+#endif
+    return REXI_OK;
+}
+
 rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
                              const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+    {
+        rexi_status_t s0 = poison_workspace(p, st, true);
+        if (s0 != REXI_OK) return s0;
+    }
+    if (small_eligible(p, b, e)) return do_step_small(p, b, e, eta, u, v, eo, uo, vo, st);
     rexi_status_t s;
     if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
     if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
@@ -425,6 +548,7 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
 // One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
 rexi_status_t do_spectral_step_direct(rexi_plan_s *p, long b, long e, cudaStream_t st) {
     rexi_status_t s;
+    if ((s = poison_workspace(p, st, false)) != REXI_OK) return s;
     if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
     CK(rexi::launch_hermitian(p->d_acc, p->d_fhat, p->n_modes, p->host.D, st));
     p->launches += 1;
@@ -760,7 +884,8 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t p, int modes_per_thread, int pole
 
 rexi_status_t rexi_plan_set_schedule(rexi_plan_t p, int schedule) {
     if (!p) return fail(REXI_EINVAL, "null plan");
-    if (schedule != REXI_SCHEDULE_AUTO && schedule != REXI_SCHEDULE_CHUNKED && schedule != REXI_SCHEDULE_STREAMK)
+    if (schedule != REXI_SCHEDULE_AUTO && schedule != REXI_SCHEDULE_CHUNKED && schedule != REXI_SCHEDULE_STREAMK &&
+        schedule != REXI_SCHEDULE_FUSED)
         return fail(REXI_EINVAL, "unknown schedule");
     DeviceGuard g(p->device);
     p->schedule = schedule;

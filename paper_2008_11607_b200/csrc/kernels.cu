@@ -14,6 +14,10 @@
 //  * fixup_k0_kernel                  : the K = 0 modes (velocities decouple from delta, zeta
 //    there): pure Coriolis 2x2 solves per pole.
 //  * hermitian_kernel                 : the spectral form of Re(.) between rexi_run steps.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "launch.h"
 
@@ -107,24 +111,43 @@ __device__ __forceinline__ void pass_twiddles(const cd *__restrict__ tw, int ste
     }
 }
 
+// The block's dynamic shared memory (all FFT kernels keep their transforms there).
+__device__ __forceinline__ cd *rx_smem_base() {
+    extern __shared__ cd rx_dyn_smem[];
+    return rx_dyn_smem;
+}
+
+// REXI_CHECKED: fill the block's dynamic shared memory with NaN first, so a read of a slot the
+// kernel never wrote propagates into the result (compared with the oracle by the checked tests).
+__device__ __forceinline__ void rx_poison_smem() {
+#ifdef REXI_CHECKED
+    cd *b = rx_smem_base();
+    const int n = (int)(dyn_smem_bytes() / sizeof(cd));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = mk(__longlong_as_double(-1LL), __longlong_as_double(-1LL));
+    __syncthreads();
+#endif
+}
+
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
 template <int R, bool INV>
 __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, int t, int tf,
-                                              const cd *__restrict__ tw) {
+                                              const cd *__restrict__ tw, bool act = true) {
     constexpr int PERMAX = 8 / R;
     const int nbf = N / R;
     cd v[8];
 #pragma unroll
     for (int b = 0; b < PERMAX; ++b) {
         const int j = t + b * tf;
-        if (b * tf < nbf && j < nbf) {
+        if (act && b * tf < nbf && j < nbf) {
             const int k = j & (Ns - 1);
             const int step = k * (N / (Ns * R));  // twiddle index step: r * k * N / (Ns R)
             cd w[R];
             if (Ns > 1) pass_twiddles<R, INV>(tw, step, w);
+            RX_ASSERT(Ns == 1 || R * step < N);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+                RX_SMEM((s - rx_smem_base()) + pidx(j + r * nbf));
                 cd x = s[pidx(j + r * nbf)];
                 if (r > 0 && Ns > 1) x = cmul(x, w[r]);
                 v[b * R + r] = x;
@@ -135,27 +158,33 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
 #pragma unroll
     for (int b = 0; b < PERMAX; ++b) {
         const int j = t + b * tf;
-        if (b * tf < nbf && j < nbf) {
+        if (act && b * tf < nbf && j < nbf) {
             dftR<R, INV>(v + b * R);
             const int k = j & (Ns - 1);
             const int d = (j - k) * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) s[pidx(d + r * Ns)] = v[b * R + r];
+            for (int r = 0; r < R; ++r) {
+                RX_SMEM((s - rx_smem_base()) + pidx(d + r * Ns));
+                s[pidx(d + r * Ns)] = v[b * R + r];
+            }
         }
     }
     __syncthreads();
 }
 
+// act = false: the thread only joins the block barriers (blocks with more threads than
+// transforms x tf, e.g. the fused small-grid step)
 template <bool INV>
-__device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw) {
+__device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw,
+                                            bool act = true) {
     int Ns = 1, rem = logN;
     while (rem >= 3) {
-        stockham_pass<8, INV>(s, N, logN, Ns, t, tf, tw);
+        stockham_pass<8, INV>(s, N, logN, Ns, t, tf, tw, act);
         Ns <<= 3;
         rem -= 3;
     }
-    if (rem == 2) stockham_pass<4, INV>(s, N, logN, Ns, t, tf, tw);
-    else if (rem == 1) stockham_pass<2, INV>(s, N, logN, Ns, t, tf, tw);
+    if (rem == 2) stockham_pass<4, INV>(s, N, logN, Ns, t, tf, tw, act);
+    else if (rem == 1) stockham_pass<2, INV>(s, N, logN, Ns, t, tf, tw, act);
 }
 
 // ----------------------------------------------------------------------------- real 2-D FFT
@@ -185,6 +214,7 @@ __global__ void __launch_bounds__(1024) fft_rows_fwd_kernel(FftArgs a) {
     const double *inp = static_cast<const double *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *outp = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int PL = padded_len(D);
+    rx_poison_smem();
     cd tmp[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -192,13 +222,17 @@ __global__ void __launch_bounds__(1024) fft_rows_fwd_kernel(FftArgs a) {
         if (i < n) {
             const int pr = i >> log2D, x = i & (D - 1);
             const size_t g = (2 * (pair0 + pr)) * D + x;
+            RX_ASSERT(g + D < (size_t)D * D);
             tmp[q] = mk(__ldg(inp + g), __ldg(inp + g + D));
         }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) smem[(i >> log2D) * PL + pidx(i & (D - 1))] = tmp[q];
+        if (i < n) {
+            RX_SMEM((i >> log2D) * PL + pidx(i & (D - 1)));
+            smem[(i >> log2D) * PL + pidx(i & (D - 1))] = tmp[q];
+        }
     }
     __syncthreads();
     const int row = threadIdx.x / tf, t = threadIdx.x - row * tf;
@@ -220,6 +254,7 @@ __global__ void __launch_bounds__(1024) fft_rows_fwd_kernel(FftArgs a) {
             X2 = mk(hs * (zk.y + zm.y), hs * (zm.x - zk.x));
         }
         const size_t g = (2 * (pair0 + pr)) * D + k;
+        RX_ASSERT(g + D < (size_t)D * D && k < H);
         outp[g] = X1;
         outp[g + D] = X2;
     }
@@ -238,16 +273,23 @@ __global__ void __launch_bounds__(1024) fft_cols_fwd_kernel(FftArgs a) {
     const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int n = C << log2D;
+    rx_poison_smem();
     cd tmp[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) tmp[q] = in[(size_t)(i >> logC) * D + col0 + (i & (C - 1))];
+        if (i < n) {
+            RX_ASSERT(col0 + (i & (C - 1)) < (D >> 1) && (i >> logC) < D);
+            tmp[q] = in[(size_t)(i >> logC) * D + col0 + (i & (C - 1))];
+        }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
+        if (i < n) {
+            RX_SMEM((i & (C - 1)) * stride + pidx(i >> logC));
+            smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
+        }
     }
     __syncthreads();
     const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
@@ -257,6 +299,7 @@ __global__ void __launch_bounds__(1024) fft_cols_fwd_kernel(FftArgs a) {
         const int l = i >> logC, c = i & (C - 1);
         const int k = col0 + c;
         const int lm = (D - l) & (D - 1);
+        RX_ASSERT(l < D && k < (D >> 1));
         const cd v = smem[c * stride + pidx(l)];
         if (k == 0) {
             // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
@@ -289,6 +332,7 @@ __global__ void __launch_bounds__(1024) fft_cols_inv_kernel(FftArgs a) {
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int n = C << log2D;
     const int H = D >> 1;
+    rx_poison_smem();
     cd tmp[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -296,6 +340,7 @@ __global__ void __launch_bounds__(1024) fft_cols_inv_kernel(FftArgs a) {
         if (i < n) {
             const int l = i >> logC, k = col0 + (i & (C - 1));
             const int lm = (D - l) & (D - 1);
+            RX_ASSERT(l < D && k < H);
             if (k == 0) {
                 cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
                 if (SYM) {
@@ -317,7 +362,10 @@ __global__ void __launch_bounds__(1024) fft_cols_inv_kernel(FftArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const int i = threadIdx.x + q * blockDim.x;
-        if (i < n) smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
+        if (i < n) {
+            RX_SMEM((i & (C - 1)) * stride + pidx(i >> logC));
+            smem[(i & (C - 1)) * stride + pidx(i >> logC)] = tmp[q];
+        }
     }
     __syncthreads();
     const int col = threadIdx.x / tf, t = threadIdx.x - col * tf;
@@ -346,10 +394,13 @@ __global__ void __launch_bounds__(1024) fft_rows_inv_kernel(FftArgs a) {
     const cd *inp = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     double *outp = static_cast<double *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const int PL = padded_len(D);
+    rx_poison_smem();
     const int m = nb * H;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         const int pr = i / H, k = i - pr * H;
         const size_t g = (2 * (pair0 + pr)) * D + k;
+        RX_ASSERT(g + D < (size_t)D * D);
+        RX_SMEM(pr * PL + pidx(D - 1));
         const cd g1 = inp[g], g2 = inp[g + D];
         cd *Z = smem + pr * PL;
         if (k == 0) {
@@ -372,6 +423,7 @@ __global__ void __launch_bounds__(1024) fft_rows_inv_kernel(FftArgs a) {
             const int pr = i >> log2D, x = i & (D - 1);
             const cd v = smem[pr * PL + pidx(x)];
             const size_t g = (2 * (pair0 + pr)) * D + x;
+            RX_ASSERT(g + D < (size_t)D * D);
             outp[g] = v.x * sc;
             outp[g + D] = v.y * sc;
         }
@@ -924,27 +976,31 @@ __device__ __forceinline__ void r2x_tile(const R2XPole *sp, int cnt, const doubl
     }
 }
 
-// grid = (octet-item tiles of 128, pole chunks); a thread owns one octet item (four {K, -K}
-// pairs with one K2, r2c_octet_item) and runs every pole of its chunk.
-template <int PU, int MINB>
-__global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) {
-    __shared__ R2XPole sp[kR2CTile];
+// Spectrum load; CG: through L2 only (ld.global.cg), for data another CTA of the same launch
+// wrote (the fused small-grid step), which must not be served from a stale L1 line.
+template <bool CG>
+__device__ __forceinline__ cd ld_spec(const cd *p) {
+    if (CG) {
+        const double2 v = __ldcg(reinterpret_cast<const double2 *>(p));
+        return mk(v.x, v.y);
+    }
+    return *p;
+}
+
+// Per-item setup of the explicit-solve R2C kernel: the four {K, -K} pairs of octet item `item`
+// (r2c_octet_item), their representative modes rep[], validity ok[] and the shared K2; the
+// pair state from the representative's spectrum (pole-independent, kept in registers).
+template <bool CG>
+__device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&st)[4], long (&rep)[4],
+                                          bool (&ok)[2], double &K2) {
     const long n_modes = a.n_modes;
-    const int chunk = blockIdx.y;
-    const long len = a.pole_end - a.pole_begin;
-    const long p0 = a.pole_begin + len * chunk / a.n_chunks;
-    const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
     const double c = a.tau;
     const double hmu = a.hmu;
     const int H = a.D >> 1;
-    const long item = (long)blockIdx.x * kPoleBlock + threadIdx.x;
     long quad[2];
-    bool ok[2];
     bool shared_k2 = false;
     r2c_octet_item(item, a.D, quad, ok, shared_k2);
-    long rep[4];
-    double K2 = 0.0;
-    XPair st[4];
+    K2 = 0.0;
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
         const long qs = quad[g];
@@ -956,9 +1012,11 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) 
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const long mm = rep[2 * g + j];
+            RX_ASSERT(mm >= 0 && mm < n_modes);
             const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
             const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
-            const cd e = a.fhat[mm], uu = a.fhat[n_modes + mm], vv = a.fhat[2 * n_modes + mm];
+            const cd e = ld_spec<CG>(a.fhat + mm), uu = ld_spec<CG>(a.fhat + n_modes + mm),
+                     vv = ld_spec<CG>(a.fhat + 2 * n_modes + mm);
             // delta0 = i (kx u + ky v), zeta0 = i (kx v - ky u)   (tau-scaled)
             const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
             const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
@@ -973,6 +1031,42 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) 
             K2 = fma(kx, kx, ky * ky);   // the same for all four pairs of an octet item
         }
     }
+}
+
+// The item's Hermitian accumulators (eta, delta') at the representative modes of chunk `chunk`.
+__device__ __forceinline__ void r2x_store(const PoleArgs &a, int chunk, const XPair (&st)[4],
+                                          const long (&rep)[4], const bool (&ok)[2]) {
+    const long n_modes = a.n_modes;
+    cd *out = a.partial + (size_t)chunk * 3 * n_modes;
+    RX_ASSERT(chunk >= 0 && chunk < a.n_chunks && ((long)chunk * 3 + 2) * n_modes <= a.partial_cap);
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        if (ok[g]) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                out[rep[2 * g + j]] = st[2 * g + j].H0;
+                out[n_modes + rep[2 * g + j]] = st[2 * g + j].H1;
+            }
+        }
+    }
+}
+
+// grid = (octet-item tiles of 128, pole chunks); a thread owns one octet item (four {K, -K}
+// pairs with one K2, r2c_octet_item) and runs every pole of its chunk.
+template <int PU, int MINB>
+__global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) {
+    __shared__ R2XPole sp[kR2CTile];
+    const int chunk = blockIdx.y;
+    const long len = a.pole_end - a.pole_begin;
+    const long p0 = a.pole_begin + len * chunk / a.n_chunks;
+    const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
+    const long item = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+    RX_ASSERT(p0 >= 0 && p0 <= p1 && p1 <= a.n_poles);
+    long rep[4];
+    bool ok[2];
+    double K2;
+    XPair st[4];
+    r2x_setup<false>(a, item, st, rep, ok, K2);
     for (long pt = p0; pt < p1; pt += kR2CTile) {
         const int cnt = (int)min((long)kR2CTile, p1 - pt);
         __syncthreads();
@@ -985,17 +1079,7 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) 
         __syncthreads();
         r2x_tile<PU>(sp, cnt, K2, st);
     }
-    cd *out = a.partial + (size_t)chunk * 3 * n_modes;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-        if (ok[g]) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                out[rep[2 * g + j]] = st[2 * g + j].H0;
-                out[n_modes + rep[2 * g + j]] = st[2 * g + j].H1;
-            }
-        }
-    }
+    r2x_store(a, chunk, st, rep, ok);
 }
 
 // grid = (tiles, pole chunks). MPT < 4: a thread owns MPT modes m = tile0 + j * 128 + tid.
@@ -1109,6 +1193,43 @@ pole_kernel(PoleArgs a) {
     }
 }
 
+// R2C finish of mode m (kinds 6, 7): if m represents a {K, -K} pair (the smaller linear index),
+// sum the chunk partials in a fixed order, rebuild delta and zeta, recover (u, v) and write the
+// Hermitian spectrum at both modes. CG: partial / fhat loads through L2 only (fused step).
+template <bool CG>
+__device__ __forceinline__ void finish_r2c_mode(const FinishArgs &a, long m) {
+    const long n = a.n_modes;
+    const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
+    const long mm = ((long)((a.D - l) & (a.D - 1)) << a.log2D) + ((a.D - k) & (a.D - 1));
+    if (mm <= m) return;   // self-mirror K = 0 corner (fixup_k0_kernel), or the mirror of a pair
+    RX_ASSERT(m >= 0 && mm < n && ((long)(a.n_chunks - 1) * 3 + 2) * n <= a.partial_cap);
+    // m is the representative of {K, -K} (the smaller linear index): finish both modes
+    cd h0 = mk(0, 0), h1 = mk(0, 0);
+    for (int c = 0; c < a.n_chunks; ++c) {
+        const cd *p = a.partial + (size_t)c * 3 * n;
+        const cd x0 = ld_spec<CG>(p + m), x1 = ld_spec<CG>(p + n + m);
+        h0 = mk(h0.x + x0.x, h0.y + x0.y);
+        h1 = mk(h1.x + x1.x, h1.y + x1.y);
+    }
+    const double kx = a.ksym[k], ky = a.ksym[l];
+    const cd e = ld_spec<CG>(a.fhat + m), uu = ld_spec<CG>(a.fhat + n + m), vv = ld_spec<CG>(a.fhat + 2 * n + m);
+    const double c = a.tau;
+    // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
+    h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
+    const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
+    const cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
+    const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0: only the corners have K2 = 0
+    const cd t = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
+    const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
+    const cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
+    a.acc[m] = h0;
+    a.acc[n + m] = U;
+    a.acc[2 * n + m] = V;
+    a.acc[mm] = mk(h0.x, -h0.y);   // the Hermitian spectrum at -K is the conjugate
+    a.acc[n + mm] = mk(U.x, -U.y);
+    a.acc[2 * n + mm] = mk(V.x, -V.y);
+}
+
 // ============================================================================= finish
 // Sums the chunk partials in a fixed order. Kinds 0 and 2 accumulate only (eta, delta): the
 // zeta component of every solve is affine in its eta component (the third equation,
@@ -1122,34 +1243,7 @@ __global__ void __launch_bounds__(256) finish_kernel(FinishArgs a) {
     const long n = a.n_modes;
     if (m >= n) return;
     if (a.kind == 6 || a.kind == 7) {   // R2C pairs: Hermitian accumulators at the representative mode
-        const int l = (int)(m >> a.log2D), k = (int)(m & (a.D - 1));
-        const long mm = ((long)((a.D - l) & (a.D - 1)) << a.log2D) + ((a.D - k) & (a.D - 1));
-        if (mm <= m) return;   // self-mirror K = 0 corner (fixup_k0_kernel), or the mirror of a pair
-        // m is the representative of {K, -K} (the smaller linear index): finish both modes
-        cd h0 = mk(0, 0), h1 = mk(0, 0);
-        for (int c = 0; c < a.n_chunks; ++c) {
-            const cd *p = a.partial + (size_t)c * 3 * n;
-            const cd x0 = p[m], x1 = p[n + m];
-            h0 = mk(h0.x + x0.x, h0.y + x0.y);
-            h1 = mk(h1.x + x1.x, h1.y + x1.y);
-        }
-        const double kx = a.ksym[k], ky = a.ksym[l];
-        const cd e = a.fhat[m], uu = a.fhat[n + m], vv = a.fhat[2 * n + m];
-        const double c = a.tau;
-        // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
-        h1 = mk(fma(-a.Sd.x, e.x, h1.x), fma(-a.Sd.x, e.y, h1.y));
-        const cd m0 = mk(fma(-c, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c, e.y, fma(kx, vv.x, -ky * uu.x)));
-        const cd h2 = mk(fma(a.S.x, m0.x, c * h0.x), fma(a.S.x, m0.y, c * h0.y));
-        const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0: only the corners have K2 = 0
-        const cd t = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
-        const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
-        const cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
-        a.acc[m] = h0;
-        a.acc[n + m] = U;
-        a.acc[2 * n + m] = V;
-        a.acc[mm] = mk(h0.x, -h0.y);   // the Hermitian spectrum at -K is the conjugate
-        a.acc[n + mm] = mk(U.x, -U.y);
-        a.acc[2 * n + mm] = mk(V.x, -V.y);
+        finish_r2c_mode<false>(a, m);
         return;
     }
     const bool pv = (a.kind == 0 || a.kind == 2 || a.kind == 4 || a.kind == 5);
@@ -1312,6 +1406,238 @@ __global__ void __launch_bounds__(256) hermitian_kernel(const cd *__restrict__ i
 }
 
 // ============================================================================= launchers
+// ============================================================================= fused small-grid step
+// For small grids the seven launches of a step (4 FFT passes, pole kernel, finish, K = 0 fix-up)
+// cost more in launch gaps than in work (C1: 64^2, 47 poles). This kernel runs the whole step
+// S1..S5 in ONE launch of one thread-block cluster (16 CTAs when the device allows a non-portable
+// cluster size, else 8), the stages separated by cluster barriers (barrier.cluster arrive.release /
+// wait.acquire, after a __threadfence): the intermediate arrays (half spectra, spectrum, chunk
+// partials, accumulator) stay in L2 in the plan's workspace, read back with ld.global.cg.
+//   A  forward rows (two real rows per complex transform)      -> half   (fft_rows_fwd_kernel)
+//   B  forward half-spectrum columns, D^-2                      -> fhat   (fft_cols_fwd_kernel)
+//   C  PFHX pole loop: thread (item, chunk) runs its poles      -> partial (pole_kernel_r2x)
+//      + the four K = 0 corners, one warp each                  -> acc    (fixup_k0_kernel)
+//   D  R2C finish of every pair                                 -> acc    (finish_kernel)
+//   E  inverse columns (Hermitian input)                        -> half   (fft_cols_inv_kernel<0>)
+//   F  inverse rows                                             -> out    (fft_rows_inv_kernel)
+// Same arithmetic as the multi-launch path stage by stage (shared device functions), except the
+// K = 0 pole sums, which are reduced across a warp in a different order.
+constexpr int kSmallThreads = 256;
+
+namespace cgx = cooperative_groups;
+
+__device__ __forceinline__ void cluster_barrier() {
+    __threadfence();
+    cgx::this_cluster().sync();
+}
+
+// The four K = 0 corners (self-mirror modes), one warp per corner: the Coriolis 2x2 solves of
+// fixup_k0_kernel summed over the pole range, lanes striding the poles, then a warp reduction.
+__device__ __forceinline__ void fixup_k0_warp(const FixupArgs &a, int corner, int lane) {
+    const int D = a.D, H = D / 2;
+    const int ls[4] = {0, 0, H, H}, ks[4] = {0, H, 0, H};
+    const long m = (long)ls[corner] * D + ks[corner];
+    const long n = a.n_modes;
+    const cd ua = ld_spec<true>(a.fhat + n + m), vb = ld_spec<true>(a.fhat + 2 * n + m);
+    cd Au = mk(0, 0), Av = mk(0, 0);
+    for (long p = a.pole_begin + lane; p < a.pole_end; p += 32) {
+        const PoleConst *P = a.poles + p;
+        const cd s3 = mk(__ldg(&P->s3r), __ldg(&P->s3i)), s4 = mk(__ldg(&P->s4r), __ldg(&P->s4i));
+        const cd w1 = mk(__ldg(&P->w1r), __ldg(&P->w1i)), w2 = mk(__ldg(&P->w2r), __ldg(&P->w2i));
+        const cd u1 = cfms(s4, vb, cmul(s3, ua));
+        const cd v1 = cfma(s3, vb, cmul(s4, ua));
+        if (a.method == 1) {   // REXI: one solve per term
+            Au = cfma(w1, u1, Au);
+            Av = cfma(w1, v1, Av);
+            continue;
+        }
+        const cd u2 = cjfma(s4, v1, cjfma(s3, u1, mk(0, 0)));
+        const cd v2 = cjfms(s4, u1, cjfma(s3, v1, mk(0, 0)));
+        Au = cfma(w2, u2, cfma(w1, u1, Au));
+        Av = cfma(w2, v2, cfma(w1, v1, Av));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Au.x += __shfl_xor_sync(0xffffffffu, Au.x, o);
+        Av.x += __shfl_xor_sync(0xffffffffu, Av.x, o);
+    }
+    if (lane == 0) {
+        // the R2C accumulator is the Hermitian part, at a self-mirror mode Re A; eta = S e0 there
+        a.acc[m] = mk(cmul(a.S, ld_spec<true>(a.fhat + m)).x, 0.0);
+        a.acc[n + m] = mk(Au.x, 0.0);
+        a.acc[2 * n + m] = mk(Av.x, 0.0);
+    }
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs a) {
+    extern __shared__ cd smem[];
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int cta = (int)cl.block_rank();
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int D = a.pole.D, log2D = a.pole.log2D, H = D >> 1;
+    const long n = a.pole.n_modes;
+    const int tf = D >= 8 ? D / 8 : 1;
+    const int PL = padded_len(D);
+    const int stride = PL + 1;   // column slabs
+    const int P3 = 3 * H;        // row pairs (A, F) = half-spectrum columns (B, E), all fields
+    const int u0 = (int)((long)P3 * cta / CS), u1 = (int)((long)P3 * (cta + 1) / CS);
+    const int nu = u1 - u0;      // this CTA's row pairs / columns
+    rx_poison_smem();
+    RX_ASSERT(nu * stride * 16 <= (int)dyn_smem_bytes() && u1 <= P3);
+
+    // ---- A: forward rows
+    for (int i = tid; i < nu * D; i += NT) {
+        const int pr = i >> log2D, x = i & (D - 1);
+        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const double *in = a.in[f];
+        const size_t g = (size_t)(2 * pair) * D + x;
+        RX_ASSERT(f < 3 && g + D < (size_t)n);
+        smem[pr * PL + pidx(x)] = mk(__ldg(in + g), __ldg(in + g + D));
+    }
+    __syncthreads();
+    {
+        const int row = tid / tf, t = tid - row * tf;
+        fft_in_smem<false>(smem + row * PL, D, log2D, t, tf, a.tw, row < nu);
+    }
+    for (int i = tid; i < nu * H; i += NT) {
+        const int pr = i / H, k = i - pr * H;
+        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const cd *Z = smem + pr * PL;
+        cd X1, X2;
+        if (k == 0) {
+            const cd z0 = Z[pidx(0)], zh = Z[pidx(H)];
+            X1 = mk(z0.x, zh.x);
+            X2 = mk(z0.y, zh.y);
+        } else {
+            const cd zk = Z[pidx(k)], zm = Z[pidx(D - k)];
+            X1 = mk(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+            X2 = mk(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+        }
+        const size_t g = (size_t)f * n + (size_t)(2 * pair) * D + k;
+        a.half[g] = X1;
+        a.half[g + D] = X2;
+    }
+    cluster_barrier();
+
+    // ---- B: forward columns of the half spectra -> full spectrum (F(-K) = conj F(K)), D^-2
+    for (int i = tid; i < nu * D; i += NT) {
+        const int c = i % nu, l = i / nu;
+        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        smem[c * stride + pidx(l)] = ld_spec<true>(a.half + (size_t)f * n + (size_t)l * D + k);
+    }
+    __syncthreads();
+    {
+        const int col = tid / tf, t = tid - col * tf;
+        fft_in_smem<false>(smem + col * stride, D, log2D, t, tf, a.tw, col < nu);
+    }
+    {
+        const double sc = a.scale;
+        cd *fhat = const_cast<cd *>(a.pole.fhat);
+        for (int i = tid; i < nu * D; i += NT) {
+            const int c = i % nu, l = i / nu;
+            const int gc = u0 + c, f = gc / H, k = gc - f * H;
+            const int lm = (D - l) & (D - 1);
+            const cd v = smem[c * stride + pidx(l)];
+            cd *out = fhat + (size_t)f * n;
+            if (k == 0) {
+                const cd w = smem[c * stride + pidx(lm)];
+                const double hs = 0.5 * sc;
+                out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+                out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            } else {
+                out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+                out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);
+            }
+        }
+    }
+    cluster_barrier();
+
+    // ---- C: pole loop (thread = (octet item, pole chunk)) and the K = 0 corners
+    {
+        // every thread but the last four warps of the cluster works on (item, chunk) units
+        const long gt = (long)cta * NT + tid;
+        const long W = (long)CS * NT - 128;
+        const long items = a.n_items;
+        const int chunks = a.pole.n_chunks;
+        const long len = a.pole.pole_end - a.pole.pole_begin;
+        for (long w = gt; gt < W && w < items * chunks; w += W) {
+            const long item = w % items;
+            const int chunk = (int)(w / items);
+            const long p0 = a.pole.pole_begin + len * chunk / chunks;
+            const long p1 = a.pole.pole_begin + len * (chunk + 1) / chunks;
+            long rep[4];
+            bool ok[2];
+            double K2;
+            XPair st[4];
+            r2x_setup<true>(a.pole, item, st, rep, ok, K2);
+            r2x_tile<1>(a.pole.xpoles + p0, (int)(p1 - p0), K2, st);
+            r2x_store(a.pole, chunk, st, rep, ok);
+        }
+        if (gt >= W) fixup_k0_warp(a.fix, (int)((gt - W) >> 5), tid & 31);
+    }
+    cluster_barrier();
+
+    // ---- D: R2C finish of every pair
+    for (long m = (long)cta * NT + tid; m < n; m += (long)CS * NT) finish_r2c_mode<true>(a.fin, m);
+    cluster_barrier();
+
+    // ---- E: inverse columns (the accumulator is Hermitian: no symmetrisation)
+    for (int i = tid; i < nu * D; i += NT) {
+        const int c = i % nu, l = i / nu;
+        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        const cd *in = a.fin.acc + (size_t)f * n + (size_t)l * D;
+        cd v;
+        if (k == 0) {
+            const cd t0 = ld_spec<true>(in), th = ld_spec<true>(in + H);
+            v = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+        } else {
+            v = ld_spec<true>(in + k);
+        }
+        smem[c * stride + pidx(l)] = v;
+    }
+    __syncthreads();
+    {
+        const int col = tid / tf, t = tid - col * tf;
+        fft_in_smem<true>(smem + col * stride, D, log2D, t, tf, a.tw, col < nu);
+    }
+    for (int i = tid; i < nu * D; i += NT) {
+        const int c = i % nu, r = i / nu;
+        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        a.half[(size_t)f * n + (size_t)r * D + k] = smem[c * stride + pidx(r)];
+    }
+    cluster_barrier();
+
+    // ---- F: inverse rows -> the three real fields
+    for (int i = tid; i < nu * H; i += NT) {
+        const int pr = i / H, k = i - pr * H;
+        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const size_t g = (size_t)f * n + (size_t)(2 * pair) * D + k;
+        const cd g1 = ld_spec<true>(a.half + g), g2 = ld_spec<true>(a.half + g + D);
+        cd *Z = smem + pr * PL;
+        if (k == 0) {
+            Z[pidx(0)] = mk(g1.x, g2.x);
+            Z[pidx(H)] = mk(g1.y, g2.y);
+        } else {
+            Z[pidx(k)] = mk(g1.x - g2.y, g1.y + g2.x);        // g1 + i g2
+            Z[pidx(D - k)] = mk(g1.x + g2.y, g2.x - g1.y);    // conj g1 + i conj g2
+        }
+    }
+    __syncthreads();
+    {
+        const int row = tid / tf, t = tid - row * tf;
+        fft_in_smem<true>(smem + row * PL, D, log2D, t, tf, a.tw, row < nu);
+    }
+    for (int i = tid; i < nu * D; i += NT) {
+        const int pr = i >> log2D, x = i & (D - 1);
+        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const cd v = smem[pr * PL + pidx(x)];
+        const size_t g = (size_t)(2 * pair) * D + x;
+        a.out[f][g] = v.x;
+        a.out[f][g + D] = v.y;
+    }
+}
+
 static int ilog2(int x) {
     int r = 0;
     while ((1 << r) < x) ++r;
@@ -1589,6 +1915,138 @@ cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStr
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel) {
     if (beside_pole_kernel) fixup_k0_kernel<128><<<4, 128, 0, st>>>(a);
     else fixup_k0_kernel<1024><<<4, 1024, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------- fused small-grid step
+// Cluster size (16 if the device allows a non-portable cluster of this kernel, else 8), or 0 if
+// cluster launch is unavailable. Cached per process (one device model per run).
+int small_step_cluster() {
+    static int cs = -1;
+    if (cs >= 0) return cs;
+    cs = 0;
+    if (cudaFuncSetAttribute(step_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+    }
+    // the 8-CTA cluster at D = 128 needs 56 KB of dynamic shared memory per CTA (> the 48 KB default)
+    if (cudaFuncSetAttribute(step_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)small_step_smem(128)) != cudaSuccess) {
+        cudaGetLastError();
+        return cs;
+    }
+    for (int want : {16, 8}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(want);
+        cfg.blockDim = dim3(kSmallThreads);
+        cfg.dynamicSmemBytes = small_step_smem(128);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = want;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, step_small_kernel, &cfg) == cudaSuccess && nclusters >= 1) {
+            cs = want;
+            break;
+        }
+        cudaGetLastError();
+    }
+    return cs;
+}
+
+size_t small_step_smem(int D) {
+    const int cs = 8;   // the smaller cluster needs the larger per-CTA share
+    const int nu = (3 * (D / 2) + cs - 1) / cs;
+    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd);
+}
+
+long small_step_items(int D) { return r2c_items(D, 2, true); }
+
+cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = small_step_smem(a.pole.D);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, step_small_kernel, a);
+}
+
+// ----------------------------------------------------------------------------- 1-D transforms (NEXT-3)
+// The length-n DFT of one complex vector, out[j] = scale * sum_k in[k] e^{-+2 pi i j k / n}, for
+// the circulant test matrices of Sec. 3.2 (rexi_circulant_apply): power-of-two n <= 2048 through
+// the radix-8 Stockham passes of the 2-D transforms (one block, twiddles from a table made by
+// sincospi), any other n by a direct DFT (one thread per output, index j k reduced mod n exactly).
+__global__ void twiddle_table_kernel(cd *tw, int n) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double sn, cs;
+    sincospi(-2.0 * (double)j / (double)n, &sn, &cs);
+    tw[j] = mk(cs, sn);
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256) fft1d_kernel(const cd *__restrict__ in, cd *__restrict__ out, int n,
+                                                    int logn, double scale, const cd *__restrict__ tw) {
+    extern __shared__ cd smem[];
+    rx_poison_smem();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        RX_SMEM(pidx(i));
+        smem[pidx(i)] = in[i];
+    }
+    __syncthreads();
+    const int tf = n >= 8 ? n / 8 : 1;
+    fft_in_smem<INV>(smem, n, logn, (int)threadIdx.x, tf, tw, (int)threadIdx.x < tf);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const cd v = smem[pidx(i)];
+        out[i] = mk(v.x * scale, v.y * scale);
+    }
+}
+
+__global__ void __launch_bounds__(256) dft1d_direct_kernel(const cd *__restrict__ in, cd *__restrict__ out, long n,
+                                                           int sign, double scale) {
+    const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double ar = 0.0, ai = 0.0;
+    long idx = 0;   // (j * k) mod n, advanced by j each step (exact integers)
+    for (long k = 0; k < n; ++k) {
+        double sn, cs;
+        sincospi((double)sign * 2.0 * (double)idx / (double)n, &sn, &cs);
+        const cd x = in[k];
+        ar = fma(x.x, cs, fma(-x.y, sn, ar));
+        ai = fma(x.x, sn, fma(x.y, cs, ai));
+        idx += j;
+        if (idx >= n) idx -= n;
+    }
+    out[j] = mk(ar * scale, ai * scale);
+}
+
+bool dft1d_uses_fft(long n) { return n >= 2 && n <= 2048 && (n & (n - 1)) == 0; }
+
+cudaError_t launch_twiddles(cd *tw, int n, cudaStream_t st) {
+    twiddle_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(tw, n);
+    return cudaGetLastError();
+}
+
+// in != out required; tw: table of n entries (launch_twiddles) when dft1d_uses_fft(n)
+cudaError_t launch_dft1d(const cd *in, cd *out, long n, bool inverse, double scale, const cd *tw, cudaStream_t st) {
+    if (dft1d_uses_fft(n)) {
+        const int nn = (int)n;
+        const int threads = std::max(32, std::min(256, nn / 8));
+        const size_t sm = (size_t)padded_len(nn) * sizeof(cd);
+        if (inverse) fft1d_kernel<true><<<1, threads, sm, st>>>(in, out, nn, ilog2(nn), scale, tw);
+        else fft1d_kernel<false><<<1, threads, sm, st>>>(in, out, nn, ilog2(nn), scale, tw);
+        return cudaGetLastError();
+    }
+    dft1d_direct_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, n, inverse ? 1 : -1, scale);
     return cudaGetLastError();
 }
 

@@ -11,7 +11,36 @@
 #define REXI_RCP_F32_SEED 0
 #endif
 
+// REXI_CHECKED builds (librexi_checked.so, paper_2008_11607_b200/build.py --checked): device-side
+// bounds checks on every global / shared-memory index of the default path, a trap on failure
+// (the replacement for compute-sanitizer memcheck, which this pool does not allow). Compiled out
+// otherwise.
+#ifdef REXI_CHECKED
+#include <cstdio>
+#define RX_ASSERT(cond)                                                                            \
+    do {                                                                                           \
+        if (!(cond)) {                                                                             \
+            printf("REXI_CHECKED: (%s) failed at %s:%d block (%d,%d) thread %d\n", #cond, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                  \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define RX_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace rexi {
+
+// bytes of dynamic shared memory of the running block (%dynamic_smem_size)
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+    unsigned r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+// a complex index into the block's dynamic shared memory is in range
+#define RX_SMEM(i) RX_ASSERT((long)(i) >= 0 && ((long)(i) + 1) * 16 <= (long)dyn_smem_bytes())
 
 // ----------------------------------------------------------------------------- complex fp64
 struct __align__(16) cd {
@@ -73,6 +102,8 @@ struct PoleArgs {
     double hmu;            // Re(alpha_n) = h mu (same for every pole)
     long sk_tiles;         // R2C stream-K: tiles of 128 octet items (0: chunked launch)
     int sk_slots;          // R2C stream-K: partial slots per tile
+    long partial_cap;      // complex values in `partial` (REXI_CHECKED bounds checks)
+    long n_poles;          // entries of the pole tables (REXI_CHECKED)
 };
 
 struct FinishArgs {
@@ -90,6 +121,7 @@ struct FinishArgs {
     long sk_tiles;         // R2C stream-K (see PoleArgs); 0: chunked partials
     int sk_slots, sk_ctas;
     long sk_poles;         // pole-range length
+    long partial_cap;      // complex values in `partial` (REXI_CHECKED)
 };
 
 struct FixupArgs {
@@ -102,6 +134,23 @@ struct FixupArgs {
     long pole_begin, pole_end;
     long n_modes;
     int D;
+};
+
+// ----------------------------------------------------------------------------- fused small-grid step
+// One cluster of CTAs runs a whole physical step S1..S5 for small grids (kernels.cu
+// "fused small-grid step"): rows/columns forward FFT, the PFHX pole loop (octet items x pole
+// chunks) with the K = 0 corners, the R2C finish, columns/rows inverse FFT, separated by
+// cluster barriers; intermediate arrays live in L2 (plan workspace).
+struct SmallArgs {
+    const double *in[3];
+    double *out[3];
+    cd *half;              // [3][D*D] scratch: half spectra (row layout of the FFT passes)
+    PoleArgs pole;         // fhat (written here), partial, xpoles, ksym, range, n_chunks, ...
+    FinishArgs fin;        // acc, S, Sd (partial, fhat, ksym as in pole)
+    FixupArgs fix;         // the four K = 0 corners (poles = generic table)
+    const cd *tw;
+    double scale;          // D^-2
+    long n_items;          // octet work items (r2c_items(D, 2, true))
 };
 
 // ----------------------------------------------------------------------------- FFT passes

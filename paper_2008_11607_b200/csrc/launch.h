@@ -38,6 +38,18 @@ long sk_slots_bound(long tiles, long poles, long ctas);
 cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
+// fused small-grid step (one cluster launch for S1..S5, PFHX kernel): cluster size (0: unavailable),
+// dynamic shared memory per CTA, octet work items, launch
+int small_step_cluster();
+size_t small_step_smem(int D);
+long small_step_items(int D);
+constexpr int kSmallThreadsHost = 256;
+cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st);
+// NEXT-3 1-D transforms: power-of-two n <= 2048 by Stockham passes (twiddle table of n entries
+// from launch_twiddles), other n by a direct DFT; out = scale * DFT(in) (inverse: e^{+})
+bool dft1d_uses_fft(long n);
+cudaError_t launch_twiddles(cd *tw, int n, cudaStream_t st);
+cudaError_t launch_dft1d(const cd *in, cd *out, long n, bool inverse, double scale, const cd *tw, cudaStream_t st);
 // rows D/2+1 .. D-1 of a Hermitian spectrum from rows 1 .. D/2-1 (in place)
 cudaError_t launch_mirror_rows(cd *acc, long n_modes, int D, cudaStream_t st);
 

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <complex>
 #include <new>
 #include <string>
 #include <vector>
@@ -68,6 +69,14 @@ __global__ void __launch_bounds__(kScalarBlock) scalar_kernel(const rexi::Scalar
         __syncthreads();
     }
     if (threadIdx.x == 0) out[j] = cmul(phase, cmul(red[0], in[j]));
+}
+
+// i x_j = tau (lambda_j - nu): x_j = Im(tau (lambda_j - nu)) for real tau (the eigenvalues of
+// the circulant are purely imaginary up to rounding; their real part is dropped).
+__global__ void eig_to_x_kernel(const cd *__restrict__ lam, double *__restrict__ x, long n, double tau,
+                                double nu_im) {
+    const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) x[j] = tau * (lam[j].y - nu_im);
 }
 
 }  // namespace
@@ -167,6 +176,59 @@ rexi_status_t rexi_scalar_apply(rexi_scalar_plan_t p, int method, long n, const 
     else
         scalar_kernel<REXI_SCALAR_REXI_M><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, cin, cout, ph);
     cudaError_t e = cudaGetLastError();
+    cudaSetDevice(prev);
+    return e == cudaSuccess ? REXI_OK : sfail(REXI_ECUDA, cudaGetErrorString(e));
+}
+
+rexi_status_t rexi_circulant_apply(rexi_scalar_plan_t p, int method, long n, const double *col,
+                                   const double *f, double *out, double tau, double nu_re,
+                                   double nu_im, void *stream) {
+    if (!p || n < 1 || !col || !f || !out) return sfail(REXI_EINVAL, "null plan/pointer or n < 1");
+    if (method != REXI_SCALAR_REXII && method != REXI_SCALAR_REXI && method != REXI_SCALAR_REXI_M)
+        return sfail(REXI_EINVAL, "unknown scalar method");
+    if (n > (1L << 20)) return sfail(REXI_EINVAL, "n > 2^20");
+    if (!std::isfinite(tau) || !std::isfinite(nu_re) || !std::isfinite(nu_im))
+        return sfail(REXI_EINVAL, "tau and nu must be finite");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(p->device) != cudaSuccess) {
+        cudaGetLastError();
+        return sfail(REXI_ECUDA, "cudaSetDevice failed");
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // stream-ordered scratch: lambda, fh, out-hat (n complex each), x (n doubles), twiddles (n)
+    void *work = nullptr;
+    const size_t bytes = sizeof(cd) * (size_t)n * 4 + sizeof(double) * (size_t)n;
+    cudaError_t e = cudaMallocAsync(&work, bytes, st);
+    if (e == cudaSuccess) {
+        cd *lam = static_cast<cd *>(work), *fh = lam + n, *oh = fh + n, *tw = oh + n;
+        double *x = reinterpret_cast<double *>(tw + n);
+        const bool fft = rexi::dft1d_uses_fft(n);
+        // e^{tau nu}: the phase of Remark 1's shift
+        const std::complex<double> ph = std::exp(tau * std::complex<double>(nu_re, nu_im));
+        if (fft) e = rexi::launch_twiddles(tw, (int)n, st);
+        if (e == cudaSuccess) e = rexi::launch_dft1d(reinterpret_cast<const cd *>(col), lam, n, false, 1.0, tw, st);
+        if (e == cudaSuccess) e = rexi::launch_dft1d(reinterpret_cast<const cd *>(f), fh, n, false, 1.0, tw, st);
+        if (e == cudaSuccess) {
+            eig_to_x_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lam, x, n, tau, nu_im);
+            e = cudaGetLastError();
+        }
+        const long nt = 2 * p->N + 1;
+        const cd phc = cd{ph.real(), ph.imag()};
+        if (e == cudaSuccess) {
+            if (method == REXI_SCALAR_REXII)
+                scalar_kernel<REXI_SCALAR_REXII><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, fh, oh, phc);
+            else if (method == REXI_SCALAR_REXI)
+                scalar_kernel<REXI_SCALAR_REXI><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, fh, oh, phc);
+            else
+                scalar_kernel<REXI_SCALAR_REXI_M><<<(unsigned)n, kScalarBlock, 0, st>>>(p->d_terms, nt, x, fh, oh, phc);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess)
+            e = rexi::launch_dft1d(oh, reinterpret_cast<cd *>(out), n, true, 1.0 / (double)n, tw, st);
+        cudaError_t ef = cudaFreeAsync(work, st);
+        if (e == cudaSuccess) e = ef;
+    }
     cudaSetDevice(prev);
     return e == cudaSuccess ? REXI_OK : sfail(REXI_ECUDA, cudaGetErrorString(e));
 }

@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 REXI_OK, REXI_EINVAL, REXI_ENOMEM, REXI_ECUDA, REXI_ERANGE = range(5)
 VARIANTS = {"dz": 0, "uv": 1, "dz3": 2, "pf": 3, "pfh": 4, "pfhr": 5, "pfhx": 6}
 METHODS = {"rexii": 0, "rexi": 1}
-SCHEDULES = {"auto": 0, "chunked": 1, "streamk": 2}
+SCHEDULES = {"auto": 0, "chunked": 1, "streamk": 2, "fused": 3}
 
 _vp = ctypes.c_void_p
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -80,6 +80,8 @@ EXPORTS = {
     "rexi_scalar_plan_terms": (ctypes.c_long, [_vp]),
     "rexi_scalar_apply": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_long, _vp, _vp, _vp, ctypes.c_double,
                                          ctypes.c_double, _vp]),
+    "rexi_circulant_apply": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_long, _vp, _vp, _vp, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_double, _vp]),
     "rexi_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rexi_last_error": (ctypes.c_char_p, []),
     "rexi_abi_version": (ctypes.c_int, []),
@@ -450,4 +452,29 @@ class ScalarPlan:
         _check(_lib.rexi_scalar_apply(self._h, SCALAR_METHODS[method], int(x.numel()), _vp(x.data_ptr()),
                                       _vp(vec.data_ptr()), _vp(out.data_ptr()), float(complex(phase).real),
                                       float(complex(phase).imag), stream), "rexi_scalar_apply")
+        return out
+
+    def circulant_apply(self, col, f, tau, method="rexii", nu=0.0, out=None):
+        """rexi_circulant_apply: e^{tau A} f for the circulant A with first column `col` (complex128
+        CUDA tensors of length n on this plan's device): library DFTs + the scalar pole kernel."""
+        torch = _torch()
+
+        def chk(t, name):
+            if not (isinstance(t, torch.Tensor) and t.dtype == torch.complex128 and t.dim() == 1
+                    and t.is_cuda and t.device.index == self.device and t.is_contiguous()):
+                raise ValueError(f"{name}: expected a contiguous 1-D complex128 tensor on cuda:{self.device}")
+            return _vp(t.data_ptr())
+        if method not in SCALAR_METHODS:
+            raise ValueError(f"method must be one of {sorted(SCALAR_METHODS)}")
+        n = int(col.numel()) if isinstance(col, torch.Tensor) else -1
+        if not isinstance(f, torch.Tensor) or f.numel() != n:
+            raise ValueError("col and f must have the same length")
+        out = torch.empty_like(f) if out is None else out
+        if out.numel() != n or out.data_ptr() in (col.data_ptr(), f.data_ptr()):
+            raise ValueError("out: length n, must not alias col or f")
+        nu = complex(nu)
+        stream = _vp(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(_lib.rexi_circulant_apply(self._h, SCALAR_METHODS[method], n, chk(col, "col"), chk(f, "f"),
+                                         chk(out, "out"), float(tau), nu.real, nu.imag, stream),
+               "rexi_circulant_apply")
         return out

@@ -23,16 +23,15 @@ def R():
 
 
 def gpu_apply(R, A, f, tau, h, M, method, nu=0.0):
-    """Diagonalise the circulant A by the DFT (A f = c (*) f, eigenvalues fft(c)), evaluate the
-    scalar form per eigenvalue on the GPU, transform back."""
+    """The whole evaluation on the GPU through rexi_circulant_apply: the library's DFT kernels
+    diagonalise the circulant A (eigenvalues = DFT of its first column), the scalar pole kernel
+    applies r(tau (lambda - nu)) e^{tau nu} per eigenvalue, the inverse DFT returns the vector."""
     import torch
-    lam = np.fft.fft(A[:, 0])                    # eigenvalues (purely imaginary)
-    x = ((tau * (lam - nu)) / 1j).real           # i x = tau (lambda - nu)
-    fh = np.fft.fft(f.astype(np.complex128))
+    col = torch.from_numpy(np.ascontiguousarray(A[:, 0].astype(np.complex128))).cuda()
+    fd = torch.from_numpy(np.ascontiguousarray(f.astype(np.complex128))).cuda()
     sp = R.ScalarPlan(h, M)
-    out = sp.apply(torch.from_numpy(np.ascontiguousarray(x)).cuda(),
-                   torch.from_numpy(fh).cuda(), method=method, phase=np.exp(tau * nu))
-    return np.fft.ifft(out.cpu().numpy())
+    out = sp.circulant_apply(col, fd, tau, method=method, nu=nu)
+    return out.cpu().numpy()
 
 
 def test_scalar_rexii_vs_exp(R):
@@ -90,3 +89,16 @@ def test_fig2c_rexie_A2_gpu(R):
     ref = X.rexie_matrix(A2, f, 1.0, 0.5, M, nu=-2450j)
     assert X.rel_l2(got, ref) < TOL
     assert X.rel_l2(got, X.expm_apply(A2, f, 1.0)) < 1e-11
+
+
+@pytest.mark.parametrize("n", [64, 70, 128])
+def test_circulant_apply_transform_paths(R, n):
+    """rexi_circulant_apply with both transform paths (Stockham passes for n = 64, 128; direct DFT
+    for the paper's n = 70): REXII on A_1 vs the oracle's dense-solve matrix form and expm."""
+    A1, x = X.advection_A1(n)
+    f = X.f0(x)
+    M = C.M_rule(float(n), 0.5)
+    got = gpu_apply(R, A1, f, 1.0, 0.5, M, "rexii")
+    assert np.abs(got.imag).max() < 1e-12 * np.abs(got).max()
+    assert X.rel_l2(got.real, X.rexii_matrix(A1, f, 1.0, 0.5, M)) < TOL
+    assert X.rel_l2(got.real, X.expm_apply(A1, f, 1.0)) < 1e-13

@@ -637,7 +637,9 @@ def test_pfhx_tunings_vs_oracle(R, pu, minb, D):
     f = inputs.white_noise(D)
     p = R.Plan(D, tau, variant="pfhx")
     p.set_tuning(8, pu, minb)
+    p.set_schedule("chunked")   # the multi-launch kernel (AUTO would fuse these small steps)
     got = [host(t) for t in p.apply(*(dev(x) for x in f))]
+    assert p.info["last_schedule"] == 1
     info = p.info
     ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])
     assert rel_l2(got, ref) < TOL

@@ -87,7 +87,7 @@ __device__ __forceinline__ void dftR(cd *v) {
 // Padded shared-memory index: one pad slot per 8 values, so the stride-8 writes of the first
 // Stockham pass (and the stride-N/8 reads) spread over the banks.
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 3); }
-__host__ __device__ __forceinline__ int padded_len(int N) { return N + (N >> 3); }
+__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3); }
 
 // Twiddles w_r = e^{-+2 pi i r step / N}, r = 1..R-1, of one butterfly: w_1, w_2, w_4 from the
 // table (e^{-2 pi i j / N}, j < N), the others as products of two or three of them (<= 3 ulp;
@@ -128,11 +128,17 @@ __device__ __forceinline__ void rx_poison_smem() {
 #endif
 }
 
+// Element i of a transform held in shared memory at s[ix(i)]: PidxIx for a padded contiguous
+// transform (pidx), other accessors for strided ones (columns of the fused small-grid step).
+struct PidxIx {
+    __device__ __forceinline__ int operator()(int i) const { return pidx(i); }
+};
+
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
-template <int R, bool INV>
-__device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, int t, int tf,
-                                              const cd *__restrict__ tw, bool act = true) {
+template <int R, bool INV, class IX>
+__device__ __forceinline__ void stockham_pass_ix(cd *s, IX ix, int N, int Ns, int t, int tf,
+                                                 const cd *__restrict__ tw, bool act) {
     constexpr int PERMAX = 8 / R;
     const int nbf = N / R;
     cd v[8];
@@ -147,8 +153,8 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
             RX_ASSERT(Ns == 1 || R * step < N);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                RX_SMEM((s - rx_smem_base()) + pidx(j + r * nbf));
-                cd x = s[pidx(j + r * nbf)];
+                RX_SMEM((s - rx_smem_base()) + ix(j + r * nbf));
+                cd x = s[ix(j + r * nbf)];
                 if (r > 0 && Ns > 1) x = cmul(x, w[r]);
                 v[b * R + r] = x;
             }
@@ -164,27 +170,40 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
             const int d = (j - k) * R + k;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                RX_SMEM((s - rx_smem_base()) + pidx(d + r * Ns));
-                s[pidx(d + r * Ns)] = v[b * R + r];
+                RX_SMEM((s - rx_smem_base()) + ix(d + r * Ns));
+                s[ix(d + r * Ns)] = v[b * R + r];
             }
         }
     }
     __syncthreads();
 }
 
+template <int R, bool INV>
+__device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, int t, int tf,
+                                              const cd *__restrict__ tw, bool act = true) {
+    (void)logN;
+    stockham_pass_ix<R, INV>(s, PidxIx{}, N, Ns, t, tf, tw, act);
+}
+
 // act = false: the thread only joins the block barriers (blocks with more threads than
 // transforms x tf, e.g. the fused small-grid step)
-template <bool INV>
-__device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw,
-                                            bool act = true) {
+template <bool INV, class IX>
+__device__ __forceinline__ void fft_in_smem_ix(cd *s, IX ix, int N, int logN, int t, int tf, const cd *tw,
+                                               bool act) {
     int Ns = 1, rem = logN;
     while (rem >= 3) {
-        stockham_pass<8, INV>(s, N, logN, Ns, t, tf, tw, act);
+        stockham_pass_ix<8, INV>(s, ix, N, Ns, t, tf, tw, act);
         Ns <<= 3;
         rem -= 3;
     }
-    if (rem == 2) stockham_pass<4, INV>(s, N, logN, Ns, t, tf, tw, act);
-    else if (rem == 1) stockham_pass<2, INV>(s, N, logN, Ns, t, tf, tw, act);
+    if (rem == 2) stockham_pass_ix<4, INV>(s, ix, N, Ns, t, tf, tw, act);
+    else if (rem == 1) stockham_pass_ix<2, INV>(s, ix, N, Ns, t, tf, tw, act);
+}
+
+template <bool INV>
+__device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw,
+                                            bool act = true) {
+    fft_in_smem_ix<INV>(s, PidxIx{}, N, logN, t, tf, tw, act);
 }
 
 // ----------------------------------------------------------------------------- real 2-D FFT
@@ -1426,10 +1445,9 @@ constexpr int kSmallThreads = 256;
 
 namespace cgx = cooperative_groups;
 
-__device__ __forceinline__ void cluster_barrier() {
-    __threadfence();
-    cgx::this_cluster().sync();
-}
+// cluster-wide barrier: barrier.cluster.arrive (.release) + wait (.acquire) — orders the
+// global-memory writes of one stage before the reads of the next across the cluster's CTAs
+__device__ __forceinline__ void cluster_barrier() { cgx::this_cluster().sync(); }
 
 // The four K = 0 corners (self-mirror modes), one warp per corner: the Coriolis 2x2 solves of
 // fixup_k0_kernel summed over the pole range, lanes striding the poles, then a warp reduction.
@@ -1469,27 +1487,49 @@ __device__ __forceinline__ void fixup_k0_warp(const FixupArgs &a, int corner, in
     }
 }
 
+// Pole records cached in shared memory when the range fits (loaded while stage A runs).
+constexpr int kSmallPoleCache = 256;
+
+// Stages A, B, E, F split the 3 H row pairs (A, F) / half-spectrum columns (B, E) of the three
+// fields over the cluster's CTAs; the pole stage C and the finish D use every CTA. (Giving each
+// field's whole 2-D transform to one CTA, three barriers instead of five, measured 20 % slower:
+// the transform chain of one CTA is longer than two cluster barriers.)
+template <int LOGD>
 __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs a) {
+    constexpr int D = 1 << LOGD, H = D >> 1, LOGH = LOGD - 1;
+    constexpr int tf = D >= 8 ? D / 8 : 1;
+    constexpr int PL = padded_len(D);
+    constexpr int stride = PL + 1;   // column slabs
+    constexpr long n = (long)D * D;
     extern __shared__ cd smem[];
     cgx::cluster_group cl = cgx::this_cluster();
     const int CS = (int)cl.num_blocks();
     const int cta = (int)cl.block_rank();
     const int tid = threadIdx.x, NT = blockDim.x;
-    const int D = a.pole.D, log2D = a.pole.log2D, H = D >> 1;
-    const long n = a.pole.n_modes;
-    const int tf = D >= 8 ? D / 8 : 1;
-    const int PL = padded_len(D);
-    const int stride = PL + 1;   // column slabs
-    const int P3 = 3 * H;        // row pairs (A, F) = half-spectrum columns (B, E), all fields
+    constexpr int P3 = 3 * H;        // row pairs (A, F) = half-spectrum columns (B, E), all fields
     const int u0 = (int)((long)P3 * cta / CS), u1 = (int)((long)P3 * (cta + 1) / CS);
-    const int nu = u1 - u0;      // this CTA's row pairs / columns
+    const int nu = u1 - u0;          // this CTA's row pairs / columns
+    const int nu_max = (P3 + CS - 1) / CS;
     rx_poison_smem();
-    RX_ASSERT(nu * stride * 16 <= (int)dyn_smem_bytes() && u1 <= P3);
+    RX_ASSERT(nu <= nu_max && u1 <= P3);
+    // pole cache after the FFT region
+    R2XPole *pc = reinterpret_cast<R2XPole *>(smem + nu_max * stride);
+    const long pb = a.pole.pole_begin, npl = a.pole.pole_end - a.pole.pole_begin;
+    const bool cached = npl <= kSmallPoleCache;
+    if (cached) {
+        const double2 *src = reinterpret_cast<const double2 *>(a.pole.xpoles + pb);
+        double2 *dst = reinterpret_cast<double2 *>(pc);
+        constexpr int kPer = (int)(sizeof(R2XPole) / sizeof(double2));
+        for (int i = tid; i < npl * kPer; i += NT) {
+            RX_SMEM(nu_max * stride + i);
+            dst[i] = __ldg(src + i);
+        }
+    }
 
     // ---- A: forward rows
     for (int i = tid; i < nu * D; i += NT) {
-        const int pr = i >> log2D, x = i & (D - 1);
-        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const int pr = i >> LOGD, x = i & (D - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
         const double *in = a.in[f];
         const size_t g = (size_t)(2 * pair) * D + x;
         RX_ASSERT(f < 3 && g + D < (size_t)n);
@@ -1498,11 +1538,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<false>(smem + row * PL, D, log2D, t, tf, a.tw, row < nu);
+        fft_in_smem<false>(smem + row * PL, D, LOGD, t, tf, a.tw, row < nu);
     }
     for (int i = tid; i < nu * H; i += NT) {
-        const int pr = i / H, k = i - pr * H;
-        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const int pr = i >> LOGH, k = i & (H - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
         const cd *Z = smem + pr * PL;
         cd X1, X2;
         if (k == 0) {
@@ -1522,21 +1562,21 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
 
     // ---- B: forward columns of the half spectra -> full spectrum (F(-K) = conj F(K)), D^-2
     for (int i = tid; i < nu * D; i += NT) {
-        const int c = i % nu, l = i / nu;
-        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        const int c = i >> LOGD, l = i & (D - 1);
+        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
         smem[c * stride + pidx(l)] = ld_spec<true>(a.half + (size_t)f * n + (size_t)l * D + k);
     }
     __syncthreads();
     {
         const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<false>(smem + col * stride, D, log2D, t, tf, a.tw, col < nu);
+        fft_in_smem<false>(smem + col * stride, D, LOGD, t, tf, a.tw, col < nu);
     }
     {
         const double sc = a.scale;
         cd *fhat = const_cast<cd *>(a.pole.fhat);
         for (int i = tid; i < nu * D; i += NT) {
-            const int c = i % nu, l = i / nu;
-            const int gc = u0 + c, f = gc / H, k = gc - f * H;
+            const int c = i >> LOGD, l = i & (D - 1);
+            const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
             const int lm = (D - l) & (D - 1);
             const cd v = smem[c * stride + pidx(l)];
             cd *out = fhat + (size_t)f * n;
@@ -1560,18 +1600,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
         const long W = (long)CS * NT - 128;
         const long items = a.n_items;
         const int chunks = a.pole.n_chunks;
-        const long len = a.pole.pole_end - a.pole.pole_begin;
         for (long w = gt; gt < W && w < items * chunks; w += W) {
             const long item = w % items;
             const int chunk = (int)(w / items);
-            const long p0 = a.pole.pole_begin + len * chunk / chunks;
-            const long p1 = a.pole.pole_begin + len * (chunk + 1) / chunks;
+            const long p0 = npl * chunk / chunks;
+            const long p1 = npl * (chunk + 1) / chunks;
             long rep[4];
             bool ok[2];
             double K2;
             XPair st[4];
             r2x_setup<true>(a.pole, item, st, rep, ok, K2);
-            r2x_tile<1>(a.pole.xpoles + p0, (int)(p1 - p0), K2, st);
+            if (cached) r2x_tile<2>(pc + p0, (int)(p1 - p0), K2, st);
+            else r2x_tile<1>(a.pole.xpoles + pb + p0, (int)(p1 - p0), K2, st);
             r2x_store(a.pole, chunk, st, rep, ok);
         }
         if (gt >= W) fixup_k0_warp(a.fix, (int)((gt - W) >> 5), tid & 31);
@@ -1584,8 +1624,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
 
     // ---- E: inverse columns (the accumulator is Hermitian: no symmetrisation)
     for (int i = tid; i < nu * D; i += NT) {
-        const int c = i % nu, l = i / nu;
-        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        const int c = i >> LOGD, l = i & (D - 1);
+        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
         const cd *in = a.fin.acc + (size_t)f * n + (size_t)l * D;
         cd v;
         if (k == 0) {
@@ -1599,19 +1639,19 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<true>(smem + col * stride, D, log2D, t, tf, a.tw, col < nu);
+        fft_in_smem<true>(smem + col * stride, D, LOGD, t, tf, a.tw, col < nu);
     }
     for (int i = tid; i < nu * D; i += NT) {
-        const int c = i % nu, r = i / nu;
-        const int gc = u0 + c, f = gc / H, k = gc - f * H;
+        const int c = i >> LOGD, r = i & (D - 1);
+        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
         a.half[(size_t)f * n + (size_t)r * D + k] = smem[c * stride + pidx(r)];
     }
     cluster_barrier();
 
     // ---- F: inverse rows -> the three real fields
     for (int i = tid; i < nu * H; i += NT) {
-        const int pr = i / H, k = i - pr * H;
-        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const int pr = i >> LOGH, k = i & (H - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
         const size_t g = (size_t)f * n + (size_t)(2 * pair) * D + k;
         const cd g1 = ld_spec<true>(a.half + g), g2 = ld_spec<true>(a.half + g + D);
         cd *Z = smem + pr * PL;
@@ -1626,11 +1666,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<true>(smem + row * PL, D, log2D, t, tf, a.tw, row < nu);
+        fft_in_smem<true>(smem + row * PL, D, LOGD, t, tf, a.tw, row < nu);
     }
     for (int i = tid; i < nu * D; i += NT) {
-        const int pr = i >> log2D, x = i & (D - 1);
-        const int gp = u0 + pr, f = gp / H, pair = gp - f * H;
+        const int pr = i >> LOGD, x = i & (D - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
         const cd v = smem[pr * PL + pidx(x)];
         const size_t g = (size_t)(2 * pair) * D + x;
         a.out[f][g] = v.x;
@@ -1919,21 +1959,31 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pol
 }
 
 // ----------------------------------------------------------------------------- fused small-grid step
+#define REXI_SMALL_LOGD(X) X(2) X(3) X(4) X(5) X(6) X(7)
+
+// FFT slabs of the smaller (8-CTA) cluster's share + the pole cache
+size_t small_step_smem(int D) {
+    const int cs = 8;
+    const int nu = (3 * (D / 2) + cs - 1) / cs;
+    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd) + (size_t)kSmallPoleCache * sizeof(R2XPole);
+}
+
 // Cluster size (16 if the device allows a non-portable cluster of this kernel, else 8), or 0 if
 // cluster launch is unavailable. Cached per process (one device model per run).
 int small_step_cluster() {
     static int cs = -1;
     if (cs >= 0) return cs;
     cs = 0;
-    if (cudaFuncSetAttribute(step_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-        cudaGetLastError();
+#define X(L)                                                                                                  \
+    cudaFuncSetAttribute(step_small_kernel<L>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);             \
+    if (cudaFuncSetAttribute(step_small_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                             (int)small_step_smem(1 << L)) != cudaSuccess) {                                   \
+        cudaGetLastError();                                                                                    \
+        return cs;                                                                                             \
     }
-    // the 8-CTA cluster at D = 128 needs 56 KB of dynamic shared memory per CTA (> the 48 KB default)
-    if (cudaFuncSetAttribute(step_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)small_step_smem(128)) != cudaSuccess) {
-        cudaGetLastError();
-        return cs;
-    }
+    REXI_SMALL_LOGD(X)
+#undef X
+    cudaGetLastError();
     for (int want : {16, 8}) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(want);
@@ -1947,19 +1997,13 @@ int small_step_cluster() {
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, step_small_kernel, &cfg) == cudaSuccess && nclusters >= 1) {
+        if (cudaOccupancyMaxActiveClusters(&nclusters, step_small_kernel<7>, &cfg) == cudaSuccess && nclusters >= 1) {
             cs = want;
             break;
         }
         cudaGetLastError();
     }
     return cs;
-}
-
-size_t small_step_smem(int D) {
-    const int cs = 8;   // the smaller cluster needs the larger per-CTA share
-    const int nu = (3 * (D / 2) + cs - 1) / cs;
-    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd);
 }
 
 long small_step_items(int D) { return r2c_items(D, 2, true); }
@@ -1977,7 +2021,11 @@ cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, step_small_kernel, a);
+#define X(L) \
+    if (a.pole.log2D == L) return cudaLaunchKernelEx(&cfg, step_small_kernel<L>, a);
+    REXI_SMALL_LOGD(X)
+#undef X
+    return cudaErrorInvalidValue;
 }
 
 // ----------------------------------------------------------------------------- 1-D transforms (NEXT-3)

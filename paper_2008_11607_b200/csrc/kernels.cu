@@ -92,18 +92,24 @@ __host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3); }
 // Twiddles w_r = e^{-+2 pi i r step / N}, r = 1..R-1, of one butterfly: w_1, w_2, w_4 from the
 // table (e^{-2 pi i j / N}, j < N), the others as products of two or three of them (<= 3 ulp;
 // the table loads through L1 were the FFT's limiter with one load per r).
-template <int R, bool INV>
+// TWS: the table is in shared memory (fused small-grid step), read with generic loads.
+template <bool TWS>
+__device__ __forceinline__ double2 ld_tw(const double2 *p) {
+    if (TWS) return *p;
+    return __ldg(p);
+}
+template <int R, bool INV, bool TWS = false>
 __device__ __forceinline__ void pass_twiddles(const cd *__restrict__ tw, int step, cd *w) {
     const double2 *t = reinterpret_cast<const double2 *>(tw);
-    const double2 a = __ldg(t + step);
+    const double2 a = ld_tw<TWS>(t + step);
     w[1] = mk(a.x, INV ? -a.y : a.y);
     if (R >= 4) {
-        const double2 b = __ldg(t + 2 * step);
+        const double2 b = ld_tw<TWS>(t + 2 * step);
         w[2] = mk(b.x, INV ? -b.y : b.y);
         w[3] = cmul(w[1], w[2]);
     }
     if (R == 8) {
-        const double2 c4 = __ldg(t + 4 * step);
+        const double2 c4 = ld_tw<TWS>(t + 4 * step);
         w[4] = mk(c4.x, INV ? -c4.y : c4.y);
         w[5] = cmul(w[1], w[4]);
         w[6] = cmul(w[2], w[4]);
@@ -136,7 +142,7 @@ struct PidxIx {
 
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
-template <int R, bool INV, class IX>
+template <int R, bool INV, class IX, bool TWS = false>
 __device__ __forceinline__ void stockham_pass_ix(cd *s, IX ix, int N, int Ns, int t, int tf,
                                                  const cd *__restrict__ tw, bool act) {
     constexpr int PERMAX = 8 / R;
@@ -149,7 +155,7 @@ __device__ __forceinline__ void stockham_pass_ix(cd *s, IX ix, int N, int Ns, in
             const int k = j & (Ns - 1);
             const int step = k * (N / (Ns * R));  // twiddle index step: r * k * N / (Ns R)
             cd w[R];
-            if (Ns > 1) pass_twiddles<R, INV>(tw, step, w);
+            if (Ns > 1) pass_twiddles<R, INV, TWS>(tw, step, w);
             RX_ASSERT(Ns == 1 || R * step < N);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -187,23 +193,23 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
 
 // act = false: the thread only joins the block barriers (blocks with more threads than
 // transforms x tf, e.g. the fused small-grid step)
-template <bool INV, class IX>
+template <bool INV, class IX, bool TWS = false>
 __device__ __forceinline__ void fft_in_smem_ix(cd *s, IX ix, int N, int logN, int t, int tf, const cd *tw,
                                                bool act) {
     int Ns = 1, rem = logN;
     while (rem >= 3) {
-        stockham_pass_ix<8, INV>(s, ix, N, Ns, t, tf, tw, act);
+        stockham_pass_ix<8, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
         Ns <<= 3;
         rem -= 3;
     }
-    if (rem == 2) stockham_pass_ix<4, INV>(s, ix, N, Ns, t, tf, tw, act);
-    else if (rem == 1) stockham_pass_ix<2, INV>(s, ix, N, Ns, t, tf, tw, act);
+    if (rem == 2) stockham_pass_ix<4, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
+    else if (rem == 1) stockham_pass_ix<2, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
 }
 
-template <bool INV>
+template <bool INV, bool TWS = false>
 __device__ __forceinline__ void fft_in_smem(cd *s, int N, int logN, int t, int tf, const cd *tw,
                                             bool act = true) {
-    fft_in_smem_ix<INV>(s, PidxIx{}, N, logN, t, tf, tw, act);
+    fft_in_smem_ix<INV, PidxIx, TWS>(s, PidxIx{}, N, logN, t, tf, tw, act);
 }
 
 // ----------------------------------------------------------------------------- real 2-D FFT
@@ -1033,7 +1039,8 @@ __device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&
             const long mm = rep[2 * g + j];
             RX_ASSERT(mm >= 0 && mm < n_modes);
             const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
-            const double kx = __ldg(&a.ksym[k]), ky = __ldg(&a.ksym[l]);
+            // CG (fused step): ksym may be the CTA's shared-memory copy -> generic loads
+            const double kx = CG ? a.ksym[k] : __ldg(&a.ksym[k]), ky = CG ? a.ksym[l] : __ldg(&a.ksym[l]);
             const cd e = ld_spec<CG>(a.fhat + mm), uu = ld_spec<CG>(a.fhat + n_modes + mm),
                      vv = ld_spec<CG>(a.fhat + 2 * n_modes + mm);
             // delta0 = i (kx u + ky v), zeta0 = i (kx v - ky u)   (tau-scaled)
@@ -1512,8 +1519,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     const int nu_max = (P3 + CS - 1) / CS;
     rx_poison_smem();
     RX_ASSERT(nu <= nu_max && u1 <= P3);
-    // pole cache after the FFT region
+    // pole cache after the FFT region, then the twiddle table (D) and the symbols (D doubles)
     R2XPole *pc = reinterpret_cast<R2XPole *>(smem + nu_max * stride);
+    cd *tws = smem + nu_max * stride + kSmallPoleCache * (int)(sizeof(R2XPole) / sizeof(cd));
+    double *ks = reinterpret_cast<double *>(tws + D);
     const long pb = a.pole.pole_begin, npl = a.pole.pole_end - a.pole.pole_begin;
     const bool cached = npl <= kSmallPoleCache;
     if (cached) {
@@ -1525,6 +1534,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
             dst[i] = __ldg(src + i);
         }
     }
+    for (int i = tid; i < D; i += NT) {
+        RX_SMEM((tws - smem) + i);
+        RX_SMEM((tws - smem) + D + i / 2);
+        tws[i] = a.tw[i];
+        ks[i] = __ldg(a.pole.ksym + i);
+    }
+    __syncthreads();
+    PoleArgs pa = a.pole;
+    pa.ksym = ks;
+    FinishArgs fa = a.fin;
+    fa.ksym = ks;
 
     // ---- A: forward rows
     for (int i = tid; i < nu * D; i += NT) {
@@ -1538,7 +1558,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<false>(smem + row * PL, D, LOGD, t, tf, a.tw, row < nu);
+        fft_in_smem<false, true>(smem + row * PL, D, LOGD, t, tf, tws, row < nu);
     }
     for (int i = tid; i < nu * H; i += NT) {
         const int pr = i >> LOGH, k = i & (H - 1);
@@ -1569,7 +1589,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<false>(smem + col * stride, D, LOGD, t, tf, a.tw, col < nu);
+        fft_in_smem<false, true>(smem + col * stride, D, LOGD, t, tf, tws, col < nu);
     }
     {
         const double sc = a.scale;
@@ -1609,7 +1629,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
             bool ok[2];
             double K2;
             XPair st[4];
-            r2x_setup<true>(a.pole, item, st, rep, ok, K2);
+            r2x_setup<true>(pa, item, st, rep, ok, K2);
             if (cached) r2x_tile<2>(pc + p0, (int)(p1 - p0), K2, st);
             else r2x_tile<1>(a.pole.xpoles + pb + p0, (int)(p1 - p0), K2, st);
             r2x_store(a.pole, chunk, st, rep, ok);
@@ -1619,7 +1639,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     cluster_barrier();
 
     // ---- D: R2C finish of every pair
-    for (long m = (long)cta * NT + tid; m < n; m += (long)CS * NT) finish_r2c_mode<true>(a.fin, m);
+    for (long m = (long)cta * NT + tid; m < n; m += (long)CS * NT) finish_r2c_mode<true>(fa, m);
     cluster_barrier();
 
     // ---- E: inverse columns (the accumulator is Hermitian: no symmetrisation)
@@ -1639,7 +1659,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<true>(smem + col * stride, D, LOGD, t, tf, a.tw, col < nu);
+        fft_in_smem<true, true>(smem + col * stride, D, LOGD, t, tf, tws, col < nu);
     }
     for (int i = tid; i < nu * D; i += NT) {
         const int c = i >> LOGD, r = i & (D - 1);
@@ -1666,7 +1686,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     __syncthreads();
     {
         const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<true>(smem + row * PL, D, LOGD, t, tf, a.tw, row < nu);
+        fft_in_smem<true, true>(smem + row * PL, D, LOGD, t, tf, tws, row < nu);
     }
     for (int i = tid; i < nu * D; i += NT) {
         const int pr = i >> LOGD, x = i & (D - 1);
@@ -1965,7 +1985,8 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pol
 size_t small_step_smem(int D) {
     const int cs = 8;
     const int nu = (3 * (D / 2) + cs - 1) / cs;
-    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd) + (size_t)kSmallPoleCache * sizeof(R2XPole);
+    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd) + (size_t)kSmallPoleCache * sizeof(R2XPole) +
+           (size_t)D * (sizeof(cd) + sizeof(double));
 }
 
 // Cluster size (16 if the device allows a non-portable cluster of this kernel, else 8), or 0 if

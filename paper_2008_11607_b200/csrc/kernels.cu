@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "launch.h"
@@ -77,9 +78,43 @@ __device__ __forceinline__ void dft8(cd *v) {
     v[1] = b[4]; v[3] = b[5]; v[5] = b[6]; v[7] = b[7];
 }
 
+// DFT of length 16 in registers, natural order in and out: n = 4 n1 + n2, k = k1 + 4 k2,
+// X[k1 + 4 k2] = sum_n2 w4^(n2 k2) [w16^(n2 k1) sum_n1 w4^(n1 k1) x[4 n1 + n2]].
+template <bool INV>
+__device__ __forceinline__ void dft16(cd *v) {
+    // cos / sin of 2 pi m / 16, m = 0..9 (products n2 k1 <= 9)
+    constexpr double C[10] = {1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173,
+                              0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128675613,
+                              -1.0, -0.92387953251128675613};
+    constexpr double S[10] = {0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128675613,
+                              1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173,
+                              0.0, -0.38268343236508977173};
+    cd y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+        cd g[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+        dft4<INV>(g);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            const int m = n2 * k1;
+            // w16^m = cos(2 pi m/16) -+ i sin(2 pi m/16) (forward: e^{-})
+            const double c = C[m], sn = INV ? S[m] : -S[m];
+            y[n2][k1] = m == 0 ? g[k1] : mk(g[k1].x * c - g[k1].y * sn, g[k1].x * sn + g[k1].y * c);
+        }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        cd g[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+        dft4<INV>(g);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = g[k2];
+    }
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void dftR(cd *v) {
-    if (R == 8) dft8<INV>(v);
+    if (R == 16) dft16<INV>(v);
+    else if (R == 8) dft8<INV>(v);
     else if (R == 4) dft4<INV>(v);
     else dft2<INV>(v);
 }
@@ -108,12 +143,18 @@ __device__ __forceinline__ void pass_twiddles(const cd *__restrict__ tw, int ste
         w[2] = mk(b.x, INV ? -b.y : b.y);
         w[3] = cmul(w[1], w[2]);
     }
-    if (R == 8) {
+    if (R >= 8) {
         const double2 c4 = ld_tw<TWS>(t + 4 * step);
         w[4] = mk(c4.x, INV ? -c4.y : c4.y);
         w[5] = cmul(w[1], w[4]);
         w[6] = cmul(w[2], w[4]);
         w[7] = cmul(w[3], w[4]);
+    }
+    if (R == 16) {
+        const double2 c8 = ld_tw<TWS>(t + 8 * step);
+        w[8] = mk(c8.x, INV ? -c8.y : c8.y);
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
     }
 }
 
@@ -142,12 +183,13 @@ struct PidxIx {
 
 // One Stockham pass of radix R on the transform at s (length N, current span Ns); thread t of
 // tf threads per transform handles butterflies j = t, t + tf, ... < N/R.
-template <int R, bool INV, class IX, bool TWS = false>
+// V values per thread (8, or 16 for the radix-16 passes): V / R butterflies per thread.
+template <int R, bool INV, class IX, bool TWS = false, int V = 8>
 __device__ __forceinline__ void stockham_pass_ix(cd *s, IX ix, int N, int Ns, int t, int tf,
                                                  const cd *__restrict__ tw, bool act) {
-    constexpr int PERMAX = 8 / R;
+    constexpr int PERMAX = V / R;
     const int nbf = N / R;
-    cd v[8];
+    cd v[V];
 #pragma unroll
     for (int b = 0; b < PERMAX; ++b) {
         const int j = t + b * tf;
@@ -282,6 +324,256 @@ __global__ void __launch_bounds__(1024) fft_rows_fwd_kernel(FftArgs a) {
         RX_ASSERT(g + D < (size_t)D * D && k < H);
         outp[g] = X1;
         outp[g + D] = X2;
+    }
+}
+
+// ----------------------------------------------------------------------------- radix-16 row passes
+// Row passes for 512 <= D <= 8192 with 16 values per thread (T = D/16 threads per transform) and
+// radix-16 Stockham passes: the first pass reads its 16 inputs straight from global memory into
+// registers (x[j + r T], coalesced over j) and the inverse's last pass writes straight to global
+// memory (x[j + r D/R]), so a 4096-point row makes 3 shared-memory round trips instead of 5 —
+// the radix-8 row kernels were bound by the shared-memory pipe (ncu l1tex 80 % at 4096^2).
+// NB row pairs per block keep >= 128 threads. Same arithmetic as the radix-8 path otherwise
+// (separation of the two real rows, packing of X[0], X[N/2] into slot 0).
+template <int LOGD>
+struct Row16 {
+    static constexpr int D = 1 << LOGD, H = D / 2, T = D / 16;
+    static constexpr int NB = T >= 128 ? 1 : 128 / T;
+    static constexpr int PL = padded_len(D);
+};
+
+// radix-16 passes Ns = 16, 256, ... while 4 or more bits remain, then one radix-2/4/8 pass;
+// the caller did the first (Ns = 1) pass. Every thread of the block joins the barriers.
+template <bool INV, int LOGD>
+__device__ __forceinline__ void row16_rest(cd *s, int j, const cd *tw) {
+    constexpr int D = 1 << LOGD, T = D / 16;
+    int Ns = 16, rem = LOGD - 4;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        if (rem >= 4) {
+            stockham_pass_ix<16, INV, PidxIx, false, 16>(s, PidxIx{}, D, Ns, j, T, tw, true);
+            Ns <<= 4;
+            rem -= 4;
+        }
+    }
+    if (rem == 3) stockham_pass_ix<8, INV, PidxIx, false, 16>(s, PidxIx{}, D, Ns, j, T, tw, true);
+    else if (rem == 2) stockham_pass_ix<4, INV, PidxIx, false, 16>(s, PidxIx{}, D, Ns, j, T, tw, true);
+    else if (rem == 1) stockham_pass_ix<2, INV, PidxIx, false, 16>(s, PidxIx{}, D, Ns, j, T, tw, true);
+}
+
+template <int LOGD>
+__global__ void __launch_bounds__(512) fft_rows_fwd16_kernel(FftArgs a) {
+    using L = Row16<LOGD>;
+    constexpr int D = L::D, H = L::H, T = L::T, NB = L::NB, PL = L::PL;
+    extern __shared__ cd smem[];
+    rx_poison_smem();
+    const int f = blockIdx.y;
+    const int pr = threadIdx.x / T, j = threadIdx.x - pr * T;
+    const size_t pair = (size_t)blockIdx.x * NB + pr;
+    const double *inp = static_cast<const double *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *outp = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    cd *s = smem + pr * PL;
+    {
+        cd v[16];
+        const double *r1 = inp + (2 * pair) * D;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_ASSERT((2 * pair + 1) * D + j + r * T < (size_t)D * D);
+            v[r] = mk(__ldg(r1 + j + r * T), __ldg(r1 + D + j + r * T));
+        }
+        dft16<false>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_SMEM(pr * PL + pidx(16 * j + r));
+            s[pidx(16 * j + r)] = v[r];   // Stockham output of the Ns = 1 pass: 16 j + r
+        }
+    }
+    __syncthreads();
+    row16_rest<false, LOGD>(s, j, a.twiddle);
+    const double hs = 0.5 * a.scale;
+    for (int k = j; k < H; k += T) {
+        cd X1, X2;
+        if (k == 0) {
+            const cd z0 = s[pidx(0)], zh = s[pidx(H)];
+            X1 = mk(2.0 * hs * z0.x, 2.0 * hs * zh.x);
+            X2 = mk(2.0 * hs * z0.y, 2.0 * hs * zh.y);
+        } else {
+            const cd zk = s[pidx(k)], zm = s[pidx(D - k)];
+            X1 = mk(hs * (zk.x + zm.x), hs * (zk.y - zm.y));
+            X2 = mk(hs * (zk.y + zm.y), hs * (zm.x - zk.x));
+        }
+        const size_t g = (2 * pair) * D + k;
+        outp[g] = X1;
+        outp[g + D] = X2;
+    }
+}
+
+template <int LOGD>
+__global__ void __launch_bounds__(512) fft_rows_inv16_kernel(FftArgs a) {
+    using L = Row16<LOGD>;
+    constexpr int D = L::D, H = L::H, T = L::T, NB = L::NB, PL = L::PL;
+    extern __shared__ cd smem[];
+    rx_poison_smem();
+    const int f = blockIdx.y;
+    const int pr = threadIdx.x / T, j = threadIdx.x - pr * T;
+    const size_t pair = (size_t)blockIdx.x * NB + pr;
+    const cd *inp = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    double *outp = static_cast<double *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    cd *s = smem + pr * PL;
+    {
+        // Z[p] = g1[p] + i g2[p] over the full circle from the two half-spectrum rows
+        // (g[D - p] = conj g[p]; slot 0 packs the real values at p = 0 and p = H)
+        const cd *g1r = inp + (2 * pair) * D, *g2r = g1r + D;
+        cd v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int p = j + r * T;
+            cd z;
+            if (p == 0) {
+                const cd g1 = g1r[0], g2 = g2r[0];
+                z = mk(g1.x, g2.x);
+            } else if (p == H) {
+                const cd g1 = g1r[0], g2 = g2r[0];
+                z = mk(g1.y, g2.y);
+            } else if (p < H) {
+                const cd g1 = g1r[p], g2 = g2r[p];
+                z = mk(g1.x - g2.y, g1.y + g2.x);        // g1 + i g2
+            } else {
+                const cd g1 = g1r[D - p], g2 = g2r[D - p];
+                z = mk(g1.x + g2.y, g2.x - g1.y);        // conj g1 + i conj g2
+            }
+            v[r] = z;
+        }
+        dft16<true>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_SMEM(pr * PL + pidx(16 * j + r));
+            s[pidx(16 * j + r)] = v[r];
+        }
+    }
+    __syncthreads();
+    row16_rest<true, LOGD>(s, j, a.twiddle);
+    const double sc = a.scale;
+    double *o1 = outp + (2 * pair) * D;
+#pragma unroll 4
+    for (int x = j; x < D; x += T) {
+        const cd v = s[pidx(x)];
+        o1[x] = v.x * sc;
+        o1[x + D] = v.y * sc;
+    }
+}
+
+// ----------------------------------------------------------------------------- radix-16 column passes
+// Column passes for 512 <= D <= 8192: C half-spectrum columns per block, T = D/16 threads per
+// column (thread (c, j), c fastest, so a warp's loads cover C adjacent columns of a row), the
+// first pass straight from global memory into registers, radix-16 Stockham passes in the
+// column slabs, output as in the radix-8 column kernels.
+template <int LOGD>
+struct Col16 {
+    static constexpr int D = 1 << LOGD, H = D / 2, T = D / 16;
+    static constexpr int C = T >= 512 ? 1 : (T >= 256 ? 2 : 4);
+    static constexpr int STRIDE = padded_len(D) + 1;
+};
+
+template <int LOGD>
+__global__ void __launch_bounds__(512) fft_cols_fwd16_kernel(FftArgs a) {
+    using L = Col16<LOGD>;
+    constexpr int D = L::D, H = L::H, T = L::T, C = L::C, STRIDE = L::STRIDE;
+    extern __shared__ cd smem[];
+    rx_poison_smem();
+    const int f = blockIdx.y;
+    const int c = threadIdx.x % C, j = threadIdx.x / C;
+    const int col0 = blockIdx.x * C;
+    const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    cd *s = smem + c * STRIDE;
+    {
+        cd v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_ASSERT(col0 + c < H);
+            v[r] = in[(size_t)(j + r * T) * D + col0 + c];
+        }
+        dft16<false>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_SMEM(c * STRIDE + pidx(16 * j + r));
+            s[pidx(16 * j + r)] = v[r];
+        }
+    }
+    __syncthreads();
+    row16_rest<false, LOGD>(s, j, a.twiddle);
+    const double sc = a.scale;
+    for (int i = threadIdx.x; i < C * D; i += blockDim.x) {
+        const int l = i / C, cc = i % C;
+        const int k = col0 + cc;
+        const int lm = (D - l) & (D - 1);
+        const cd v = smem[cc * STRIDE + pidx(l)];
+        if (k == 0) {
+            // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
+            // FH = (G - conj G(-l)) / (2i)
+            const cd w = smem[cc * STRIDE + pidx(lm)];
+            const double hs = 0.5 * sc;
+            out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+            out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+        } else {
+            out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+            out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
+        }
+    }
+}
+
+template <int LOGD, bool SYM>
+__global__ void __launch_bounds__(512) fft_cols_inv16_kernel(FftArgs a) {
+    using L = Col16<LOGD>;
+    constexpr int D = L::D, H = L::H, T = L::T, C = L::C, STRIDE = L::STRIDE;
+    extern __shared__ cd smem[];
+    rx_poison_smem();
+    const int f = blockIdx.y;
+    const int c = threadIdx.x % C, j = threadIdx.x / C;
+    const int col0 = blockIdx.x * C;
+    const int k = col0 + c;
+    const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    cd *s = smem + c * STRIDE;
+    {
+        cd v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = j + r * T;
+            const int lm = (D - l) & (D - 1);
+            RX_ASSERT(k < H && l < D);
+            if (k == 0) {
+                cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
+                if (SYM) {
+                    const cd m0 = in[(size_t)lm * D], mh = in[(size_t)lm * D + H];
+                    t0 = mk(0.5 * (t0.x + m0.x), 0.5 * (t0.y - m0.y));
+                    th = mk(0.5 * (th.x + mh.x), 0.5 * (th.y - mh.y));
+                }
+                v[r] = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+            } else {
+                cd t = in[(size_t)l * D + k];
+                if (SYM) {
+                    const cd m = in[(size_t)lm * D + (D - k)];
+                    t = mk(0.5 * (t.x + m.x), 0.5 * (t.y - m.y));
+                }
+                v[r] = t;
+            }
+        }
+        dft16<true>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            RX_SMEM(c * STRIDE + pidx(16 * j + r));
+            s[pidx(16 * j + r)] = v[r];
+        }
+    }
+    __syncthreads();
+    row16_rest<true, LOGD>(s, j, a.twiddle);
+    const double sc = a.scale;
+    for (int i = threadIdx.x; i < C * D; i += blockDim.x) {
+        const int r = i / C, cc = i % C;
+        const cd v = smem[cc * STRIDE + pidx(r)];
+        out[(size_t)r * D + col0 + cc] = mk(v.x * sc, v.y * sc);
     }
 }
 
@@ -1707,17 +1999,31 @@ static int ilog2(int x) {
 // FFT launch shapes: threads per transform tf = max(1, D/8); a row block holds nb row pairs
 // (nb * tf <= 64 threads unless one pair needs more, nb <= D/2); a column block a strip of
 // C <= 4 half-spectrum slots (C * tf <= 512, C <= D/2).
+// REXI_FFT_ROWS / REXI_FFT_COLS (environment, read once): override the row pairs / columns per
+// block of the FFT passes — a tuning knob for measurements (tools/time_fft.py), not a setting.
+static int fft_env(const char *name) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : 0;
+}
 static int fft_rows_per_block(int D) {
+    static const int force = fft_env("REXI_FFT_ROWS");
     const int tf = D >= 8 ? D / 8 : 1;
-    int nb = 64 / tf;   // small blocks: the passes are latency-bound, more blocks in flight help
+    int nb = force > 0 ? force : 64 / tf;   // small blocks: latency-bound passes, more blocks in flight
     if (nb < 1) nb = 1;
+    if (nb * tf > 1024) nb = 1024 / tf;
     if (nb > D / 2) nb = D / 2;
     return nb;
 }
 static int fft_cols_per_block(int D) {
+    static const int force = fft_env("REXI_FFT_COLS");
     const int tf = D >= 8 ? D / 8 : 1;
-    int C = 512 / tf;
-    if (C > 4) C = 4;   // measured: 4-column slabs beat 8 at 512^2 (more blocks), equal at 1024^2
+    // measured (tools/time_fft.py, profiles/r02l_fft_tune.log): 4-column slabs beat 8 at 512^2
+    // and 1024^2; at 4096^2 two columns per 1024-thread block (32-byte sectors per row instead
+    // of 16 bytes) beat one: forward 1058 -> 887 us, inverse 901 -> 871 us
+    int C = std::max(2, 512 / tf);
+    if (C > 4) C = 4;
+    if (force > 0) C = force;
+    if (C * tf > 1024) C = 1024 / tf;
     if (C < 1) C = 1;
     if (C > D / 2) C = D / 2;
     return C;
@@ -1732,6 +2038,15 @@ cudaError_t fft_setup_attributes() {
     SETA(fft_cols_inv_kernel<true>)
     SETA(fft_cols_inv_kernel<false>)
     SETA(fft_rows_inv_kernel)
+    SETA(fft_rows_fwd16_kernel<9>) SETA(fft_rows_fwd16_kernel<10>) SETA(fft_rows_fwd16_kernel<11>)
+    SETA(fft_rows_fwd16_kernel<12>) SETA(fft_rows_fwd16_kernel<13>)
+    SETA(fft_rows_inv16_kernel<9>) SETA(fft_rows_inv16_kernel<10>) SETA(fft_rows_inv16_kernel<11>)
+    SETA(fft_rows_inv16_kernel<12>) SETA(fft_rows_inv16_kernel<13>)
+    SETA(fft_cols_fwd16_kernel<9>) SETA(fft_cols_fwd16_kernel<10>) SETA(fft_cols_fwd16_kernel<11>)
+    SETA(fft_cols_fwd16_kernel<12>) SETA(fft_cols_fwd16_kernel<13>)
+#define SETB(L) SETA((fft_cols_inv16_kernel<L, false>)) SETA((fft_cols_inv16_kernel<L, true>))
+    SETB(9) SETB(10) SETB(11) SETB(12) SETB(13)
+#undef SETB
 #undef SETA
     return cudaSuccess;
 }
@@ -1749,21 +2064,77 @@ static FftArgs fft_args(const void *const in[3], void *const out[3], const cd *t
     return a;
 }
 
+// radix-16 row kernels for 512 <= D <= 8192 (REXI_FFT_R16=0 in the environment selects the
+// radix-8 row kernels instead: a measurement knob)
+static bool fft16_rows(int lg) {
+    static const int off = [] { const char *v = getenv("REXI_FFT_R16"); return v && atoi(v) == 0; }();
+    return !off && lg >= 9 && lg <= 13;
+}
+
+// radix-16 column kernels for 512 <= D <= 8192 (REXI_FFT_C16=0 selects the radix-8 ones)
+static bool fft16_cols(int lg) {
+    static const int off = [] { const char *v = getenv("REXI_FFT_C16"); return v && atoi(v) == 0; }();
+    return !off && lg >= 9 && lg <= 13;
+}
+
+// mode 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising
+static cudaError_t launch_cols16(int mode, const void *const i3[3], void *const o3[3], const cd *tw, int D,
+                                 double scale, cudaStream_t st) {
+#define COLS16(L)                                                                                        \
+    if (D == (1 << L)) {                                                                                 \
+        using CL = Col16<L>;                                                                             \
+        const FftArgs a = fft_args(i3, o3, tw, D, CL::C, mode ? 1 : 0, scale);                          \
+        const dim3 grid((D / 2) / CL::C, 3);                                                             \
+        const size_t sm = (size_t)CL::C * CL::STRIDE * sizeof(cd);                                      \
+        if (mode == 0) fft_cols_fwd16_kernel<L><<<grid, CL::C * CL::T, sm, st>>>(a);                     \
+        else if (mode == 1) fft_cols_inv16_kernel<L, false><<<grid, CL::C * CL::T, sm, st>>>(a);         \
+        else fft_cols_inv16_kernel<L, true><<<grid, CL::C * CL::T, sm, st>>>(a);                         \
+        return cudaGetLastError();                                                                       \
+    }
+    COLS16(9) COLS16(10) COLS16(11) COLS16(12) COLS16(13)
+#undef COLS16
+    return cudaErrorInvalidValue;
+}
+
+static cudaError_t launch_rows16(bool fwd, const void *const i3[3], void *const o3[3], const cd *tw, int D,
+                                 cudaStream_t st) {
+#define ROWS16(L)                                                                                        \
+    if (D == (1 << L)) {                                                                                 \
+        using RL = Row16<L>;                                                                             \
+        const FftArgs a = fft_args(i3, o3, tw, D, RL::NB, fwd ? 0 : 1, 1.0);                            \
+        const dim3 grid((D / 2) / RL::NB, 3);                                                            \
+        const size_t sm = (size_t)RL::NB * RL::PL * sizeof(cd);                                         \
+        if (fwd) fft_rows_fwd16_kernel<L><<<grid, RL::NB * RL::T, sm, st>>>(a);                          \
+        else fft_rows_inv16_kernel<L><<<grid, RL::NB * RL::T, sm, st>>>(a);                              \
+        return cudaGetLastError();                                                                       \
+    }
+    ROWS16(9) ROWS16(10) ROWS16(11) ROWS16(12) ROWS16(13)
+#undef ROWS16
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
                                const cd *tw, int D, double scale, cudaStream_t st) {
     const int tf = D >= 8 ? D / 8 : 1;
     {
         const void *i3[3] = {in[0], in[1], in[2]};
         void *o3[3] = {half[0], half[1], half[2]};
-        const FftArgs a = fft_args(i3, o3, tw, D, fft_rows_per_block(D), 0, 1.0);
-        const dim3 grid((D / 2) / a.per_block, 3);
-        const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
-        fft_rows_fwd_kernel<<<grid, a.per_block * tf, sm, st>>>(a);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
+        const int lg = ilog2(D);
+        if (fft16_rows(lg)) {
+            cudaError_t e = launch_rows16(true, i3, o3, tw, D, st);
+            if (e != cudaSuccess) return e;
+        } else {
+            const FftArgs a = fft_args(i3, o3, tw, D, fft_rows_per_block(D), 0, 1.0);
+            const dim3 grid((D / 2) / a.per_block, 3);
+            const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);
+            fft_rows_fwd_kernel<<<grid, a.per_block * tf, sm, st>>>(a);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
     }
     const void *i3[3] = {half[0], half[1], half[2]};
     void *o3[3] = {out[0], out[1], out[2]};
+    if (fft16_cols(ilog2(D))) return launch_cols16(0, i3, o3, tw, D, scale, st);
     const FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 0, scale);
     const dim3 grid((D / 2) / a.per_block, 3);
     const size_t sm = (size_t)a.per_block * col_stride(D, a.per_block) * sizeof(cd);
@@ -1774,7 +2145,12 @@ cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd 
 cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double *const out[3],
                                bool hermitian, const cd *tw, int D, cudaStream_t st) {
     const int tf = D >= 8 ? D / 8 : 1;
-    {
+    if (fft16_cols(ilog2(D))) {
+        const void *i3[3] = {in[0], in[1], in[2]};
+        void *o3[3] = {half[0], half[1], half[2]};
+        cudaError_t e = launch_cols16(hermitian ? 1 : 2, i3, o3, tw, D, 1.0, st);
+        if (e != cudaSuccess) return e;
+    } else {
         const void *i3[3] = {in[0], in[1], in[2]};
         void *o3[3] = {half[0], half[1], half[2]};
         const FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 1, 1.0);
@@ -1787,6 +2163,7 @@ cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double 
     }
     const void *i3[3] = {half[0], half[1], half[2]};
     void *o3[3] = {out[0], out[1], out[2]};
+    if (fft16_rows(ilog2(D))) return launch_rows16(false, i3, o3, tw, D, st);
     const FftArgs a = fft_args(i3, o3, tw, D, fft_rows_per_block(D), 1, 1.0);
     const dim3 grid((D / 2) / a.per_block, 3);
     const size_t sm = (size_t)a.per_block * padded_len(D) * sizeof(cd);

@@ -471,7 +471,9 @@ __global__ void __launch_bounds__(512) fft_rows_inv16_kernel(FftArgs a) {
 template <int LOGD>
 struct Col16 {
     static constexpr int D = 1 << LOGD, H = D / 2, T = D / 16;
-    static constexpr int C = T >= 512 ? 1 : (T >= 256 ? 2 : 4);
+    // 512 threads per block: C = 8 / 4 / 2 / 1 columns at D = 1024 / 2048 / 4096 / 8192 (the widest
+    // row segment per load; measured best or equal against C = 1, 4, 8: profiles/r02o_fft16c.log)
+    static constexpr int C = 512 / T >= 1 ? 512 / T : 1;
     static constexpr int STRIDE = padded_len(D) + 1;
 };
 
@@ -2074,7 +2076,9 @@ static bool fft16_rows(int lg) {
 // radix-16 column kernels for 512 <= D <= 8192 (REXI_FFT_C16=0 selects the radix-8 ones)
 static bool fft16_cols(int lg) {
     static const int off = [] { const char *v = getenv("REXI_FFT_C16"); return v && atoi(v) == 0; }();
-    return !off && lg >= 9 && lg <= 13;
+    // measured (profiles/r02n_fft16.log): radix-16 columns lose at 512^2 (19.5 vs 17.9 us
+    // forward), win from 1024^2 on (-14 % at 1024^2, -22 % at 4096^2 with the radix-16 rows)
+    return !off && lg >= 10 && lg <= 13;
 }
 
 // mode 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising

@@ -18,7 +18,11 @@ n = D * D
 algo = {  # bytes that must move per launch (3 fields)
     "fft_rows_fwd_kernel": 3 * n * (8 + 8),         # real rows in, half-spectrum rows out
     "fft_cols_fwd_kernel": 3 * n * (8 + 16),        # half spectrum in, full spectrum out
-    "fft_cols_inv_kernel": 3 * n * (16 + 8),        # full (or Hermitian-known) spectrum in, half out
+    "fft_cols_inv_kernel": 3 * n * (8 + 8),         # Hermitian accumulator: half columns in, half out
+    "fft_rows_fwd16_kernel": 3 * n * (8 + 8),
+    "fft_cols_fwd16_kernel": 3 * n * (8 + 16),
+    "fft_cols_inv16_kernel": 3 * n * (8 + 8),
+    "fft_rows_inv16_kernel": 3 * n * (8 + 8),
     "fft_rows_inv_kernel": 3 * n * (8 + 8),         # half-spectrum rows in, real rows out
     "finish_kernel": None,
     "fixup_k0_kernel": None,
@@ -30,8 +34,8 @@ ir, iw = col("dram__bytes_read.sum"), col("dram__bytes_write.sum")
 unit_r = rows[1][ir]
 print(f"# Non-pole kernels at {D}^2 (ncu --set full, cold cache)\n")
 print(f"HBM peak: {peak} GB/s (MEASURED_PEAKS.json `hbm_gbs`, of measured).\n")
-print("| kernel | time (us) | DRAM read+write (MB) | algorithmic (MB) | DRAM GB/s | of measured peak |")
-print("|---|---|---|---|---|---|")
+print("| kernel | time (us) | DRAM read+write (MB) | algorithmic (MB) | DRAM GB/s | DRAM of measured peak | algorithmic GB/s | algorithmic of measured peak |")
+print("|---|---|---|---|---|---|---|---|")
 scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
 for r in rows[2:]:
     name = r[ik].split("(")[0].replace("void ", "").replace("rexi::", "")
@@ -43,4 +47,5 @@ for r in rows[2:]:
         float(r[iw].replace(",", "")) * scale.get(rows[1][iw], 1e-6)
     al = algo.get(base)
     gbs = mb * 1e6 / (t_us * 1e-6) / 1e9
-    print(f"| `{name}` | {t_us:.1f} | {mb:.2f} | {al / 1e6 if al else float('nan'):.2f} | {gbs:.0f} | {gbs / peak:.2f} |")
+    alg = (al / 1e6) / t_us * 1e6 / 1e3 if al else float('nan')   # algorithmic GB/s
+    print(f"| `{name}` | {t_us:.1f} | {mb:.2f} | {al / 1e6 if al else float('nan'):.2f} | {gbs:.0f} | {gbs / peak:.2f} | {alg:.0f} | {alg / peak:.2f} |")

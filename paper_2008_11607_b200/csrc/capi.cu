@@ -233,14 +233,17 @@ rexi_status_t record(rexi_plan_s *p, cudaStream_t st, bool start) {
     return REXI_OK;
 }
 
+// half_out: write only the spectrum's rows l <= D/2, which hold the representative of every
+// {K, -K} pair — enough for the R2C pole kernels and their finish / fix-up (internal steps only;
+// rexi_forward writes the full spectrum)
 rexi_status_t do_forward(rexi_plan_s *p, const double *eta, const double *u, const double *v,
-                         cd *fhat, cudaStream_t st) {
+                         cd *fhat, cudaStream_t st, bool half_out = false) {
     const long n = p->n_modes;
     const int D = p->host.D;
     const double *in[3] = {eta, u, v};
     cd *half[3] = {p->d_tmp, p->d_tmp + n, p->d_tmp + 2 * n};
     cd *out[3] = {fhat, fhat + n, fhat + 2 * n};
-    CK(rexi::launch_fft_forward(in, half, out, p->d_tw, D, 1.0 / ((double)D * (double)D), st));
+    CK(rexi::launch_fft_forward(in, half, out, p->d_tw, D, 1.0 / ((double)D * (double)D), st, half_out));
     p->launches += 2;
     return REXI_OK;
 }
@@ -261,8 +264,10 @@ rexi_status_t do_inverse(rexi_plan_s *p, const cd *acc, double *eta, double *u, 
 
 // real_input: fhat is the spectrum of real fields (Hermitian), so the R2C pair kernel may be
 // used; rexi_poles (arbitrary complex spectra) passes false.
+// half_acc (R2C kinds): the finish writes only the modes with k <= D/2, all that the inverse
+// transform of the Hermitian accumulator reads (internal physical steps only)
 rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, cudaStream_t st,
-                       bool real_input) {
+                       bool real_input, bool half_acc = false) {
     const long n = p->n_modes;
     if (e <= b) {
         CK(cudaMemsetAsync(acc, 0, sizeof(cd) * 3 * (size_t)n, st));
@@ -373,6 +378,7 @@ rexi_status_t do_poles(rexi_plan_s *p, long b, long e, const cd *fhat, cd *acc, 
     f.sk_ctas = sk_ctas;
     f.sk_poles = e - b;
     f.partial_cap = 3 * n * (long)p->max_chunks;
+    f.half_out = (half_acc && kd >= 6) ? 1 : 0;
     if (sk_tiles) CK(rexi::launch_finish_r2c_sk(f, st));
     else CK(rexi::launch_finish(f, st));
     p->launches += 2;
@@ -494,6 +500,7 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     f.S = S;
     f.Sd = Sd;
     f.partial_cap = q.partial_cap;
+    f.half_out = 1;   // stage E reads the columns k <= D/2 only
     rexi::FixupArgs &x = a.fix;
     x.method = p->method;
     x.write_eta = 1;
@@ -540,9 +547,10 @@ rexi_status_t do_step_direct(rexi_plan_s *p, long b, long e, const double *eta, 
     }
     if (small_eligible(p, b, e)) return do_step_small(p, b, e, eta, u, v, eo, uo, vo, st);
     rexi_status_t s;
-    if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
-    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true)) != REXI_OK) return s;
-    return do_inverse(p, p->d_acc, eo, uo, vo, st, p->kind() >= 6);
+    const bool r2c = p->kind() >= 6;
+    if ((s = do_forward(p, eta, u, v, p->d_fhat, st, r2c)) != REXI_OK) return s;
+    if ((s = do_poles(p, b, e, p->d_fhat, p->d_acc, st, true, r2c)) != REXI_OK) return s;
+    return do_inverse(p, p->d_acc, eo, uo, vo, st, r2c);
 }
 
 // One spectral-resident step: acc = poles(fhat), fhat = H(acc) (the Re projection, spectral).
@@ -1097,7 +1105,7 @@ rexi_status_t rexi_run(rexi_plan_t p, int steps, double *eta, double *u, double 
         if (steps == 1) return do_step(p, 0, N1, eta, u, v, eta, u, v, st);
         // spectral-resident: forward once, (poles + Re projection) per step, inverse once
         rexi_status_t s;
-        if ((s = do_forward(p, eta, u, v, p->d_fhat, st)) != REXI_OK) return s;
+        if ((s = do_forward(p, eta, u, v, p->d_fhat, st, p->kind() >= 6)) != REXI_OK) return s;
         for (int k = 0; k < steps; ++k)
             if ((s = do_spectral_step(p, 0, N1, st)) != REXI_OK) return s;
         return do_inverse(p, p->d_fhat, eta, u, v, st, true);

@@ -511,16 +511,19 @@ __global__ void __launch_bounds__(512) fft_cols_fwd16_kernel(FftArgs a) {
         const int k = col0 + cc;
         const int lm = (D - l) & (D - 1);
         const cd v = smem[cc * STRIDE + pidx(l)];
+        const bool lo = !a.half_out || l <= H, mlo = !a.half_out || lm <= H;
         if (k == 0) {
             // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
             // FH = (G - conj G(-l)) / (2i)
-            const cd w = smem[cc * STRIDE + pidx(lm)];
-            const double hs = 0.5 * sc;
-            out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
-            out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            if (lo) {
+                const cd w = smem[cc * STRIDE + pidx(lm)];
+                const double hs = 0.5 * sc;
+                out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+                out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            }
         } else {
-            out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
-            out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
+            if (lo) out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+            if (mlo) out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
         }
     }
 }
@@ -620,16 +623,19 @@ __global__ void __launch_bounds__(1024) fft_cols_fwd_kernel(FftArgs a) {
         const int lm = (D - l) & (D - 1);
         RX_ASSERT(l < D && k < (D >> 1));
         const cd v = smem[c * stride + pidx(l)];
+        const bool lo = !a.half_out || l <= (D >> 1), mlo = !a.half_out || lm <= (D >> 1);
         if (k == 0) {
             // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
             // FH = (G - conj G(-l)) / (2i)
-            const cd w = smem[c * stride + pidx(lm)];
-            const double hs = 0.5 * sc;
-            out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
-            out[(size_t)l * D + (D >> 1)] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            if (lo) {
+                const cd w = smem[c * stride + pidx(lm)];
+                const double hs = 0.5 * sc;
+                out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+                out[(size_t)l * D + (D >> 1)] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            }
         } else {
-            out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
-            out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
+            if (lo) out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+            if (mlo) out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
         }
     }
 }
@@ -1542,12 +1548,17 @@ __device__ __forceinline__ void finish_r2c_mode(const FinishArgs &a, long m) {
     const cd t = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
     const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
     const cd U = mk(t.y * inv, -t.x * inv), V = mk(w.y * inv, -w.x * inv);
-    a.acc[m] = h0;
-    a.acc[n + m] = U;
-    a.acc[2 * n + m] = V;
-    a.acc[mm] = mk(h0.x, -h0.y);   // the Hermitian spectrum at -K is the conjugate
-    a.acc[n + mm] = mk(U.x, -U.y);
-    a.acc[2 * n + mm] = mk(V.x, -V.y);
+    const int H = a.D >> 1, km = (a.D - k) & (a.D - 1);
+    if (!a.half_out || k <= H) {
+        a.acc[m] = h0;
+        a.acc[n + m] = U;
+        a.acc[2 * n + m] = V;
+    }
+    if (!a.half_out || km <= H) {
+        a.acc[mm] = mk(h0.x, -h0.y);   // the Hermitian spectrum at -K is the conjugate
+        a.acc[n + mm] = mk(U.x, -U.y);
+        a.acc[2 * n + mm] = mk(V.x, -V.y);
+    }
 }
 
 // ============================================================================= finish
@@ -2062,6 +2073,7 @@ static FftArgs fft_args(const void *const in[3], void *const out[3], const cd *t
     a.log2D = ilog2(D);
     a.per_block = per_block;
     a.inverse = inverse;
+    a.half_out = 0;
     a.scale = scale;
     return a;
 }
@@ -2083,11 +2095,12 @@ static bool fft16_cols(int lg) {
 
 // mode 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising
 static cudaError_t launch_cols16(int mode, const void *const i3[3], void *const o3[3], const cd *tw, int D,
-                                 double scale, cudaStream_t st) {
+                                 double scale, cudaStream_t st, bool half_out = false) {
 #define COLS16(L)                                                                                        \
     if (D == (1 << L)) {                                                                                 \
         using CL = Col16<L>;                                                                             \
-        const FftArgs a = fft_args(i3, o3, tw, D, CL::C, mode ? 1 : 0, scale);                          \
+        FftArgs a = fft_args(i3, o3, tw, D, CL::C, mode ? 1 : 0, scale);                                \
+        a.half_out = half_out ? 1 : 0;                                                                   \
         const dim3 grid((D / 2) / CL::C, 3);                                                             \
         const size_t sm = (size_t)CL::C * CL::STRIDE * sizeof(cd);                                      \
         if (mode == 0) fft_cols_fwd16_kernel<L><<<grid, CL::C * CL::T, sm, st>>>(a);                     \
@@ -2118,7 +2131,7 @@ static cudaError_t launch_rows16(bool fwd, const void *const i3[3], void *const 
 }
 
 cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
-                               const cd *tw, int D, double scale, cudaStream_t st) {
+                               const cd *tw, int D, double scale, cudaStream_t st, bool half_out) {
     const int tf = D >= 8 ? D / 8 : 1;
     {
         const void *i3[3] = {in[0], in[1], in[2]};
@@ -2138,8 +2151,9 @@ cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd 
     }
     const void *i3[3] = {half[0], half[1], half[2]};
     void *o3[3] = {out[0], out[1], out[2]};
-    if (fft16_cols(ilog2(D))) return launch_cols16(0, i3, o3, tw, D, scale, st);
-    const FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 0, scale);
+    if (fft16_cols(ilog2(D))) return launch_cols16(0, i3, o3, tw, D, scale, st, half_out);
+    FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 0, scale);
+    a.half_out = half_out ? 1 : 0;
     const dim3 grid((D / 2) / a.per_block, 3);
     const size_t sm = (size_t)a.per_block * col_stride(D, a.per_block) * sizeof(cd);
     fft_cols_fwd_kernel<<<grid, a.per_block * tf, sm, st>>>(a);

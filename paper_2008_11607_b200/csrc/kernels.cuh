@@ -122,6 +122,8 @@ struct FinishArgs {
     int sk_slots, sk_ctas;
     long sk_poles;         // pole-range length
     long partial_cap;      // complex values in `partial` (REXI_CHECKED)
+    int half_out;          // R2C kinds: write only the modes with k <= D/2 (what the inverse
+                           // transform of a Hermitian spectrum reads), not both modes of a pair
 };
 
 struct FixupArgs {
@@ -162,6 +164,8 @@ struct FftArgs {
     int per_block;         // rows (row pass) or columns (column pass) per block
     int inverse;           // 0: e^{-}, 1: e^{+}
     double scale;
+    int half_out;          // forward columns: write only rows l <= D/2 of the spectrum (every
+                           // representative of a {K, -K} pair; the R2C consumers read no other)
 };
 
 }  // namespace rexi

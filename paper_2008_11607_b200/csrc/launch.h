@@ -12,8 +12,9 @@ void set_last_error(const char *msg);
 
 cudaError_t fft_setup_attributes();
 // S1: real fields -> full spectrum (x scale); half = D x D complex scratch per field.
+// half_out: only rows l <= D/2 of the spectrum are written (the R2C pole kernels' inputs)
 cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd *const out[3],
-                               const cd *tw, int D, double scale, cudaStream_t st);
+                               const cd *tw, int D, double scale, cudaStream_t st, bool half_out = false);
 // S5: Re(IDFT(in)) -> real fields; hermitian: in is known Hermitian (skip symmetrisation).
 cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double *const out[3],
                                bool hermitian, const cd *tw, int D, cudaStream_t st);

@@ -17,14 +17,14 @@ peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PE
 n = D * D
 algo = {  # bytes that must move per launch (3 fields)
     "fft_rows_fwd_kernel": 3 * n * (8 + 8),         # real rows in, half-spectrum rows out
-    "fft_cols_fwd_kernel": 3 * n * (8 + 16),        # half spectrum in, full spectrum out
+    "fft_cols_fwd_kernel": 3 * n * (8 + 8),         # half spectrum in, rows l <= D/2 out (apply path)
     "fft_cols_inv_kernel": 3 * n * (8 + 8),         # Hermitian accumulator: half columns in, half out
     "fft_rows_fwd16_kernel": 3 * n * (8 + 8),
-    "fft_cols_fwd16_kernel": 3 * n * (8 + 16),
+    "fft_cols_fwd16_kernel": 3 * n * (8 + 8),       # apply path: rows l <= D/2 of the spectrum only
     "fft_cols_inv16_kernel": 3 * n * (8 + 8),
     "fft_rows_inv16_kernel": 3 * n * (8 + 8),
     "fft_rows_inv_kernel": 3 * n * (8 + 8),         # half-spectrum rows in, real rows out
-    "finish_kernel": None,
+    "finish_kernel": None,   # chunk partials in (chunks x 32 B per pair) + 48 B per k <= D/2 mode out
     "fixup_k0_kernel": None,
 }
 def col(name):

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <complex>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -466,6 +467,11 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     a.tw = p->d_tw;
     a.scale = 1.0 / ((double)D * (double)D);
     a.n_items = items;
+    {
+        // measurement knob: REXI_SMALL_STOP=k ends the kernel after stage k (results invalid)
+        static const int stop = [] { const char *v = getenv("REXI_SMALL_STOP"); return v ? atoi(v) : 99; }();
+        a.stop_after = stop;
+    }
     rexi::PoleArgs &q = a.pole;
     q = rexi::PoleArgs{};
     q.fhat = p->d_fhat;

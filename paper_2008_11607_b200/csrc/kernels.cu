@@ -1822,6 +1822,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     const int u0 = (int)((long)P3 * cta / CS), u1 = (int)((long)P3 * (cta + 1) / CS);
     const int nu = u1 - u0;          // this CTA's row pairs / columns
     const int nu_max = (P3 + CS - 1) / CS;
+    if (a.stop_after < -1) return;   // stage-timing measurements only
     rx_poison_smem();
     RX_ASSERT(nu <= nu_max && u1 <= P3);
     // pole cache after the FFT region, then the twiddle table (D) and the symbols (D doubles)
@@ -1850,6 +1851,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     pa.ksym = ks;
     FinishArgs fa = a.fin;
     fa.ksym = ks;
+    if (a.stop_after < 0) return;   // stage-timing measurements only
 
     // ---- A: forward rows
     for (int i = tid; i < nu * D; i += NT) {
@@ -1885,6 +1887,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     }
     cluster_barrier();
 
+    if (a.stop_after <= 0) return;   // stage-timing measurements only
     // ---- B: forward columns of the half spectra -> full spectrum (F(-K) = conj F(K)), D^-2
     for (int i = tid; i < nu * D; i += NT) {
         const int c = i >> LOGD, l = i & (D - 1);
@@ -1918,6 +1921,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     }
     cluster_barrier();
 
+    if (a.stop_after <= 1) return;   // stage-timing measurements only
     // ---- C: pole loop (thread = (octet item, pole chunk)) and the K = 0 corners
     {
         // every thread but the last four warps of the cluster works on (item, chunk) units
@@ -1943,10 +1947,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     }
     cluster_barrier();
 
+    if (a.stop_after <= 2) return;   // stage-timing measurements only
     // ---- D: R2C finish of every pair
     for (long m = (long)cta * NT + tid; m < n; m += (long)CS * NT) finish_r2c_mode<true>(fa, m);
     cluster_barrier();
 
+    if (a.stop_after <= 3) return;   // stage-timing measurements only
     // ---- E: inverse columns (the accumulator is Hermitian: no symmetrisation)
     for (int i = tid; i < nu * D; i += NT) {
         const int c = i >> LOGD, l = i & (D - 1);
@@ -1973,6 +1979,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     }
     cluster_barrier();
 
+    if (a.stop_after <= 4) return;   // stage-timing measurements only
     // ---- F: inverse rows -> the three real fields
     for (int i = tid; i < nu * H; i += NT) {
         const int pr = i >> LOGH, k = i & (H - 1);

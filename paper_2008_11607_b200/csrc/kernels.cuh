@@ -153,6 +153,7 @@ struct SmallArgs {
     const cd *tw;
     double scale;          // D^-2
     long n_items;          // octet work items (r2c_items(D, 2, true))
+    int stop_after;        // measurement only (REXI_SMALL_STOP): return after stage 0..5 (A..F)
 };
 
 // ----------------------------------------------------------------------------- FFT passes

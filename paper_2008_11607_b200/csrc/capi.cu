@@ -181,7 +181,8 @@ rexi_status_t check_plan(rexi_plan_t p) {
 // 4 poles per chunk.
 int choose_chunks(const rexi_plan_s *p, long n_range, int v) {
     if (n_range <= 0) return 0;
-    const long tiles = v >= 6 ? rexi::pole_r2c_blocks(p->host.D, p->mpt[v])
+    const long tiles = v == 7   ? rexi::pole_r2x_blocks(p->host.D, p->minb[v])
+                       : v == 6 ? rexi::pole_r2c_blocks(p->host.D, p->mpt[v])
                               : (p->n_modes + rexi::pole_modes_per_block(p->mpt[v]) - 1) /
                                     rexi::pole_modes_per_block(p->mpt[v]);
     int &occ = const_cast<rexi_plan_s *>(p)->occ_cache[v];

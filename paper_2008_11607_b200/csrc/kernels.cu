@@ -1377,16 +1377,16 @@ __device__ __forceinline__ void r2x_store(const PoleArgs &a, int chunk, const XP
     }
 }
 
-// grid = (octet-item tiles of 128, pole chunks); a thread owns one octet item (four {K, -K}
+// grid = (octet-item tiles of BS, pole chunks); a thread owns one octet item (four {K, -K}
 // pairs with one K2, r2c_octet_item) and runs every pole of its chunk.
-template <int PU, int MINB>
-__global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) {
+template <int PU, int MINB, int BS = kPoleBlock>
+__global__ void __launch_bounds__(BS, MINB) pole_kernel_r2x(PoleArgs a) {
     __shared__ R2XPole sp[kR2CTile];
     const int chunk = blockIdx.y;
     const long len = a.pole_end - a.pole_begin;
     const long p0 = a.pole_begin + len * chunk / a.n_chunks;
     const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
-    const long item = (long)blockIdx.x * kPoleBlock + threadIdx.x;
+    const long item = (long)blockIdx.x * BS + threadIdx.x;
     RX_ASSERT(p0 >= 0 && p0 <= p1 && p1 <= a.n_poles);
     long rep[4];
     bool ok[2];
@@ -1400,7 +1400,7 @@ __global__ void __launch_bounds__(kPoleBlock, MINB) pole_kernel_r2x(PoleArgs a) 
             const double2 *src = reinterpret_cast<const double2 *>(a.xpoles + pt);
             double2 *dst = reinterpret_cast<double2 *>(sp);
             constexpr int kPer = (int)(sizeof(R2XPole) / sizeof(double2));
-            for (int i = threadIdx.x; i < cnt * kPer; i += kPoleBlock) dst[i] = src[i];
+            for (int i = threadIdx.x; i < cnt * kPer; i += BS) dst[i] = src[i];
         }
         __syncthreads();
         r2x_tile<PU>(sp, cnt, K2, st);
@@ -2282,8 +2282,16 @@ cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaS
 }
 
 // Explicit-solve R2C kernel (PFHX, default) instantiations: (poles per loop trip, min blocks);
-// octet items only (modes_per_thread 8).
-#define REXI_R2X_CONFIGS(X) X(1, 2) X(2, 2) X(4, 2) X(8, 2) X(1, 3) X(2, 3) X(4, 3) X(8, 3)
+// octet items only (modes_per_thread 8). min blocks 2, 3: 128-thread blocks; 5, 6: 64-thread
+// blocks (10 / 12 warps per SM at <= 200 / <= 168 registers).
+#define REXI_R2X_CONFIGS(X) X(1, 2) X(2, 2) X(4, 2) X(8, 2) X(1, 3) X(2, 3) X(4, 3) X(8, 3) \
+    X(4, 5) X(8, 5) X(4, 6) X(8, 6)
+
+int r2x_block_size(int minb) { return minb >= 5 ? 64 : kPoleBlock; }
+long pole_r2x_blocks(int D, int minb) {
+    const int bs = r2x_block_size(minb);
+    return (r2c_items(D, 2, true) + bs - 1) / bs;
+}
 
 bool pole_r2x_supported(int mpt, int pu, int minb) {
     if (mpt != 8) return false;
@@ -2293,18 +2301,20 @@ bool pole_r2x_supported(int mpt, int pu, int minb) {
     return false;
 }
 
+#define R2X_KERNEL(U, B) pole_kernel_r2x<U, B, (B >= 5 ? 64 : kPoleBlock)>
+
 cudaError_t pole_r2x_occupancy(int pu, int minb, int *blocks_per_sm) {
 #define X(U, B) if (pu == U && minb == B) \
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pole_kernel_r2x<U, B>, kPoleBlock, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, R2X_KERNEL(U, B), r2x_block_size(B), 0);
     REXI_R2X_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
-    dim3 grid((unsigned)pole_r2c_blocks(a.D, 8), (unsigned)a.n_chunks);
+    dim3 grid((unsigned)pole_r2x_blocks(a.D, minb), (unsigned)a.n_chunks);
 #define X(U, B) if (pu == U && minb == B) { \
-    pole_kernel_r2x<U, B><<<grid, kPoleBlock, 0, st>>>(a); return cudaGetLastError(); }
+    R2X_KERNEL(U, B)<<<grid, r2x_block_size(B), 0, st>>>(a); return cudaGetLastError(); }
     REXI_R2X_CONFIGS(X)
 #undef X
     return cudaErrorInvalidValue;

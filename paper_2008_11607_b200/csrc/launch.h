@@ -30,6 +30,7 @@ cudaError_t launch_poles_r2c(const PoleArgs &a, int mpt, int pu, int minb, cudaS
 // explicit-solve R2C kernel (PFHX, kind 7; octet items, modes_per_thread 8)
 bool pole_r2x_supported(int mpt, int pu, int minb);
 cudaError_t pole_r2x_occupancy(int pu, int minb, int *blocks_per_sm);
+long pole_r2x_blocks(int D, int minb);   // grid.x of the PFHX kernel (block size by min blocks)
 cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st);
 // stream-K R2C (octet items, modes_per_thread 8): persistent grid of `ctas` blocks
 cudaError_t launch_poles_r2c_sk(const PoleArgs &a, int pu, int ctas, cudaStream_t st);

@@ -22,7 +22,8 @@ TUNINGS = {"dz": [(1, 1, 8), (2, 1, 4), (2, 1, 5), (3, 1, 4), (4, 1, 3), (4, 1, 
                    (2, 2, 3), (2, 2, 4), (4, 2, 2)],
            "pfhr": [(4, 1, 4), (4, 1, 5), (4, 1, 6), (4, 2, 3), (4, 2, 4), (4, 4, 3), (8, 1, 2),
                     (8, 1, 3), (8, 2, 2), (8, 3, 2), (8, 4, 2), (8, 8, 2), (8, 2, 3), (8, 4, 3), (8, 8, 3), (16, 2, 2)],
-           "pfhx": [(8, 1, 2), (8, 2, 2), (8, 4, 2), (8, 8, 2), (8, 1, 3), (8, 2, 3), (8, 4, 3), (8, 8, 3)]}
+           "pfhx": [(8, 1, 2), (8, 2, 2), (8, 4, 2), (8, 8, 2), (8, 1, 3), (8, 2, 3), (8, 4, 3), (8, 8, 3),
+                    (8, 4, 5), (8, 8, 5), (8, 4, 6), (8, 8, 6)]}
 for variant in sys.argv[2].split(",") if len(sys.argv) > 2 else ("dz", "uv", "dz3", "pf", "pfh", "pfhr"):
     for mpt, pu, minb in TUNINGS[variant]:
         p = rexi.Plan(D, tau, tol=tol, variant=variant)

@@ -91,7 +91,7 @@ def test_forward_fft_vs_naive_dft(R, D):
         assert np.linalg.norm(F[c] - O) / np.linalg.norm(O) < 1e-14
 
 
-@pytest.mark.parametrize("D", [4, 8, 16, 32, 64, 256, 512])
+@pytest.mark.parametrize("D", [4, 8, 16, 32, 64, 256, 512, 1024])
 def test_inverse_fft_vs_naive_dft(R, D):
     p = R.Plan(D, 0.1)
     A = inputs.spectral_white(D, seed=3)
@@ -116,6 +116,38 @@ def test_fft_4096_sampled(R):
         ph = np.exp(-2j * np.pi * ((k * x[None, :] + l * x[:, None]) % D) / D)
         ref = (X * ph).sum() / D ** 2
         assert abs(F0[l, k] - ref) < 1e-13 * np.sqrt(D * D) / D ** 2 * 50
+
+
+@pytest.mark.parametrize("D", [2048, 8192])
+def test_fft_sampled_and_round_trip_large(R, D):
+    """The radix-16 passes at the sizes no full-grid test covers: sampled entries of the forward
+    transform and of the (symmetrising) inverse vs the DFT definition, and inverse(forward(X))
+    = X for real X over the whole grid."""
+    import torch
+    p = R.Plan(D, 0.001, tol=1e-8)
+    g = np.random.Generator(np.random.PCG64(D))
+    X = g.standard_normal((D, D))
+    Z = torch.zeros((D, D), dtype=torch.float64, device="cuda")
+    Xd = dev(X)
+    F = p.forward(Xd, Z, Z)
+    F0 = host(F[0])
+    x = np.arange(D)
+    H = D // 2
+    for (l, k) in [(0, 0), (1, 0), (0, H), (H, H), (17, D - 1), (D - 5, 3)]:
+        ph = np.exp(-2j * np.pi * ((k * x[None, :] + l * x[:, None]) % D) / D)
+        ref = (X * ph).sum() / D ** 2
+        assert abs(F0[l, k] - ref) < 1e-13 * np.sqrt(D * D) / D ** 2 * 50
+    back = [host(t) for t in p.inverse(F)]
+    assert np.abs(back[0] - X).max() < 1e-12
+    assert np.abs(back[1]).max() < 1e-12 and np.abs(back[2]).max() < 1e-12
+    # inverse of a non-Hermitian spectrum (symmetrised on load) at sampled points
+    A = torch.zeros_like(F)
+    A[0] = F[0] * (1.0 + 0.5j)             # breaks the Hermitian symmetry
+    out0 = host(p.inverse(A)[0])
+    Ah = host(A[0])
+    for (yy, xx) in [(0, 0), (3, D - 2), (H, 7)]:
+        ph = np.exp(2j * np.pi * ((xx * x[None, :] + yy * x[:, None]) % D) / D)
+        assert abs(out0[yy, xx] - (Ah * ph).sum().real) < 1e-11
 
 
 # ----------------------------------------------------------------------------- S2 + S3

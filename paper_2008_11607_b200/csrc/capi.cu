@@ -107,6 +107,7 @@ struct rexi_plan_s {
     cd *d_acc = nullptr;    // [3][n_modes]
     cd *d_tmp = nullptr;    // [3][n_modes]
     cd *d_partial = nullptr;  // [max_chunks][3][n_modes]
+    unsigned *d_counter = nullptr;  // fused DSMEM step: clusters arrived (0 between launches)
     double *d_stage = nullptr;  // [6][n_modes] (rexi_apply_host)
     double *d_stage2 = nullptr;  // [6][n_modes] second set (rexi_apply_host_batch)
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -163,7 +164,7 @@ struct rexi_plan_s {
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_xpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
-                        (void *)d_tmp, (void *)d_partial, (void *)d_stage, (void *)d_stage2})
+                        (void *)d_tmp, (void *)d_partial, (void *)d_counter, (void *)d_stage, (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -451,7 +452,10 @@ bool small_eligible(const rexi_plan_s *p, long b, long e) {
 
 rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
                             const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
-    const int cs = rexi::small_step_cluster();
+    // REXI_SMALL_V1=1 (measurement knob): the first fused kernel, stage exchanges through L2
+    static const bool v1 = [] { const char *v = getenv("REXI_SMALL_V1"); return v && atoi(v) != 0; }();
+    int resident = 0;
+    const int cs = v1 ? rexi::small_step_cluster() : rexi::small2_cluster(&resident);
     if (cs <= 0) return fail(REXI_ECUDA, "fused small-grid step: thread-block cluster launch unavailable");
     const long n = p->n_modes;
     const int D = p->host.D;
@@ -519,9 +523,26 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     x.pole_end = e;
     x.n_modes = n;
     x.D = D;
+    // DSMEM kernel: the pole range split over nc clusters (REXI_SMALL_NC: measurement knob)
+    {
+        static const int nc_env = [] { const char *v = getenv("REXI_SMALL_NC"); return v ? atoi(v) : 0; }();
+        int nc = nc_env > 0 ? nc_env : 1;
+        nc = (int)std::max(1L, std::min<long>({(long)nc, (long)rexi::kSmallMaxClusters, e - b}));
+        if (resident > 0) nc = std::min(nc, std::max(1, resident));
+        const long need = (long)nc * 3 * D * (D / 2 + 1);
+        if (need > 3 * n * (long)p->max_chunks) nc = 1;
+        a.n_clusters = nc;
+        for (int g = 0; g < nc; ++g) {
+            const long gb = b + (e - b) * g / nc, ge = b + (e - b) * (g + 1) / nc;
+            range_sums(p, gb, ge, &a.Sg[g], &a.Sdg[g]);
+        }
+        a.cl_acc = p->d_partial;
+        a.counter = p->d_counter;
+    }
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    CK(rexi::launch_step_small(a, cs, st));
+    if (v1) CK(rexi::launch_step_small(a, cs, st));
+    else CK(rexi::launch_step_small2(a, cs, st));
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     p->launches += 1;
@@ -752,7 +773,8 @@ rexi_status_t rexi_plan_create(rexi_plan_t *out, int D, double tau, double tol, 
         (e = alloc((void **)&p->d_tw, 2 * sizeof(double) * (size_t)D)) ||
         (e = alloc((void **)&p->d_fhat, field)) || (e = alloc((void **)&p->d_acc, field)) ||
         (e = alloc((void **)&p->d_tmp, field)) ||
-        (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks))) {
+        (e = alloc((void **)&p->d_partial, field * (size_t)p->max_chunks)) ||
+        (e = alloc((void **)&p->d_counter, sizeof(unsigned))) || (e = cudaMemset(p->d_counter, 0, sizeof(unsigned)))) {
         cudaGetLastError();
         return cleanup_fail(e == cudaErrorMemoryAllocation ? fail(REXI_ENOMEM, "cudaMalloc failed")
                                                            : cuda_fail(e, "cudaMalloc"));

@@ -1315,10 +1315,11 @@ __device__ __forceinline__ cd ld_spec(const cd *p) {
 // Per-item setup of the explicit-solve R2C kernel: the four {K, -K} pairs of octet item `item`
 // (r2c_octet_item), their representative modes rep[], validity ok[] and the shared K2; the
 // pair state from the representative's spectrum (pole-independent, kept in registers).
-template <bool CG>
-__device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&st)[4], long (&rep)[4],
-                                          bool (&ok)[2], double &K2) {
-    const long n_modes = a.n_modes;
+// ld(f, m, j) returns field f of the spectrum at mode m, the representative of the item's pair j;
+// ks(i) the symbol of index i (global or L2-only loads, or the fused step's staged copy).
+template <class LD, class KS>
+__device__ __forceinline__ void r2x_setup_ld(const PoleArgs &a, long item, XPair (&st)[4], long (&rep)[4],
+                                             bool (&ok)[2], double &K2, LD ld, KS ks) {
     const double c = a.tau;
     const double hmu = a.hmu;
     const int H = a.D >> 1;
@@ -1337,12 +1338,10 @@ __device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const long mm = rep[2 * g + j];
-            RX_ASSERT(mm >= 0 && mm < n_modes);
+            RX_ASSERT(mm >= 0 && mm < a.n_modes);
             const int l = (int)(mm >> a.log2D), k = (int)(mm & (a.D - 1));
-            // CG (fused step): ksym may be the CTA's shared-memory copy -> generic loads
-            const double kx = CG ? a.ksym[k] : __ldg(&a.ksym[k]), ky = CG ? a.ksym[l] : __ldg(&a.ksym[l]);
-            const cd e = ld_spec<CG>(a.fhat + mm), uu = ld_spec<CG>(a.fhat + n_modes + mm),
-                     vv = ld_spec<CG>(a.fhat + 2 * n_modes + mm);
+            const double kx = ks(k), ky = ks(l);
+            const cd e = ld(0, mm, 2 * g + j), uu = ld(1, mm, 2 * g + j), vv = ld(2, mm, 2 * g + j);
             // delta0 = i (kx u + ky v), zeta0 = i (kx v - ky u)   (tau-scaled)
             const cd d = mk(-fma(kx, uu.y, ky * vv.y), fma(kx, uu.x, ky * vv.x));
             const cd z = mk(-fma(kx, vv.y, -ky * uu.y), fma(kx, vv.x, -ky * uu.x));
@@ -1357,6 +1356,17 @@ __device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&
             K2 = fma(kx, kx, ky * ky);   // the same for all four pairs of an octet item
         }
     }
+}
+
+// r2x_setup_ld from the global spectrum a.fhat; CG: through L2 only (the fused small-grid step,
+// whose ksym is then the CTA's shared-memory copy, read with generic loads).
+template <bool CG>
+__device__ __forceinline__ void r2x_setup(const PoleArgs &a, long item, XPair (&st)[4], long (&rep)[4],
+                                          bool (&ok)[2], double &K2) {
+    const long n_modes = a.n_modes;
+    r2x_setup_ld(
+        a, item, st, rep, ok, K2, [&](int f, long m, int) { return ld_spec<CG>(a.fhat + f * n_modes + m); },
+        [&](int i) { return CG ? a.ksym[i] : __ldg(&a.ksym[i]); });
 }
 
 // The item's Hermitian accumulators (eta, delta') at the representative modes of chunk `chunk`.
@@ -2010,6 +2020,523 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs 
     }
 }
 
+// ============================================================================= fused small-grid step, DSMEM
+// step_small2_kernel: the fused small-grid step with every exchange between stages through
+// distributed shared memory (DSMEM) instead of L2, and the pole range optionally split over
+// several clusters. Per cluster (CS CTAs of 256 threads):
+//   A  forward rows (own row pairs, local slabs) -> X1, X2 stored into the column owners' slabs
+//   B  forward half-spectrum columns -> the spectrum rows l <= D/2, distributed by row over the
+//      cluster (row l in CTA l mod CS)
+//   C  PFHX pole loop over the cluster's pole range: a CTA owns a contiguous set of octet items,
+//      its threads split them into (item, pole chunk) units; the spectrum at the items'
+//      representative modes is read from the owning CTAs' shared memory; chunk partials meet
+//      in local shared memory; the four K = 0 corners on the last warp of the last CTA
+//   D  R2C finish of every pair by its chunk-0 thread -> the Hermitian spectrum at the modes
+//      k <= D/2, stored into the inverse column owners' slabs (one cluster) or into the
+//      cluster's slice of cl_acc (several clusters; the last cluster to arrive sums the slices
+//      in cluster order and goes on alone)
+//   E  inverse half-spectrum columns -> Z = g1 + i g2 stored into the row-pair owners' slabs
+//   F  inverse rows -> the three real fields
+// Four cluster barriers (A|B, B|C, D|E, E|F) and one block barrier (C|D); no intermediate array
+// in global memory with one cluster. Shared memory (cd units, small2_layout): column slabs,
+// one auxiliary slab (the k = D/2 values of the CTA's k = 0 column), a region that holds the row
+// slabs in A and F and the spectrum rows + chunk partials in between, the pole cache, twiddles
+// and symbols. Same arithmetic as the multi-launch path (r2x_setup_ld, r2x_tile, the
+// finish_r2c_mode formulas), except the K = 0 pole sums, reduced in a different order.
+struct Small2Layout {
+    int nu_max;   // row pairs / columns per CTA
+    int ni_max;   // octet items per CTA
+    int cslab, aux, rreg, stg, corner, part, pcache, tw, ks, total;   // offsets / size in cd
+};
+// Octet items of CTA c: [small2_items_begin(c), small2_items_begin(c + 1)), split in proportion to
+// the CTA's pole workers (256, the last CTA 224: its last warp runs the K = 0 corners).
+// (32-bit arithmetic: items <= 2142 for D <= 128, so items * 256 * CS < 2^31)
+__host__ __device__ __forceinline__ int small2_items_begin(int items, int c, int CS) {
+    return c >= CS ? items : items * (256 * c) / (256 * CS - 32);
+}
+__host__ __device__ __forceinline__ int small2_item_owner(int item, int items, int CS) {
+    const int c = ((item + 1) * (256 * CS - 32) - 1) / (items * 256);
+    return c < CS - 1 ? c : CS - 1;
+}
+__host__ __device__ __forceinline__ Small2Layout small2_layout(int D, int CS) {
+    Small2Layout L;
+    const int H = D / 2, PL = padded_len(D);
+    L.nu_max = (3 * H + CS - 1) / CS;
+    const long items = r2c_items(D, 2, true), capb = 256L * CS - 32;
+    L.ni_max = (int)((items * 256 + capb - 1) / capb + 1);
+    L.cslab = 0;
+    L.aux = L.cslab + L.nu_max * (PL + 1);
+    L.rreg = L.aux + PL;
+    // between A and F the row-slab region holds the staged spectrum of the CTA's items
+    // [pair][field][item], the four corners [corner][field] and the chunk partials
+    // [chunk][pair][eta, delta'][item] (ni * ch <= max(256, ni) units)
+    L.stg = L.rreg;
+    L.corner = L.stg + L.ni_max * 12;
+    L.part = L.corner + 12;
+    const int mid = L.ni_max * 12 + 12 + 8 * (L.ni_max > 256 ? L.ni_max : 256);
+    const int rsize = L.nu_max * PL > mid ? L.nu_max * PL : mid;
+    L.pcache = L.rreg + rsize;
+    L.tw = L.pcache + kSmallPoleCache * (int)(sizeof(R2XPole) / sizeof(cd));
+    L.ks = L.tw + D;
+    L.total = L.ks + (D + 1) / 2;
+    return L;
+}
+
+// Where stage B stores spectrum value (l, k), l <= D/2, for the pole stage: the CTA owning the
+// item whose pair it represents and the staging index there (field f at idx + f * fstride;
+// layout [pair][field][item], consecutive items in consecutive slots), or the corner slot of the
+// last CTA (K = 0 modes); false if (l, k) represents no pair (a mirror).
+// The inverse of r2c_octet_item / quad_modes / the representative choice of r2x_setup_ld.
+__device__ __forceinline__ bool small2_stage_slot(int l, int k, int D, int items, int CS, const Small2Layout &L,
+                                                  int &cta, int &idx, int &fstride) {
+    const int H = D >> 1;
+    const bool lb = (l == 0 || l == H), kb = (k == 0 || k == H);
+    if (l > H) return false;
+    if (lb && kb) {   // corner q = (l == H) * 2 + (k == H)
+        cta = CS - 1;
+        idx = L.corner + ((l == H ? 2 : 0) + (k == H ? 1 : 0)) * 3;
+        fstride = 1;
+        return true;
+    }
+    int a, b, j;
+    if (lb) {
+        if (k > H) return false;      // mirror of (l, D - k)
+        if (l == 0) { a = 0; b = k; } else { a = k; b = 0; }
+        j = 0;
+    } else if (k == 0) {
+        a = 0; b = l; j = 1;          // axis quad (0, l): pair {(l, 0), (D - l, 0)}
+    } else if (k == H) {
+        a = l; b = 0; j = 1;          // Nyquist quad (l, 0): pair {(l, H), (D - l, H)}
+    } else {
+        a = l; b = k < H ? k : D - k; j = k < H ? 0 : 1;   // interior quad (l, |k|)
+    }
+    const int n_oct = (int)r2c_n_oct(D);
+    int item;
+    int gq = 0;
+    if (a > 0 && b > 0 && a != b) {
+        const int ap = (a < b ? a : b) - 1, bp = (a < b ? b : a) - 1;
+        item = bp * (bp - 1) / 2 + ap;
+        gq = a < b ? 0 : 1;
+    } else if (a == b) {
+        item = n_oct + (a - 1);
+    } else if (a == 0) {
+        item = n_oct + (H - 1) + (b - 1);
+    } else {
+        item = n_oct + 2 * (H - 1) + (a - 1);
+    }
+    cta = small2_item_owner(item, items, CS);
+    idx = L.stg + (2 * gq + j) * 3 * L.ni_max + (item - small2_items_begin(items, cta, CS));
+    fstride = L.ni_max;
+    return true;
+}
+
+// barrier.cluster split phases: arrive (relaxed: orders nothing) at kernel start, wait before
+// the first DSMEM access (every CTA of the cluster has started); and the full barrier with
+// release / acquire semantics between stages (orders shared::cluster and global accesses)
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+// owner CTA of index u of P units split as [P c / CS, P (c + 1) / CS)
+__device__ __forceinline__ int small2_owner(int u, int P, int CS) { return ((u + 1) * CS - 1) / P; }
+
+// Representative mode of pair j (0..3) of octet item `item` (as r2x_setup_ld orders them);
+// false for the discarded half of a single-quad item.
+__device__ __forceinline__ bool r2x_pair_rep(long item, int D, int log2D, int j, long &rep) {
+    const int H = D >> 1;
+    long quad[2];
+    bool ok[2], shared_k2;
+    r2c_octet_item(item, D, quad, ok, shared_k2);
+    const int g = j >> 1;
+    if (!ok[g]) return false;
+    long mq[4];
+    quad_modes(quad[g], D, log2D, mq);
+    const int qa = (int)(quad[g] >> (log2D - 1)), qb = (int)(quad[g] & (H - 1));
+    rep = (j & 1) == 0 ? mq[0] : ((qa > 0 && qb > 0) ? mq[1] : mq[2]);
+    return true;
+}
+
+// The n (<= nmax) length-D transforms at s + j * ld (j < n) in shared memory, tf threads each,
+// in rounds of blockDim / tf transforms (uniform round count: the passes hold block barriers).
+// Not inlined: the step runs its code once, cold, so one copy for the four stages (A, B, E, F)
+// costs less instruction fetch than four.
+template <int LOGD>
+__device__ __noinline__ void small2_ffts(cd *s, int ld, int n, int nmax, const cd *tws, bool inv) {
+    constexpr int D = 1 << LOGD, tf = D >= 8 ? D / 8 : 1;
+    const int per = (int)blockDim.x / tf, j0 = (int)threadIdx.x / tf, t = (int)threadIdx.x - j0 * tf;
+    for (int base = 0; base < nmax; base += per) {
+        const int j = base + j0;
+        if (inv) fft_in_smem<true, true>(s + j * ld, D, LOGD, t, tf, tws, j < n);
+        else fft_in_smem<false, true>(s + j * ld, D, LOGD, t, tf, tws, j < n);
+    }
+}
+
+template <int LOGD>
+__global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs a) {
+    constexpr int D = 1 << LOGD, H = D >> 1, LOGH = LOGD - 1;
+    constexpr int PL = padded_len(D);
+    constexpr int stride = PL + 1;   // column slabs
+    constexpr int P3 = 3 * H;        // row pairs (A, F) = half-spectrum columns (B, E), all fields
+    extern __shared__ cd smem[];
+    __shared__ int s_last;
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int CS = (int)cl.num_blocks();
+    const int cta = (int)cl.block_rank();
+    const int g = (int)(blockIdx.x / (unsigned)CS);   // cluster index
+    const int NC = a.n_clusters;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const Small2Layout L = small2_layout(D, CS);
+    const int u0 = (P3 * cta) / CS, u1 = (P3 * (cta + 1)) / CS;
+    const int nu = u1 - u0;
+    if (a.stop_after < -1) return;   // stage-timing measurements only
+    cluster_arrive_relaxed();
+    rx_poison_smem();
+    RX_ASSERT(nu <= L.nu_max && (long)L.total * 16 <= (long)dyn_smem_bytes() && g < NC);
+    cd *cs_ = smem + L.cslab;          // column slabs
+    cd *rr = smem + L.rreg;            // row slabs (A, F) | spectrum rows + partials (B..D)
+    R2XPole *pc = reinterpret_cast<R2XPole *>(smem + L.pcache);
+    cd *tws = smem + L.tw;
+    double *ksm = reinterpret_cast<double *>(smem + L.ks);
+    // this cluster's pole range
+    const long pb_all = a.pole.pole_begin, np_all = a.pole.pole_end - a.pole.pole_begin;
+    // (32-bit: a fused step has fewer than 2^31 / kSmallMaxClusters poles, checked on the host)
+    const long pb = pb_all + (int)np_all * g / NC;
+    const int npl = (int)(pb_all + (int)np_all * (g + 1) / NC - pb);
+    const bool cached = npl <= kSmallPoleCache;
+    if (cta == CS - 1 && tid >= kSmallThreads - 32) {
+        // the corner warp's pole records (generic table, read in stage C): into L2 now
+        for (long p = pb + (tid & 31); p < pb + npl; p += 32) {
+            const char *q = reinterpret_cast<const char *>(a.fix.poles + p);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(q + sizeof(PoleConst) - 1));
+        }
+    }
+    // Preload (pole records, twiddles, symbols) and the A inputs: every global load of this
+    // thread is issued before the first shared-memory store (one memory latency, not one per
+    // loop trip; the inputs were flushed from L2 between steps)
+    {
+        constexpr int kPer = (int)(sizeof(R2XPole) / sizeof(double2));
+        constexpr int RP = (kSmallPoleCache * kPer + kSmallThreads - 1) / kSmallThreads;
+        constexpr int RI = (((3 * H + 7) / 8) * D + kSmallThreads - 1) / kSmallThreads;   // CS >= 8
+        RX_ASSERT(NT == kSmallThreads && nu * D <= RI * NT);
+        const double2 *psrc = reinterpret_cast<const double2 *>(a.pole.xpoles + pb);
+        double2 *pdst = reinterpret_cast<double2 *>(pc);
+        const int n2 = cached ? (int)npl * kPer : 0;
+        double2 pv[RP], iv[RI];
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+            if (tid + r * NT < n2) pv[r] = __ldg(psrc + tid + r * NT);
+#pragma unroll
+        for (int r = 0; r < RI; ++r) {
+            const int i = tid + r * NT;
+            if (i < nu * D) {
+                const int pr = i >> LOGD, x = i & (D - 1);
+                const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
+                const double *in = a.in[f] + (size_t)(2 * pair) * D + x;
+                iv[r] = make_double2(__ldg(in), __ldg(in + D));
+            }
+        }
+        cd tw0;
+        double ks0 = 0.0;
+        if (tid < D) {
+            tw0 = a.tw[tid];
+            ks0 = __ldg(a.pole.ksym + tid);
+        }
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+            if (tid + r * NT < n2) pdst[tid + r * NT] = pv[r];
+        // ---- A: forward rows (local): two real rows per complex transform
+#pragma unroll
+        for (int r = 0; r < RI; ++r) {
+            const int i = tid + r * NT;
+            if (i < nu * D) rr[(i >> LOGD) * PL + pidx(i & (D - 1))] = mk(iv[r].x, iv[r].y);
+        }
+        if (tid < D) {
+            tws[tid] = tw0;
+            ksm[tid] = ks0;
+        }
+    }
+    __syncthreads();
+    if (a.stop_after < 0) {   // stage-timing measurements only
+        cluster_wait();
+        return;
+    }
+    small2_ffts<LOGD>(rr, PL, nu, L.nu_max, tws, false);
+    cluster_wait();   // every CTA of the cluster runs: DSMEM stores may start
+    for (int i = tid; i < nu * H; i += NT) {
+        const int pr = i >> LOGH, k = i & (H - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
+        const cd *Z = rr + pr * PL;
+        cd X1, X2;
+        if (k == 0) {
+            const cd z0 = Z[pidx(0)], zh = Z[pidx(H)];
+            X1 = mk(z0.x, zh.x);
+            X2 = mk(z0.y, zh.y);
+        } else {
+            const cd zk = Z[pidx(k)], zm = Z[pidx(D - k)];
+            X1 = mk(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+            X2 = mk(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+        }
+        const int gc = f * H + k, oc = small2_owner(gc, P3, CS);
+        cd *col = cl.map_shared_rank(cs_, oc) + (gc - (P3 * oc) / CS) * stride;
+        RX_ASSERT((gc - (P3 * oc) / CS) < L.nu_max);
+        col[pidx(2 * pair)] = X1;
+        col[pidx(2 * pair + 1)] = X2;
+    }
+    cluster_barrier();
+
+    if (a.stop_after <= 0) return;   // stage-timing measurements only
+    // ---- B: forward columns (local) -> the spectrum at every pair representative, D^-2, staged
+    // in the shared memory of the CTA that owns the pair's octet item (and the K = 0 corners)
+    small2_ffts<LOGD>(cs_, stride, nu, L.nu_max, tws, false);
+    {
+        const double sc = a.scale;
+        const int items = (int)a.n_items;
+        auto put_spec = [&](int f, int l, int k, cd v) {
+            int oc, idx, fs;
+            if (small2_stage_slot(l, k, D, items, CS, L, oc, idx, fs)) {
+                RX_ASSERT(idx + f * fs < L.part);
+                cl.map_shared_rank(smem, oc)[idx + f * fs] = v;
+            }
+        };
+        for (int i = tid; i < nu * D; i += NT) {
+            const int c = i >> LOGD, l = i & (D - 1);
+            const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
+            const int lm = (D - l) & (D - 1);
+            const cd v = cs_[c * stride + pidx(l)];
+            if (k == 0) {
+                if (l <= H) {
+                    const cd w = cs_[c * stride + pidx(lm)];
+                    const double hs = 0.5 * sc;
+                    put_spec(f, l, 0, mk(hs * (v.x + w.x), hs * (v.y - w.y)));
+                    put_spec(f, l, H, mk(hs * (v.y + w.y), hs * (w.x - v.x)));
+                }
+            } else {
+                if (l <= H) put_spec(f, l, k, mk(v.x * sc, v.y * sc));
+                if (lm <= H) put_spec(f, lm, D - k, mk(v.x * sc, -v.y * sc));
+            }
+        }
+    }
+    cluster_barrier();
+
+    if (a.stop_after <= 1) return;   // stage-timing measurements only
+    // ---- C + D: pole loop over (item, chunk) units, chunk partials in shared memory, finish
+    const double c_tau = a.pole.tau;
+    const cd Sg = a.Sg[g], Sdg = a.Sdg[g];
+    // the Hermitian spectrum value v of field f at (l, k), k <= H: into the inverse column
+    // owner's slab (T0 at k = 0, TH of the k = 0 column at k = H: the auxiliary slab), or into
+    // this cluster's slice of cl_acc
+    auto put_acc = [&](int f, int l, int k, cd v) {
+        if (NC > 1) {
+            a.cl_acc[(((size_t)g * 3 + f) * D + l) * (H + 1) + k] = v;
+            return;
+        }
+        const int gc = f * H + (k == H ? 0 : k), oc = small2_owner(gc, P3, CS);
+        cd *base = cl.map_shared_rank(smem, oc);
+        if (k == H) base[L.aux + pidx(l)] = v;
+        else base[L.cslab + (gc - (P3 * oc) / CS) * stride + pidx(l)] = v;
+    };
+    const cd *stg = smem + L.stg;   // [item][pair][field]
+    {
+        const int items = (int)a.n_items;
+        // item split weighted by the workers per CTA (the last CTA's last warp takes the corners)
+        const int i0 = small2_items_begin(items, cta, CS), i1 = small2_items_begin(items, cta + 1, CS);
+        const int ni = i1 - i0;
+        const int W = cta == CS - 1 ? kSmallThreads - 32 : kSmallThreads;
+        const int ch = ni > 0 ? max(1, min(npl, W / ni)) : 1;
+        RX_ASSERT((long)ni * ch * 8 <= L.pcache - L.part);
+        cd *part = smem + L.part;   // [chunk][item][pair][eta, delta']
+        // one instance of the pole tile: the cached records or the global table, generic loads
+        const R2XPole *src = cached ? pc : a.pole.xpoles + pb;
+        for (int u = tid; u < ni * ch && tid < W; u += W) {
+            const int il = u % ni, chunk = u / ni;
+            XPair st[4];
+            long rep[4];
+            bool ok[2];
+            double K2;
+            r2x_setup_ld(
+                a.pole, i0 + il, st, rep, ok, K2, [&](int f, long, int j) { return stg[(j * 3 + f) * L.ni_max + il]; },
+                [&](int i) { return ksm[i]; });
+            const int p0 = npl * chunk / ch, p1 = a.stop_after == 2 ? p0 : npl * (chunk + 1) / ch;
+            r2x_tile<2>(src + p0, p1 - p0, K2, st);
+            cd *p = part + (size_t)chunk * 8 * ni + il;   // [chunk][pair][eta, delta'][item]
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                p[(2 * j) * ni] = st[j].H0;
+                p[(2 * j + 1) * ni] = st[j].H1;
+            }
+        }
+        if (cta == CS - 1 && tid >= kSmallThreads - 32) {
+            // the four K = 0 corners (fixup_k0_kernel): lanes stride the poles, every lane runs
+            // the four corners of its poles (one pole record load serves four corners)
+            const int lane = tid & 31;
+            cd e0[4], ua[4], vb[4];
+            double Au[4], Av[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {   // (0,0) (0,H) (H,0) (H,H)
+                e0[q] = smem[L.corner + q * 3];
+                ua[q] = smem[L.corner + q * 3 + 1];
+                vb[q] = smem[L.corner + q * 3 + 2];
+                Au[q] = 0.0;
+                Av[q] = 0.0;
+            }
+            for (long p = pb + lane; p < pb + npl && a.stop_after != 2; p += 32) {
+                const PoleConst *P = a.fix.poles + p;
+                const cd s3 = mk(__ldg(&P->s3r), __ldg(&P->s3i)), s4 = mk(__ldg(&P->s4r), __ldg(&P->s4i));
+                const cd w1 = mk(__ldg(&P->w1r), __ldg(&P->w1i)), w2 = mk(__ldg(&P->w2r), __ldg(&P->w2i));
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const cd u1 = cfms(s4, vb[q], cmul(s3, ua[q]));
+                    const cd v1 = cfma(s3, vb[q], cmul(s4, ua[q]));
+                    // Re(w1 u1 + w2 u2): the self-mirror modes keep the real part (Hermitian part)
+                    double ru = fma(w1.x, u1.x, -w1.y * u1.y), rv = fma(w1.x, v1.x, -w1.y * v1.y);
+                    if (a.fix.method != 1) {   // REXII: the second solve (REXI: one solve per term)
+                        const cd u2 = cjfma(s4, v1, cjfma(s3, u1, mk(0, 0)));
+                        const cd v2 = cjfms(s4, u1, cjfma(s3, v1, mk(0, 0)));
+                        ru = fma(w2.x, u2.x, fma(-w2.y, u2.y, ru));
+                        rv = fma(w2.x, v2.x, fma(-w2.y, v2.y, rv));
+                    }
+                    Au[q] += ru;
+                    Av[q] += rv;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    Au[q] += __shfl_xor_sync(0xffffffffu, Au[q], o);
+                    Av[q] += __shfl_xor_sync(0xffffffffu, Av[q], o);
+                }
+            }
+            if (lane < 4) {
+                // self-mirror modes: the Hermitian part is Re; eta = S e0 there
+                const int q = lane, l = (q >> 1) * H, k = (q & 1) * H;
+                double au = Au[0], av = Av[0];
+                cd e = e0[0];
+#pragma unroll
+                for (int r = 1; r < 4; ++r) {
+                    if (q == r) {
+                        au = Au[r];
+                        av = Av[r];
+                        e = e0[r];
+                    }
+                }
+                put_acc(0, l, k, mk(cmul(Sg, e).x, 0.0));
+                put_acc(1, l, k, mk(au, 0.0));
+                put_acc(2, l, k, mk(av, 0.0));
+            }
+        }
+        __syncthreads();
+        // D: finish every pair of the CTA's items (all threads): chunk partials in a fixed
+        // order, then the formulas of finish_r2c_mode from the pair's spectrum
+        for (int t = tid; t < ni * 4; t += NT) {
+            const int j = t / ni, il = t - j * ni;
+            long m;
+            if (!r2x_pair_rep(i0 + il, D, LOGD, j, m)) continue;
+            cd h0 = mk(0, 0), h1 = mk(0, 0);
+            for (int cc = 0; cc < ch; ++cc) {
+                const cd *p = part + ((size_t)cc * 8 + 2 * j) * ni + il;
+                h0 = mk(h0.x + p[0].x, h0.y + p[0].y);
+                h1 = mk(h1.x + p[ni].x, h1.y + p[ni].y);
+            }
+            const int l = (int)(m >> LOGD), k = (int)(m & (D - 1));
+            const double kx = ksm[k], ky = ksm[l];
+            const cd *sp = stg + j * 3 * L.ni_max + il;
+            const cd e = sp[0], uu = sp[L.ni_max], vv = sp[2 * L.ni_max];
+            // H(delta) = H(delta') - Re(sum w1) e0 ; H(zeta) = Re(S) m0 + c H(eta)
+            h1 = mk(fma(-Sdg.x, e.x, h1.x), fma(-Sdg.x, e.y, h1.y));
+            const cd m0 = mk(fma(-c_tau, e.x, -fma(kx, vv.y, -ky * uu.y)), fma(-c_tau, e.y, fma(kx, vv.x, -ky * uu.x)));
+            const cd h2 = mk(fma(Sg.x, m0.x, c_tau * h0.x), fma(Sg.x, m0.y, c_tau * h0.y));
+            const double inv = 1.0 / fma(kx, kx, ky * ky);   // K2 > 0 off the corners
+            const cd tt = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
+            const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
+            const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
+            const int lm = (D - l) & (D - 1), km = (D - k) & (D - 1);
+            if (k <= H) {
+                put_acc(0, l, k, h0);
+                put_acc(1, l, k, U);
+                put_acc(2, l, k, V);
+            }
+            if (km <= H) {
+                put_acc(0, lm, km, mk(h0.x, -h0.y));
+                put_acc(1, lm, km, mk(U.x, -U.y));
+                put_acc(2, lm, km, mk(V.x, -V.y));
+            }
+        }
+    }
+    if (NC > 1) {
+        // hand-off: the last cluster to arrive sums the clusters' spectra (fixed order) alone
+        __threadfence();
+        cluster_barrier();
+        if (cta == 0 && tid == 0) {
+            const unsigned old = atomicAdd(a.counter, 1u);
+            const int last = old == (unsigned)(NC - 1);
+            if (last) *a.counter = 0u;   // every cluster has arrived: reset for the next launch
+            __threadfence();
+            for (int r = 0; r < CS; ++r) *cl.map_shared_rank(&s_last, r) = last;
+        }
+        cluster_barrier();
+        if (!s_last) return;
+        for (int i = tid; i < nu * D; i += NT) {
+            const int c = i >> LOGD, l = i & (D - 1);
+            const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
+            cd v = mk(0, 0), vh = mk(0, 0);
+            for (int q = 0; q < NC; ++q) {
+                const cd *src = a.cl_acc + (((size_t)q * 3 + f) * D + l) * (H + 1);
+                const cd x = ld_spec<true>(src + k);
+                v = mk(v.x + x.x, v.y + x.y);
+                if (k == 0) {
+                    const cd y = ld_spec<true>(src + H);
+                    vh = mk(vh.x + y.x, vh.y + y.y);
+                }
+            }
+            if (k == 0) v = mk(v.x - vh.y, v.y + vh.x);   // T0 + i TH
+            cs_[c * stride + pidx(l)] = v;
+        }
+        __syncthreads();
+    } else {
+        cluster_barrier();
+        // the k = 0 column packs T0 + i TH (TH arrived in the auxiliary slab)
+        for (int i = tid; i < nu * D; i += NT) {
+            const int c = i >> LOGD, l = i & (D - 1);
+            if (((u0 + c) & (H - 1)) != 0) continue;
+            const cd t0 = cs_[c * stride + pidx(l)], th = smem[L.aux + pidx(l)];
+            cs_[c * stride + pidx(l)] = mk(t0.x - th.y, t0.y + th.x);
+        }
+        __syncthreads();
+    }
+
+    if (a.stop_after <= 3) return;   // stage-timing measurements only
+    // ---- E: inverse columns (Hermitian input) -> Z rows into the row-pair owners
+    small2_ffts<LOGD>(cs_, stride, nu, L.nu_max, tws, true);
+    for (int i = tid; i < nu * H; i += NT) {
+        const int c = i >> LOGH, p = i & (H - 1);
+        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
+        const cd g1 = cs_[c * stride + pidx(2 * p)], g2 = cs_[c * stride + pidx(2 * p + 1)];
+        const int gp = f * H + p, oc = small2_owner(gp, P3, CS);
+        cd *Z = cl.map_shared_rank(rr, oc) + (gp - (P3 * oc) / CS) * PL;
+        if (k == 0) {
+            Z[pidx(0)] = mk(g1.x, g2.x);
+            Z[pidx(H)] = mk(g1.y, g2.y);
+        } else {
+            Z[pidx(k)] = mk(g1.x - g2.y, g1.y + g2.x);        // g1 + i g2
+            Z[pidx(D - k)] = mk(g1.x + g2.y, g2.x - g1.y);    // conj g1 + i conj g2
+        }
+    }
+    cluster_barrier();
+
+    if (a.stop_after <= 4) return;   // stage-timing measurements only
+    // ---- F: inverse rows (local) -> the three real fields
+    small2_ffts<LOGD>(rr, PL, nu, L.nu_max, tws, true);
+    for (int i = tid; i < nu * D; i += NT) {
+        const int pr = i >> LOGD, x = i & (D - 1);
+        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
+        const cd v = rr[pr * PL + pidx(x)];
+        const size_t gi = (size_t)(2 * pair) * D + x;
+        a.out[f][gi] = v.x;
+        a.out[f][gi + D] = v.y;
+    }
+}
+
 static int ilog2(int x) {
     int r = 0;
     while ((1 << r) < x) ++r;
@@ -2456,6 +2983,72 @@ cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st) {
     cfg.numAttrs = 1;
 #define X(L) \
     if (a.pole.log2D == L) return cudaLaunchKernelEx(&cfg, step_small_kernel<L>, a);
+    REXI_SMALL_LOGD(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
+
+// DSMEM step (step_small2_kernel): shared memory per CTA for cluster size cs; the cluster size
+// (16 where the device allows the non-portable size, else 8; 0: no cluster launch) and how many
+// such clusters can be resident at once. Cached per process.
+size_t small2_smem(int D, int cs) { return (size_t)small2_layout(D, cs).total * sizeof(cd); }
+
+static int g_small2_cs = -1, g_small2_resident = 0;
+int small2_cluster(int *resident) {
+    if (g_small2_cs < 0) {
+        g_small2_cs = 0;
+        bool ok = true;
+#define X(L)                                                                                                  \
+    cudaFuncSetAttribute(step_small2_kernel<L>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);            \
+    if (cudaFuncSetAttribute(step_small2_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                             (int)small2_smem(1 << L, 8)) != cudaSuccess)                                      \
+        ok = false;
+        REXI_SMALL_LOGD(X)
+#undef X
+        cudaGetLastError();
+        for (int want : {16, 8}) {
+            if (!ok) break;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(want);
+            cfg.blockDim = dim3(kSmallThreads);
+            cfg.dynamicSmemBytes = small2_smem(128, want);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = want;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, step_small2_kernel<7>, &cfg) == cudaSuccess &&
+                nclusters >= 1) {
+                g_small2_cs = want;
+                g_small2_resident = nclusters;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    if (resident) *resident = g_small2_resident;
+    return g_small2_cs;
+}
+
+cudaError_t launch_step_small2(const SmallArgs &a, int cs, cudaStream_t st) {
+    if (a.n_clusters < 1 || a.n_clusters > kSmallMaxClusters) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs * a.n_clusters);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = small2_smem(a.pole.D, cs);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+#define X(L) \
+    if (a.pole.log2D == L) return cudaLaunchKernelEx(&cfg, step_small2_kernel<L>, a);
     REXI_SMALL_LOGD(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -143,6 +143,7 @@ struct FixupArgs {
 // "fused small-grid step"): rows/columns forward FFT, the PFHX pole loop (octet items x pole
 // chunks) with the K = 0 corners, the R2C finish, columns/rows inverse FFT, separated by
 // cluster barriers; intermediate arrays live in L2 (plan workspace).
+constexpr int kSmallMaxClusters = 9;   // 16-CTA clusters on 148 SMs
 struct SmallArgs {
     const double *in[3];
     double *out[3];
@@ -154,6 +155,13 @@ struct SmallArgs {
     double scale;          // D^-2
     long n_items;          // octet work items (r2c_items(D, 2, true))
     int stop_after;        // measurement only (REXI_SMALL_STOP): return after stage 0..5 (A..F)
+    // distributed-shared-memory step (step_small2_kernel): the pole range split over
+    // n_clusters clusters, each with its own range sums; the per-cluster Hermitian spectra meet
+    // in cl_acc and the last cluster to arrive (counter) sums them and runs the inverse transform
+    int n_clusters;
+    cd Sg[kSmallMaxClusters], Sdg[kSmallMaxClusters];
+    cd *cl_acc;            // [n_clusters][3][D][D/2 + 1] (n_clusters > 1)
+    unsigned *counter;     // clusters arrived; 0 between launches (n_clusters > 1)
 };
 
 // ----------------------------------------------------------------------------- FFT passes

@@ -47,6 +47,11 @@ size_t small_step_smem(int D);
 long small_step_items(int D);
 constexpr int kSmallThreadsHost = 256;
 cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st);
+// the same step with every stage exchange through distributed shared memory and the pole range
+// split over a.n_clusters clusters (step_small2_kernel): cluster size (0: unavailable) and the
+// number of resident clusters of that size, launch
+int small2_cluster(int *resident);
+cudaError_t launch_step_small2(const SmallArgs &a, int cs, cudaStream_t st);
 // NEXT-3 1-D transforms: power-of-two n <= 2048 by Stockham passes (twiddle table of n entries
 // from launch_twiddles), other n by a direct DFT; out = scale * DFT(in) (inverse: e^{+})
 bool dft1d_uses_fft(long n);

@@ -230,6 +230,16 @@ typedef enum {
 } rexi_schedule_t;
 rexi_status_t rexi_plan_set_schedule(rexi_plan_t plan, int schedule);
 
+/* Clusters of the fused step (REXI_SCHEDULE_FUSED / AUTO's fused choice): the step's pole range
+ * is split into `clusters` contiguous blocks (sizes differ by <= 1), one 16-CTA cluster each
+ * (the terms are independent); every cluster runs the forward transform and its
+ * poles, writes its Hermitian partial spectrum, and the last cluster to finish sums the partials
+ * in cluster order and runs the inverse transform. 0 (default): chosen from the pole count
+ * (DESIGN.md 6.6); 1..9 fixed (capped at the clusters that can be resident at once and at the
+ * range length). Results differ only in the summation order. Clears the plan's graph cache.
+ * EINVAL outside 0..9. */
+rexi_status_t rexi_plan_set_fused_clusters(rexi_plan_t plan, int clusters);
+
 /* Whole-step CUDA graphs (default on): rexi_apply / rexi_apply_partial / rexi_apply_host /
  * rexi_run capture their kernel sequence once per (buffers, pole range, method, variant,
  * tuning, timing) on a private stream and replay it on `stream` afterwards (up to 8 cached

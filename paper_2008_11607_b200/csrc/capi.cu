@@ -65,6 +65,7 @@ struct rexi_plan_s {
     int occ_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // resident blocks per SM of the current tuning
     int sk_occ = 0;                            // same, stream-K R2C kernel
     int schedule = REXI_SCHEDULE_AUTO;
+    int fused_clusters = 0;   // rexi_plan_set_fused_clusters (0: from the pole count)
     int last_schedule = REXI_SCHEDULE_AUTO;
     // pole-kernel kind: 0 REXII DZ, 1 REXII UV, 2 REXI, 3 REXII DZ3, 4 REXII PF, 5 REXII PFH,
     // 6 REXII PFH on R2C pairs, collapsed (real input only; spectral calls use kind 5),
@@ -438,37 +439,42 @@ void range_sums(const rexi_plan_s *p, long b, long e, cd *S, cd *Sd) {
 }
 
 // The fused small-grid step (REXI_SCHEDULE_FUSED / AUTO, include/rexi.h): PFHX kind, D <= 128,
-// a non-empty pole range, cluster launch available; under AUTO only for small pole work.
-constexpr long kSmallWorkMax = 1L << 18;   // octet items x poles
+// a non-empty pole range, cluster launch available; under AUTO for D <= 64 and pole work up to
+// 2^19 octet item-poles (measured: at 64^2 the fused step with 8 clusters still takes half the
+// chunked path's time at 604 poles; at 128^2 it is at best even with it, tools/sweep_fused.py).
+constexpr long kSmallWorkMax = 1L << 19;   // octet items x poles
 bool small_eligible(const rexi_plan_s *p, long b, long e) {
     if (p->kind() != 7 || e <= b || p->host.D > 128) return false;
     if (p->schedule != REXI_SCHEDULE_FUSED && p->schedule != REXI_SCHEDULE_AUTO) return false;
-    if (p->schedule == REXI_SCHEDULE_AUTO && rexi::small_step_items(p->host.D) * (e - b) > kSmallWorkMax)
+    if (p->schedule == REXI_SCHEDULE_AUTO &&
+        (p->host.D > 64 || rexi::small_step_items(p->host.D) * (e - b) > kSmallWorkMax))
         return false;
     // AUTO falls back to the multi-launch path without a cluster launch; an explicit FUSED
     // request then fails in do_step_small (no silent change of schedule)
-    return p->schedule == REXI_SCHEDULE_FUSED || rexi::small_step_cluster() > 0;
+    return p->schedule == REXI_SCHEDULE_FUSED || rexi::small2_cluster(nullptr) > 0;
+}
+
+// Clusters of the fused step when the plan leaves the choice open, from the pole work w = octet
+// items x poles of the range (measured on B200, tools/sweep_fused.py): one
+// cluster up to w = 30 000 (C1: 558 x 47), then 4..8 clusters, one per ~40 000 item-poles.
+int fused_clusters_auto(long items, long n) {
+    const long w = items * n;
+    if (w <= 30000) return 1;
+    return (int)std::min(8L, std::max(4L, (w + 39999) / 40000));
 }
 
 rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
                             const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
-    // REXI_SMALL_V1=1 (measurement knob): the first fused kernel, stage exchanges through L2
-    static const bool v1 = [] { const char *v = getenv("REXI_SMALL_V1"); return v && atoi(v) != 0; }();
     int resident = 0;
-    const int cs = v1 ? rexi::small_step_cluster() : rexi::small2_cluster(&resident);
+    const int cs = rexi::small2_cluster(&resident);
     if (cs <= 0) return fail(REXI_ECUDA, "fused small-grid step: thread-block cluster launch unavailable");
+    if (e - b > (1L << 27)) return fail(REXI_EINVAL, "fused small-grid step: pole range above 2^27");
     const long n = p->n_modes;
     const int D = p->host.D;
     const long items = rexi::small_step_items(D);
-    const long W = (long)cs * rexi::kSmallThreadsHost - 128;   // pole workers (kernels.cu)
-    long chunks = std::min(e - b, std::max(1L, W / items));
-    chunks = std::max(1L, std::min(chunks, (long)p->max_chunks));
-    cd S, Sd;
-    range_sums(p, b, e, &S, &Sd);
     rexi::SmallArgs a;
     a.in[0] = eta; a.in[1] = u; a.in[2] = v;
     a.out[0] = eo; a.out[1] = uo; a.out[2] = vo;
-    a.half = p->d_tmp;
     a.tw = p->d_tw;
     a.scale = 1.0 / ((double)D * (double)D);
     a.n_items = items;
@@ -479,70 +485,56 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     }
     rexi::PoleArgs &q = a.pole;
     q = rexi::PoleArgs{};
-    q.fhat = p->d_fhat;
-    q.partial = p->d_partial;
-    q.poles = p->d_poles;
-    q.rpoles = p->d_rpoles;
     q.xpoles = p->d_xpoles;
     q.ksym = p->d_ksym;
     q.pole_begin = b;
     q.pole_end = e;
     q.n_modes = n;
-    q.n_chunks = (int)chunks;
     q.D = D;
     q.log2D = 0;
     while ((1 << q.log2D) < D) ++q.log2D;
     q.tau = p->host.tau;
     q.hmu = p->host.poles[0].ar;
-    q.partial_cap = 3 * n * (long)p->max_chunks;
     q.n_poles = p->host.n_poles;
-    rexi::FinishArgs &f = a.fin;
-    f = rexi::FinishArgs{};
-    f.partial = p->d_partial;
-    f.acc = p->d_acc;
-    f.fhat = p->d_fhat;
-    f.ksym = p->d_ksym;
-    f.n_modes = n;
-    f.n_chunks = (int)chunks;
-    f.D = D;
-    f.log2D = q.log2D;
-    f.kind = 7;
-    f.tau = p->host.tau;
-    f.S = S;
-    f.Sd = Sd;
-    f.partial_cap = q.partial_cap;
-    f.half_out = 1;   // stage E reads the columns k <= D/2 only
-    rexi::FixupArgs &x = a.fix;
-    x.method = p->method;
-    x.write_eta = 1;
-    x.S = S;
-    x.fhat = p->d_fhat;
-    x.acc = p->d_acc;
-    x.poles = p->d_poles;
-    x.pole_begin = b;
-    x.pole_end = e;
-    x.n_modes = n;
-    x.D = D;
-    // DSMEM kernel: the pole range split over nc clusters (REXI_SMALL_NC: measurement knob)
-    {
-        static const int nc_env = [] { const char *v = getenv("REXI_SMALL_NC"); return v ? atoi(v) : 0; }();
-        int nc = nc_env > 0 ? nc_env : 1;
-        nc = (int)std::max(1L, std::min<long>({(long)nc, (long)rexi::kSmallMaxClusters, e - b}));
-        if (resident > 0) nc = std::min(nc, std::max(1, resident));
-        const long need = (long)nc * 3 * D * (D / 2 + 1);
-        if (need > 3 * n * (long)p->max_chunks) nc = 1;
-        a.n_clusters = nc;
-        for (int g = 0; g < nc; ++g) {
-            const long gb = b + (e - b) * g / nc, ge = b + (e - b) * (g + 1) / nc;
-            range_sums(p, gb, ge, &a.Sg[g], &a.Sdg[g]);
-        }
-        a.cl_acc = p->d_partial;
-        a.counter = p->d_counter;
+    a.poles = p->d_poles;
+    a.method = p->method;
+    // the pole range split over nc clusters, each with its own range sums
+    int nc = p->fused_clusters > 0 ? p->fused_clusters : fused_clusters_auto(items, e - b);
+    nc = (int)std::max(1L, std::min<long>({(long)nc, (long)rexi::kSmallMaxClusters, e - b}));
+    if (resident > 0) nc = std::min(nc, resident);
+    if ((long)nc * 3 * D * (D / 2 + 1) > 3 * n * (long)p->max_chunks) nc = 1;
+    a.n_clusters = nc;
+    for (int g = 0; g < nc; ++g) {
+        const long gb = b + (e - b) * g / nc, ge = b + (e - b) * (g + 1) / nc;
+        range_sums(p, gb, ge, &a.Sg[g], &a.Sdg[g]);
     }
+    a.cl_acc = p->d_partial;
+    a.counter = p->d_counter;
     rexi_status_t s;
     if ((s = record(p, st, true)) != REXI_OK) return s;
-    if (v1) CK(rexi::launch_step_small(a, cs, st));
-    else CK(rexi::launch_step_small2(a, cs, st));
+    // REXI_SMALL_TRACE=1 (measurement knob, graphs off): clock64 marks per CTA, printed to stderr
+    static const bool trace = [] { const char *v = getenv("REXI_SMALL_TRACE"); return v && atoi(v) != 0; }();
+    static long long *d_trace = nullptr;
+    const size_t trace_n = (size_t)cs * nc * 2 * 16;
+    a.trace = nullptr;
+    if (trace && !p->capturing) {
+        if (!d_trace) CK(cudaMalloc(&d_trace, (size_t)rexi::kSmallMaxClusters * 16 * 2 * 16 * sizeof(long long)));
+        CK(cudaMemsetAsync(d_trace, 0, trace_n * sizeof(long long), st));
+        a.trace = d_trace;
+    }
+    CK(rexi::launch_step_small2(a, cs, st));
+    if (a.trace) {
+        std::vector<long long> h(trace_n);
+        CK(cudaMemcpyAsync(h.data(), d_trace, trace_n * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (size_t c = 0; c < (size_t)cs * nc; ++c)
+            for (int w = 0; w < 2; ++w) {
+                const long long *t = h.data() + (c * 2 + w) * 16;
+                fprintf(stderr, "REXI_SMALL_TRACE cta %zu t%d:", c, w ? 255 : 0);
+                for (int k = 1; k < 16; ++k) fprintf(stderr, " %lld", t[k] ? t[k] - t[0] : -1LL);
+                fprintf(stderr, "\n");
+            }
+    }
     if ((s = record(p, st, false)) != REXI_OK) return s;
     p->pole_launches += 1;
     p->launches += 1;
@@ -926,6 +918,15 @@ rexi_status_t rexi_plan_set_schedule(rexi_plan_t p, int schedule) {
         return fail(REXI_EINVAL, "unknown schedule");
     DeviceGuard g(p->device);
     p->schedule = schedule;
+    p->clear_graphs();
+    return REXI_OK;
+}
+
+rexi_status_t rexi_plan_set_fused_clusters(rexi_plan_t p, int clusters) {
+    if (!p) return fail(REXI_EINVAL, "null plan");
+    if (clusters < 0 || clusters > rexi::kSmallMaxClusters) return fail(REXI_EINVAL, "clusters outside 0..9");
+    DeviceGuard g(p->device);
+    p->fused_clusters = clusters;
     p->clear_graphs();
     return REXI_OK;
 }

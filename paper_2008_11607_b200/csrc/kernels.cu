@@ -1748,282 +1748,22 @@ __global__ void __launch_bounds__(256) hermitian_kernel(const cd *__restrict__ i
 
 // ============================================================================= launchers
 // ============================================================================= fused small-grid step
-// For small grids the seven launches of a step (4 FFT passes, pole kernel, finish, K = 0 fix-up)
-// cost more in launch gaps than in work (C1: 64^2, 47 poles). This kernel runs the whole step
-// S1..S5 in ONE launch of one thread-block cluster (16 CTAs when the device allows a non-portable
-// cluster size, else 8), the stages separated by cluster barriers (barrier.cluster arrive.release /
-// wait.acquire, after a __threadfence): the intermediate arrays (half spectra, spectrum, chunk
-// partials, accumulator) stay in L2 in the plan's workspace, read back with ld.global.cg.
-//   A  forward rows (two real rows per complex transform)      -> half   (fft_rows_fwd_kernel)
-//   B  forward half-spectrum columns, D^-2                      -> fhat   (fft_cols_fwd_kernel)
-//   C  PFHX pole loop: thread (item, chunk) runs its poles      -> partial (pole_kernel_r2x)
-//      + the four K = 0 corners, one warp each                  -> acc    (fixup_k0_kernel)
-//   D  R2C finish of every pair                                 -> acc    (finish_kernel)
-//   E  inverse columns (Hermitian input)                        -> half   (fft_cols_inv_kernel<0>)
-//   F  inverse rows                                             -> out    (fft_rows_inv_kernel)
-// Same arithmetic as the multi-launch path stage by stage (shared device functions), except the
-// K = 0 pole sums, which are reduced across a warp in a different order.
 constexpr int kSmallThreads = 256;
 
 namespace cgx = cooperative_groups;
 
-// cluster-wide barrier: barrier.cluster.arrive (.release) + wait (.acquire) — orders the
-// global-memory writes of one stage before the reads of the next across the cluster's CTAs
+// cluster-wide barrier: barrier.cluster.arrive (.release) + wait (.acquire) — orders the shared::
+// cluster and global-memory accesses of one stage before those of the next across the cluster
 __device__ __forceinline__ void cluster_barrier() { cgx::this_cluster().sync(); }
 
-// The four K = 0 corners (self-mirror modes), one warp per corner: the Coriolis 2x2 solves of
-// fixup_k0_kernel summed over the pole range, lanes striding the poles, then a warp reduction.
-__device__ __forceinline__ void fixup_k0_warp(const FixupArgs &a, int corner, int lane) {
-    const int D = a.D, H = D / 2;
-    const int ls[4] = {0, 0, H, H}, ks[4] = {0, H, 0, H};
-    const long m = (long)ls[corner] * D + ks[corner];
-    const long n = a.n_modes;
-    const cd ua = ld_spec<true>(a.fhat + n + m), vb = ld_spec<true>(a.fhat + 2 * n + m);
-    cd Au = mk(0, 0), Av = mk(0, 0);
-    for (long p = a.pole_begin + lane; p < a.pole_end; p += 32) {
-        const PoleConst *P = a.poles + p;
-        const cd s3 = mk(__ldg(&P->s3r), __ldg(&P->s3i)), s4 = mk(__ldg(&P->s4r), __ldg(&P->s4i));
-        const cd w1 = mk(__ldg(&P->w1r), __ldg(&P->w1i)), w2 = mk(__ldg(&P->w2r), __ldg(&P->w2i));
-        const cd u1 = cfms(s4, vb, cmul(s3, ua));
-        const cd v1 = cfma(s3, vb, cmul(s4, ua));
-        if (a.method == 1) {   // REXI: one solve per term
-            Au = cfma(w1, u1, Au);
-            Av = cfma(w1, v1, Av);
-            continue;
-        }
-        const cd u2 = cjfma(s4, v1, cjfma(s3, u1, mk(0, 0)));
-        const cd v2 = cjfms(s4, u1, cjfma(s3, v1, mk(0, 0)));
-        Au = cfma(w2, u2, cfma(w1, u1, Au));
-        Av = cfma(w2, v2, cfma(w1, v1, Av));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        Au.x += __shfl_xor_sync(0xffffffffu, Au.x, o);
-        Av.x += __shfl_xor_sync(0xffffffffu, Av.x, o);
-    }
-    if (lane == 0) {
-        // the R2C accumulator is the Hermitian part, at a self-mirror mode Re A; eta = S e0 there
-        a.acc[m] = mk(cmul(a.S, ld_spec<true>(a.fhat + m)).x, 0.0);
-        a.acc[n + m] = mk(Au.x, 0.0);
-        a.acc[2 * n + m] = mk(Av.x, 0.0);
-    }
-}
-
-// Pole records cached in shared memory when the range fits (loaded while stage A runs).
+// Pole records cached in shared memory when the cluster's range fits (loaded before stage A).
 constexpr int kSmallPoleCache = 256;
 
-// Stages A, B, E, F split the 3 H row pairs (A, F) / half-spectrum columns (B, E) of the three
-// fields over the cluster's CTAs; the pole stage C and the finish D use every CTA. (Giving each
-// field's whole 2-D transform to one CTA, three barriers instead of five, measured 20 % slower:
-// the transform chain of one CTA is longer than two cluster barriers.)
-template <int LOGD>
-__global__ void __launch_bounds__(kSmallThreads, 1) step_small_kernel(SmallArgs a) {
-    constexpr int D = 1 << LOGD, H = D >> 1, LOGH = LOGD - 1;
-    constexpr int tf = D >= 8 ? D / 8 : 1;
-    constexpr int PL = padded_len(D);
-    constexpr int stride = PL + 1;   // column slabs
-    constexpr long n = (long)D * D;
-    extern __shared__ cd smem[];
-    cgx::cluster_group cl = cgx::this_cluster();
-    const int CS = (int)cl.num_blocks();
-    const int cta = (int)cl.block_rank();
-    const int tid = threadIdx.x, NT = blockDim.x;
-    constexpr int P3 = 3 * H;        // row pairs (A, F) = half-spectrum columns (B, E), all fields
-    const int u0 = (int)((long)P3 * cta / CS), u1 = (int)((long)P3 * (cta + 1) / CS);
-    const int nu = u1 - u0;          // this CTA's row pairs / columns
-    const int nu_max = (P3 + CS - 1) / CS;
-    if (a.stop_after < -1) return;   // stage-timing measurements only
-    rx_poison_smem();
-    RX_ASSERT(nu <= nu_max && u1 <= P3);
-    // pole cache after the FFT region, then the twiddle table (D) and the symbols (D doubles)
-    R2XPole *pc = reinterpret_cast<R2XPole *>(smem + nu_max * stride);
-    cd *tws = smem + nu_max * stride + kSmallPoleCache * (int)(sizeof(R2XPole) / sizeof(cd));
-    double *ks = reinterpret_cast<double *>(tws + D);
-    const long pb = a.pole.pole_begin, npl = a.pole.pole_end - a.pole.pole_begin;
-    const bool cached = npl <= kSmallPoleCache;
-    if (cached) {
-        const double2 *src = reinterpret_cast<const double2 *>(a.pole.xpoles + pb);
-        double2 *dst = reinterpret_cast<double2 *>(pc);
-        constexpr int kPer = (int)(sizeof(R2XPole) / sizeof(double2));
-        for (int i = tid; i < npl * kPer; i += NT) {
-            RX_SMEM(nu_max * stride + i);
-            dst[i] = __ldg(src + i);
-        }
-    }
-    for (int i = tid; i < D; i += NT) {
-        RX_SMEM((tws - smem) + i);
-        RX_SMEM((tws - smem) + D + i / 2);
-        tws[i] = a.tw[i];
-        ks[i] = __ldg(a.pole.ksym + i);
-    }
-    __syncthreads();
-    PoleArgs pa = a.pole;
-    pa.ksym = ks;
-    FinishArgs fa = a.fin;
-    fa.ksym = ks;
-    if (a.stop_after < 0) return;   // stage-timing measurements only
-
-    // ---- A: forward rows
-    for (int i = tid; i < nu * D; i += NT) {
-        const int pr = i >> LOGD, x = i & (D - 1);
-        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
-        const double *in = a.in[f];
-        const size_t g = (size_t)(2 * pair) * D + x;
-        RX_ASSERT(f < 3 && g + D < (size_t)n);
-        smem[pr * PL + pidx(x)] = mk(__ldg(in + g), __ldg(in + g + D));
-    }
-    __syncthreads();
-    {
-        const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<false, true>(smem + row * PL, D, LOGD, t, tf, tws, row < nu);
-    }
-    for (int i = tid; i < nu * H; i += NT) {
-        const int pr = i >> LOGH, k = i & (H - 1);
-        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
-        const cd *Z = smem + pr * PL;
-        cd X1, X2;
-        if (k == 0) {
-            const cd z0 = Z[pidx(0)], zh = Z[pidx(H)];
-            X1 = mk(z0.x, zh.x);
-            X2 = mk(z0.y, zh.y);
-        } else {
-            const cd zk = Z[pidx(k)], zm = Z[pidx(D - k)];
-            X1 = mk(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-            X2 = mk(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-        }
-        const size_t g = (size_t)f * n + (size_t)(2 * pair) * D + k;
-        a.half[g] = X1;
-        a.half[g + D] = X2;
-    }
-    cluster_barrier();
-
-    if (a.stop_after <= 0) return;   // stage-timing measurements only
-    // ---- B: forward columns of the half spectra -> full spectrum (F(-K) = conj F(K)), D^-2
-    for (int i = tid; i < nu * D; i += NT) {
-        const int c = i >> LOGD, l = i & (D - 1);
-        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
-        smem[c * stride + pidx(l)] = ld_spec<true>(a.half + (size_t)f * n + (size_t)l * D + k);
-    }
-    __syncthreads();
-    {
-        const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<false, true>(smem + col * stride, D, LOGD, t, tf, tws, col < nu);
-    }
-    {
-        const double sc = a.scale;
-        cd *fhat = const_cast<cd *>(a.pole.fhat);
-        for (int i = tid; i < nu * D; i += NT) {
-            const int c = i >> LOGD, l = i & (D - 1);
-            const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
-            const int lm = (D - l) & (D - 1);
-            const cd v = smem[c * stride + pidx(l)];
-            cd *out = fhat + (size_t)f * n;
-            if (k == 0) {
-                const cd w = smem[c * stride + pidx(lm)];
-                const double hs = 0.5 * sc;
-                out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
-                out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
-            } else {
-                out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
-                out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);
-            }
-        }
-    }
-    cluster_barrier();
-
-    if (a.stop_after <= 1) return;   // stage-timing measurements only
-    // ---- C: pole loop (thread = (octet item, pole chunk)) and the K = 0 corners
-    {
-        // every thread but the last four warps of the cluster works on (item, chunk) units
-        const long gt = (long)cta * NT + tid;
-        const long W = (long)CS * NT - 128;
-        const long items = a.n_items;
-        const int chunks = a.pole.n_chunks;
-        for (long w = gt; gt < W && w < items * chunks; w += W) {
-            const long item = w % items;
-            const int chunk = (int)(w / items);
-            const long p0 = npl * chunk / chunks;
-            const long p1 = npl * (chunk + 1) / chunks;
-            long rep[4];
-            bool ok[2];
-            double K2;
-            XPair st[4];
-            r2x_setup<true>(pa, item, st, rep, ok, K2);
-            if (cached) r2x_tile<2>(pc + p0, (int)(p1 - p0), K2, st);
-            else r2x_tile<1>(a.pole.xpoles + pb + p0, (int)(p1 - p0), K2, st);
-            r2x_store(a.pole, chunk, st, rep, ok);
-        }
-        if (gt >= W) fixup_k0_warp(a.fix, (int)((gt - W) >> 5), tid & 31);
-    }
-    cluster_barrier();
-
-    if (a.stop_after <= 2) return;   // stage-timing measurements only
-    // ---- D: R2C finish of every pair
-    for (long m = (long)cta * NT + tid; m < n; m += (long)CS * NT) finish_r2c_mode<true>(fa, m);
-    cluster_barrier();
-
-    if (a.stop_after <= 3) return;   // stage-timing measurements only
-    // ---- E: inverse columns (the accumulator is Hermitian: no symmetrisation)
-    for (int i = tid; i < nu * D; i += NT) {
-        const int c = i >> LOGD, l = i & (D - 1);
-        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
-        const cd *in = a.fin.acc + (size_t)f * n + (size_t)l * D;
-        cd v;
-        if (k == 0) {
-            const cd t0 = ld_spec<true>(in), th = ld_spec<true>(in + H);
-            v = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
-        } else {
-            v = ld_spec<true>(in + k);
-        }
-        smem[c * stride + pidx(l)] = v;
-    }
-    __syncthreads();
-    {
-        const int col = tid / tf, t = tid - col * tf;
-        fft_in_smem<true, true>(smem + col * stride, D, LOGD, t, tf, tws, col < nu);
-    }
-    for (int i = tid; i < nu * D; i += NT) {
-        const int c = i >> LOGD, r = i & (D - 1);
-        const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
-        a.half[(size_t)f * n + (size_t)r * D + k] = smem[c * stride + pidx(r)];
-    }
-    cluster_barrier();
-
-    if (a.stop_after <= 4) return;   // stage-timing measurements only
-    // ---- F: inverse rows -> the three real fields
-    for (int i = tid; i < nu * H; i += NT) {
-        const int pr = i >> LOGH, k = i & (H - 1);
-        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
-        const size_t g = (size_t)f * n + (size_t)(2 * pair) * D + k;
-        const cd g1 = ld_spec<true>(a.half + g), g2 = ld_spec<true>(a.half + g + D);
-        cd *Z = smem + pr * PL;
-        if (k == 0) {
-            Z[pidx(0)] = mk(g1.x, g2.x);
-            Z[pidx(H)] = mk(g1.y, g2.y);
-        } else {
-            Z[pidx(k)] = mk(g1.x - g2.y, g1.y + g2.x);        // g1 + i g2
-            Z[pidx(D - k)] = mk(g1.x + g2.y, g2.x - g1.y);    // conj g1 + i conj g2
-        }
-    }
-    __syncthreads();
-    {
-        const int row = tid / tf, t = tid - row * tf;
-        fft_in_smem<true, true>(smem + row * PL, D, LOGD, t, tf, tws, row < nu);
-    }
-    for (int i = tid; i < nu * D; i += NT) {
-        const int pr = i >> LOGD, x = i & (D - 1);
-        const int gp = u0 + pr, f = gp >> LOGH, pair = gp & (H - 1);
-        const cd v = smem[pr * PL + pidx(x)];
-        const size_t g = (size_t)(2 * pair) * D + x;
-        a.out[f][g] = v.x;
-        a.out[f][g + D] = v.y;
-    }
-}
-
-// ============================================================================= fused small-grid step, DSMEM
-// step_small2_kernel: the fused small-grid step with every exchange between stages through
-// distributed shared memory (DSMEM) instead of L2, and the pole range optionally split over
-// several clusters. Per cluster (CS CTAs of 256 threads):
+// For small grids the seven launches of a step (4 FFT passes, pole kernel, finish, K = 0 fix-up)
+// cost more in launch gaps than in work (C1: 64^2, 47 poles). step_small2_kernel runs the whole
+// step S1..S5 as ONE launch of thread-block clusters (16 CTAs where the device allows the
+// non-portable size, else 8), every exchange between stages through distributed shared memory
+// (DSMEM), the pole range optionally split over several clusters. Per cluster:
 //   A  forward rows (own row pairs, local slabs) -> X1, X2 stored into the column owners' slabs
 //   B  forward half-spectrum columns -> the spectrum rows l <= D/2, distributed by row over the
 //      cluster (row l in CTA l mod CS)
@@ -2155,10 +1895,13 @@ __device__ __forceinline__ bool r2x_pair_rep(long item, int D, int log2D, int j,
     return true;
 }
 
-// The n (<= nmax) length-D transforms at s + j * ld (j < n) in shared memory, tf threads each,
-// in rounds of blockDim / tf transforms (uniform round count: the passes hold block barriers).
-// Not inlined: the step runs its code once, cold, so one copy for the four stages (A, B, E, F)
-// costs less instruction fetch than four.
+// The n (<= nmax) length-D transforms at s + j * ld (j < n) in shared memory (natural order at
+// pidx(i), in place), X[k] = sum_i x[i] e^{-+2 pi i ik/D}, by the Stockham passes of the
+// multi-launch kernels (tf = D/8 threads per transform), in rounds of blockDim / tf transforms
+// (uniform round count: the passes hold block barriers). Not inlined: the step runs its code
+// once, cold, so one copy for the four stages (A, B, E, F) costs less instruction fetch than
+// four. (A warp-synchronous radix-2 variant with shfl.xor stages measured 1420 cycles against
+// 1230 for these passes on the C1 shape: tools/fft_probe.cu.)
 template <int LOGD>
 __device__ __noinline__ void small2_ffts(cd *s, int ld, int n, int nmax, const cd *tws, bool inv) {
     constexpr int D = 1 << LOGD, tf = D >= 8 ? D / 8 : 1;
@@ -2188,6 +1931,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     const int u0 = (P3 * cta) / CS, u1 = (P3 * (cta + 1)) / CS;
     const int nu = u1 - u0;
     if (a.stop_after < -1) return;   // stage-timing measurements only
+#define SMALL2_MARK(k)                                                             \
+    do {                                                                           \
+        if (a.trace && (tid == 0 || tid == kSmallThreads - 1))                     \
+            a.trace[((long)blockIdx.x * 2 + (tid != 0)) * 16 + (k)] = clock64();   \
+    } while (0)
+    SMALL2_MARK(0);
     cluster_arrive_relaxed();
     rx_poison_smem();
     RX_ASSERT(nu <= L.nu_max && (long)L.total * 16 <= (long)dyn_smem_bytes() && g < NC);
@@ -2205,7 +1954,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     if (cta == CS - 1 && tid >= kSmallThreads - 32) {
         // the corner warp's pole records (generic table, read in stage C): into L2 now
         for (long p = pb + (tid & 31); p < pb + npl; p += 32) {
-            const char *q = reinterpret_cast<const char *>(a.fix.poles + p);
+            const char *q = reinterpret_cast<const char *>(a.poles + p);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(q + sizeof(PoleConst) - 1));
         }
@@ -2255,12 +2004,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             ksm[tid] = ks0;
         }
     }
+    SMALL2_MARK(1);
     __syncthreads();
     if (a.stop_after < 0) {   // stage-timing measurements only
         cluster_wait();
         return;
     }
     small2_ffts<LOGD>(rr, PL, nu, L.nu_max, tws, false);
+    SMALL2_MARK(2);
     cluster_wait();   // every CTA of the cluster runs: DSMEM stores may start
     for (int i = tid; i < nu * H; i += NT) {
         const int pr = i >> LOGH, k = i & (H - 1);
@@ -2284,10 +2035,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     }
     cluster_barrier();
 
+    SMALL2_MARK(3);
     if (a.stop_after <= 0) return;   // stage-timing measurements only
     // ---- B: forward columns (local) -> the spectrum at every pair representative, D^-2, staged
     // in the shared memory of the CTA that owns the pair's octet item (and the K = 0 corners)
     small2_ffts<LOGD>(cs_, stride, nu, L.nu_max, tws, false);
+    SMALL2_MARK(13);
     {
         const double sc = a.scale;
         const int items = (int)a.n_items;
@@ -2316,8 +2069,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             }
         }
     }
+    SMALL2_MARK(14);
     cluster_barrier();
 
+    SMALL2_MARK(4);
     if (a.stop_after <= 1) return;   // stage-timing measurements only
     // ---- C + D: pole loop over (item, chunk) units, chunk partials in shared memory, finish
     const double c_tau = a.pole.tau;
@@ -2356,8 +2111,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             r2x_setup_ld(
                 a.pole, i0 + il, st, rep, ok, K2, [&](int f, long, int j) { return stg[(j * 3 + f) * L.ni_max + il]; },
                 [&](int i) { return ksm[i]; });
+            if (u == tid) SMALL2_MARK(5);
             const int p0 = npl * chunk / ch, p1 = a.stop_after == 2 ? p0 : npl * (chunk + 1) / ch;
             r2x_tile<2>(src + p0, p1 - p0, K2, st);
+            if (u == tid) SMALL2_MARK(6);
             cd *p = part + (size_t)chunk * 8 * ni + il;   // [chunk][pair][eta, delta'][item]
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -2380,7 +2137,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
                 Av[q] = 0.0;
             }
             for (long p = pb + lane; p < pb + npl && a.stop_after != 2; p += 32) {
-                const PoleConst *P = a.fix.poles + p;
+                const PoleConst *P = a.poles + p;
                 const cd s3 = mk(__ldg(&P->s3r), __ldg(&P->s3i)), s4 = mk(__ldg(&P->s4r), __ldg(&P->s4i));
                 const cd w1 = mk(__ldg(&P->w1r), __ldg(&P->w1i)), w2 = mk(__ldg(&P->w2r), __ldg(&P->w2i));
 #pragma unroll
@@ -2389,7 +2146,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
                     const cd v1 = cfma(s3, vb[q], cmul(s4, ua[q]));
                     // Re(w1 u1 + w2 u2): the self-mirror modes keep the real part (Hermitian part)
                     double ru = fma(w1.x, u1.x, -w1.y * u1.y), rv = fma(w1.x, v1.x, -w1.y * v1.y);
-                    if (a.fix.method != 1) {   // REXII: the second solve (REXI: one solve per term)
+                    if (a.method != 1) {   // REXII: the second solve (REXI: one solve per term)
                         const cd u2 = cjfma(s4, v1, cjfma(s3, u1, mk(0, 0)));
                         const cd v2 = cjfms(s4, u1, cjfma(s3, v1, mk(0, 0)));
                         ru = fma(w2.x, u2.x, fma(-w2.y, u2.y, ru));
@@ -2425,7 +2182,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
                 put_acc(2, l, k, mk(av, 0.0));
             }
         }
+        SMALL2_MARK(7);
         __syncthreads();
+        SMALL2_MARK(8);
         // D: finish every pair of the CTA's items (all threads): chunk partials in a fixed
         // order, then the formulas of finish_r2c_mode from the pair's spectrum
         for (int t = tid; t < ni * 4; t += NT) {
@@ -2463,11 +2222,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             }
         }
     }
+    SMALL2_MARK(9);
     if (NC > 1) {
-        // hand-off: the last cluster to arrive sums the clusters' spectra (fixed order) alone
-        __threadfence();
+        // hand-off: the last cluster to arrive sums the clusters' spectra (fixed order) alone.
+        // The cluster barrier orders every thread's cl_acc stores before thread 0's gpu-scope
+        // fence (cumulative), which precedes its arrival on the counter
         cluster_barrier();
         if (cta == 0 && tid == 0) {
+            __threadfence();
             const unsigned old = atomicAdd(a.counter, 1u);
             const int last = old == (unsigned)(NC - 1);
             if (last) *a.counter = 0u;   // every cluster has arrived: reset for the next launch
@@ -2505,9 +2267,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
         __syncthreads();
     }
 
+    SMALL2_MARK(10);
     if (a.stop_after <= 3) return;   // stage-timing measurements only
     // ---- E: inverse columns (Hermitian input) -> Z rows into the row-pair owners
     small2_ffts<LOGD>(cs_, stride, nu, L.nu_max, tws, true);
+    SMALL2_MARK(15);
     for (int i = tid; i < nu * H; i += NT) {
         const int c = i >> LOGH, p = i & (H - 1);
         const int gc = u0 + c, f = gc >> LOGH, k = gc & (H - 1);
@@ -2524,6 +2288,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     }
     cluster_barrier();
 
+    SMALL2_MARK(11);
     if (a.stop_after <= 4) return;   // stage-timing measurements only
     // ---- F: inverse rows (local) -> the three real fields
     small2_ffts<LOGD>(rr, PL, nu, L.nu_max, tws, true);
@@ -2535,6 +2300,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
         a.out[f][gi] = v.x;
         a.out[f][gi + D] = v.y;
     }
+    SMALL2_MARK(12);
+#undef SMALL2_MARK
 }
 
 static int ilog2(int x) {
@@ -2920,73 +2687,7 @@ cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pol
 // ----------------------------------------------------------------------------- fused small-grid step
 #define REXI_SMALL_LOGD(X) X(2) X(3) X(4) X(5) X(6) X(7)
 
-// FFT slabs of the smaller (8-CTA) cluster's share + the pole cache
-size_t small_step_smem(int D) {
-    const int cs = 8;
-    const int nu = (3 * (D / 2) + cs - 1) / cs;
-    return (size_t)nu * (padded_len(D) + 1) * sizeof(cd) + (size_t)kSmallPoleCache * sizeof(R2XPole) +
-           (size_t)D * (sizeof(cd) + sizeof(double));
-}
-
-// Cluster size (16 if the device allows a non-portable cluster of this kernel, else 8), or 0 if
-// cluster launch is unavailable. Cached per process (one device model per run).
-int small_step_cluster() {
-    static int cs = -1;
-    if (cs >= 0) return cs;
-    cs = 0;
-#define X(L)                                                                                                  \
-    cudaFuncSetAttribute(step_small_kernel<L>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);             \
-    if (cudaFuncSetAttribute(step_small_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
-                             (int)small_step_smem(1 << L)) != cudaSuccess) {                                   \
-        cudaGetLastError();                                                                                    \
-        return cs;                                                                                             \
-    }
-    REXI_SMALL_LOGD(X)
-#undef X
-    cudaGetLastError();
-    for (int want : {16, 8}) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(want);
-        cfg.blockDim = dim3(kSmallThreads);
-        cfg.dynamicSmemBytes = small_step_smem(128);
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = want;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, step_small_kernel<7>, &cfg) == cudaSuccess && nclusters >= 1) {
-            cs = want;
-            break;
-        }
-        cudaGetLastError();
-    }
-    return cs;
-}
-
 long small_step_items(int D) { return r2c_items(D, 2, true); }
-
-cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kSmallThreads);
-    cfg.dynamicSmemBytes = small_step_smem(a.pole.D);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-#define X(L) \
-    if (a.pole.log2D == L) return cudaLaunchKernelEx(&cfg, step_small_kernel<L>, a);
-    REXI_SMALL_LOGD(X)
-#undef X
-    return cudaErrorInvalidValue;
-}
 
 // DSMEM step (step_small2_kernel): shared memory per CTA for cluster size cs; the cluster size
 // (16 where the device allows the non-portable size, else 8; 0: no cluster launch) and how many

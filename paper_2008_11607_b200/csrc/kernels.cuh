@@ -139,29 +139,26 @@ struct FixupArgs {
 };
 
 // ----------------------------------------------------------------------------- fused small-grid step
-// One cluster of CTAs runs a whole physical step S1..S5 for small grids (kernels.cu
-// "fused small-grid step"): rows/columns forward FFT, the PFHX pole loop (octet items x pole
-// chunks) with the K = 0 corners, the R2C finish, columns/rows inverse FFT, separated by
-// cluster barriers; intermediate arrays live in L2 (plan workspace).
+// The whole physical step S1..S5 for small grids as one launch of thread-block clusters
+// (kernels.cu step_small2_kernel): forward FFT, PFHX pole loop with the K = 0 corners, R2C
+// finish and inverse FFT, the stages exchanging data through distributed shared memory; the pole
+// range split over n_clusters clusters whose partial spectra the last one to finish sums.
 constexpr int kSmallMaxClusters = 9;   // 16-CTA clusters on 148 SMs
 struct SmallArgs {
     const double *in[3];
     double *out[3];
-    cd *half;              // [3][D*D] scratch: half spectra (row layout of the FFT passes)
-    PoleArgs pole;         // fhat (written here), partial, xpoles, ksym, range, n_chunks, ...
-    FinishArgs fin;        // acc, S, Sd (partial, fhat, ksym as in pole)
-    FixupArgs fix;         // the four K = 0 corners (poles = generic table)
+    PoleArgs pole;         // xpoles, ksym, pole range, D, log2D, tau, hmu (r2x_setup_ld / r2x_tile)
+    const PoleConst *poles;   // generic pole table (K = 0 corners)
+    int method;            // 0: REXII, 1: REXI (corners: one solve per term)
     const cd *tw;
     double scale;          // D^-2
     long n_items;          // octet work items (r2c_items(D, 2, true))
-    int stop_after;        // measurement only (REXI_SMALL_STOP): return after stage 0..5 (A..F)
-    // distributed-shared-memory step (step_small2_kernel): the pole range split over
-    // n_clusters clusters, each with its own range sums; the per-cluster Hermitian spectra meet
-    // in cl_acc and the last cluster to arrive (counter) sums them and runs the inverse transform
+    int stop_after;        // measurement only (REXI_SMALL_STOP): return after stage 0..4
     int n_clusters;
-    cd Sg[kSmallMaxClusters], Sdg[kSmallMaxClusters];
+    cd Sg[kSmallMaxClusters], Sdg[kSmallMaxClusters];   // per-cluster range sums (finish S, Sd)
     cd *cl_acc;            // [n_clusters][3][D][D/2 + 1] (n_clusters > 1)
     unsigned *counter;     // clusters arrived; 0 between launches (n_clusters > 1)
+    long long *trace;      // measurement only (REXI_SMALL_TRACE): clock64 per CTA at stage marks
 };
 
 // ----------------------------------------------------------------------------- FFT passes

@@ -40,16 +40,11 @@ long sk_slots_bound(long tiles, long poles, long ctas);
 cudaError_t launch_finish_r2c_sk(const FinishArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_k0(const FixupArgs &a, cudaStream_t st, bool beside_pole_kernel);
 cudaError_t launch_hermitian(const cd *in, cd *out, long n_modes, int D, cudaStream_t st);
-// fused small-grid step (one cluster launch for S1..S5, PFHX kernel): cluster size (0: unavailable),
-// dynamic shared memory per CTA, octet work items, launch
-int small_step_cluster();
-size_t small_step_smem(int D);
+// fused small-grid step (step_small2_kernel): octet work items; cluster size (16 where the
+// device allows it, else 8; 0: cluster launch unavailable) and the number of resident clusters
+// of that size; launch of a.n_clusters clusters
 long small_step_items(int D);
 constexpr int kSmallThreadsHost = 256;
-cudaError_t launch_step_small(const SmallArgs &a, int cs, cudaStream_t st);
-// the same step with every stage exchange through distributed shared memory and the pole range
-// split over a.n_clusters clusters (step_small2_kernel): cluster size (0: unavailable) and the
-// number of resident clusters of that size, launch
 int small2_cluster(int *resident);
 cudaError_t launch_step_small2(const SmallArgs &a, int cs, cudaStream_t st);
 // NEXT-3 1-D transforms: power-of-two n <= 2048 by Stockham passes (twiddle table of n entries

@@ -51,6 +51,7 @@ EXPORTS = {
     "rexi_plan_set_method": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_schedule": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rexi_plan_set_fused_clusters": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rexi_plan_set_tuning": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "rexi_plan_coeffs": (ctypes.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "rexi_forward": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
@@ -233,6 +234,10 @@ class Plan:
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {sorted(SCHEDULES)}")
         _check(_lib.rexi_plan_set_schedule(self._h, SCHEDULES[schedule]), "rexi_plan_set_schedule")
+
+    def set_fused_clusters(self, clusters):
+        """Clusters the fused step splits its pole range over (0: automatic; rexi_plan_set_fused_clusters)."""
+        _check(_lib.rexi_plan_set_fused_clusters(self._h, int(clusters)), "rexi_plan_set_fused_clusters")
 
     def set_graphs(self, enable):
         _check(_lib.rexi_plan_set_graphs(self._h, int(bool(enable))), "rexi_plan_set_graphs")

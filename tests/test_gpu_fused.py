@@ -1,7 +1,8 @@
 """The fused small-grid step (REXI_SCHEDULE_FUSED; AUTO picks it for small PFHX steps): the whole
-S1..S5 as one thread-block-cluster launch (kernels.cu "fused small-grid step"), element by
-element against the oracle on full grids, including pole sub-ranges (one rank's share), the
-REXI method, graphs on/off and the host-buffer entry."""
+S1..S5 as one launch of thread-block clusters exchanging stage data through distributed shared
+memory (kernels.cu step_small2_kernel), element by element against the oracle on full grids,
+including the pole range split over 1..8 clusters, pole sub-ranges (one rank's share), the REXI
+method, graphs on/off and the host-buffer entry."""
 import numpy as np
 import pytest
 
@@ -61,6 +62,35 @@ def test_fused_step_vs_oracle(R, D, tau, tol, scen, graphs):
     q.set_schedule("chunked")
     other = [host(t) for t in q.apply(*(dev(x) for x in f))]
     assert rel(got, other) < 1e-13
+
+
+@pytest.mark.parametrize("clusters", [1, 2, 3, 8])
+@pytest.mark.parametrize("D,tau,scen", [(4, 0.5, "white"), (16, 1.0, "white"), (64, 0.02, "gauss"),
+                                        (64, 1.0, "white"), (128, 0.05, "white")])
+def test_fused_clusters_vs_oracle(R, D, tau, scen, clusters):
+    """The pole range split over `clusters` clusters (partial spectra summed by the last cluster
+    to finish, in cluster order) against the oracle; repeated launches reuse the arrival counter."""
+    f = inputs.gaussian_scenario(D) if scen == "gauss" else inputs.white_noise(D, seed=77)
+    p = R.Plan(D, tau, tol=1e-12)
+    p.set_schedule("fused")
+    p.set_fused_clusters(clusters)
+    fd = [dev(x) for x in f]
+    info = p.info
+    ref = lrsw.rexii_step(*f, tau, info["h"], info["M"])
+    first = [host(t) for t in p.apply(*fd)]
+    assert p.info["last_schedule"] == FUSED
+    assert rel(first, ref) < TOL
+    for _ in range(3):
+        again = [host(t) for t in p.apply(*fd)]
+    for x, y in zip(first, again):
+        assert np.array_equal(x, y)   # fixed summation order: bit-for-bit across launches
+
+
+def test_fused_clusters_rejects_out_of_range(R):
+    p = R.Plan(16, 0.5, tol=1e-12)
+    for bad in (-1, 10):
+        with pytest.raises(R.RexiError):
+            p.set_fused_clusters(bad)
 
 
 def test_auto_picks_fused_for_c1(R):

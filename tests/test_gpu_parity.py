@@ -402,12 +402,18 @@ def test_timing_counters(R):
     D = 64
     f = [dev(x) for x in inputs.white_noise(D)]
     p = R.Plan(D, 1.0)
+    p.set_schedule("chunked")             # seven launches per step
     p.timing_enable(True)
     p.timing_read()
     for _ in range(3):
         p.apply(*f)
     ms, pl, tl = p.timing_read()
     assert pl == 3 and ms > 0.0 and tl == 3 * 7
+    p.set_schedule("auto")                # 64^2, 604 poles: the fused step, one launch per step
+    for _ in range(3):
+        p.apply(*f)
+    ms, pl, tl = p.timing_read()
+    assert pl == 3 and ms > 0.0 and tl == 3
 
 
 TUNINGS = [("dz", 1, 1, 8), ("dz", 2, 1, 4), ("dz", 2, 1, 5), ("dz", 3, 1, 4), ("dz", 4, 1, 3),
@@ -560,6 +566,7 @@ def test_graphs_match_direct_and_timing(R):
     D = 64
     f = [dev(x) for x in inputs.white_noise(D)]
     p = R.Plan(D, 1.0)
+    p.set_schedule("chunked")             # the seven-launch graph (AUTO fuses 64^2 steps)
     p.set_graphs(False)
     a = [host(t) for t in p.apply(*f)]
     p.set_graphs(True)

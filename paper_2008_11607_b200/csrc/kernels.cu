@@ -582,6 +582,144 @@ __global__ void __launch_bounds__(512) fft_cols_inv16_kernel(FftArgs a) {
     }
 }
 
+namespace cgx = cooperative_groups;
+
+// cluster-wide barrier: barrier.cluster.arrive (.release) + wait (.acquire) — orders the shared::
+// cluster and global-memory accesses of one stage before those of the next across the cluster
+__device__ __forceinline__ void cluster_barrier() { cgx::this_cluster().sync(); }
+
+// ----------------------------------------------------------------------------- cluster column passes
+// Column passes for 1024 <= D <= 4096 with 128-byte row segments on every global load and store:
+// a cluster of 8 CTAs transforms 8 adjacent half-spectrum columns, four-step with D = 8 N2,
+// n = N2 n1 + n2, k = k1 + 8 k2:
+//   X[k1 + 8 k2] = sum_{n2} W_{N2}^{n2 k2} [ W_D^{n2 k1} sum_{n1} W_8^{n1 k1} x[N2 n1 + n2] ].
+// Stage 1, CTA c (rank in the cluster): thread (n2, col), n2 in [c N2/8, (c+1) N2/8), loads its
+// eight values x[N2 n1 + n2] straight from global memory (a warp: 4 rows x 8 columns), DFT-8 in
+// registers, twiddles W_D^{n2 k1}, and stores result k1 into the shared memory of CTA k1 of the
+// cluster (distributed shared memory, [n2][col]). Stage 2, after a cluster barrier: CTA k1 runs the
+// N2-point Stockham passes on its 8 columns and writes rows k1 + 8 k2. The single-CTA column
+// kernels above hold whole columns in one CTA, so at 4096^2 a load covers 2 columns = 32 bytes
+// of a row (0.32 of HBM, profiles/r02q_aux_c4.md). Output handling (scale, the packed k = 0 pair,
+// mirrors, half_out, the inverse's symmetrisation) as in fft_cols_fwd16 / fft_cols_inv16; the
+// k = 0 separation reads the mirror row from the CTA that holds it (the one cluster with col0 = 0).
+// MODE 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising.
+template <int LOGD>
+struct ColCl {
+    static constexpr int D = 1 << LOGD, H = D / 2, N2 = D / 8, LOGN2 = LOGD - 3;
+    static constexpr int T = N2;   // threads per CTA: one (n2, column) pair each in stage 1
+    static constexpr size_t SMEM = (size_t)(8 * N2 + N2) * sizeof(cd);   // [n2][8 columns] + N2 twiddles
+};
+
+struct ColIx {
+    int col;
+    __device__ __forceinline__ int operator()(int i) const { return i * 8 + col; }
+};
+
+template <int LOGD, int MODE>
+// (two CTAs per SM: <= 64 registers; unbounded the compiler takes 70-80, i.e. one CTA per SM)
+__global__ void __launch_bounds__(ColCl<LOGD>::T, 2) fft_cols_cl_kernel(FftArgs a) {
+    using L = ColCl<LOGD>;
+    constexpr int D = L::D, H = L::H, N2 = L::N2, T = L::T;
+    constexpr bool INV = MODE != 0;
+    extern __shared__ cd smem[];
+    cd *buf = smem;                 // [n2][8]
+    cd *tw2 = smem + 8 * N2;        // W_{N2}^j = W_D^{8 j}
+    rx_poison_smem();
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int c = (int)cl.block_rank();
+    const int f = blockIdx.y;
+    const int col0 = (int)(blockIdx.x / 8) * 8;
+    const int tid = threadIdx.x;
+    const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
+    cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
+    const double2 *twg = reinterpret_cast<const double2 *>(a.twiddle);
+    {
+        const double2 w = __ldg(twg + 8 * tid);
+        tw2[tid] = mk(w.x, w.y);
+    }
+    // ---- stage 1
+    {
+        const int col = tid & 7, n2 = c * (N2 / 8) + (tid >> 3);
+        const int k = col0 + col;
+        RX_ASSERT(k < H && n2 < N2);
+        cd v[8];
+#pragma unroll
+        for (int n1 = 0; n1 < 8; ++n1) {
+            const int l = N2 * n1 + n2;
+            if (MODE == 0) {
+                v[n1] = in[(size_t)l * D + k];
+            } else {
+                const int lm = (D - l) & (D - 1);
+                if (k == 0) {
+                    cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
+                    if (MODE == 2) {
+                        const cd m0 = in[(size_t)lm * D], mh = in[(size_t)lm * D + H];
+                        t0 = mk(0.5 * (t0.x + m0.x), 0.5 * (t0.y - m0.y));
+                        th = mk(0.5 * (th.x + mh.x), 0.5 * (th.y - mh.y));
+                    }
+                    v[n1] = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+                } else {
+                    cd t = in[(size_t)l * D + k];
+                    if (MODE == 2) {
+                        const cd m = in[(size_t)lm * D + (D - k)];
+                        t = mk(0.5 * (t.x + m.x), 0.5 * (t.y - m.y));
+                    }
+                    v[n1] = t;
+                }
+            }
+        }
+        dft8<INV>(v);
+#pragma unroll
+        for (int k1 = 0; k1 < 8; ++k1) {
+            cd y = v[k1];
+            if (k1 > 0) {
+                const double2 w = __ldg(twg + n2 * k1);   // W_D^{n2 k1}, n2 k1 < D
+                y = INV ? mk(fma(y.x, w.x, y.y * w.y), fma(y.y, w.x, -y.x * w.y))
+                        : mk(fma(y.x, w.x, -y.y * w.y), fma(y.y, w.x, y.x * w.y));
+            }
+            cl.map_shared_rank(buf, k1)[n2 * 8 + col] = y;
+        }
+    }
+    cluster_barrier();
+    // ---- stage 2: N2-point transforms of the 8 columns (k1 = c)
+    {
+        const int col = tid & 7, j = tid >> 3;
+        fft_in_smem_ix<INV, ColIx, true>(buf, ColIx{col}, N2, L::LOGN2, j, N2 / 8, tw2, true);
+    }
+    const double sc = a.scale;
+    if (MODE != 0) {
+        for (int i = tid; i < 8 * N2; i += T) {
+            const int k2 = i >> 3, col = i & 7;
+            const cd v = buf[i];
+            out[(size_t)(c + 8 * k2) * D + col0 + col] = mk(v.x * sc, v.y * sc);
+        }
+        return;
+    }
+    const bool zero = col0 == 0;   // uniform over the cluster
+    if (zero) cluster_barrier();   // every CTA's stage 2 done: the k = 0 mirror rows are readable
+    for (int i = tid; i < 8 * N2; i += T) {
+        const int k2 = i >> 3, col = i & 7;
+        const int l = c + 8 * k2, k = col0 + col;
+        const int lm = (D - l) & (D - 1);
+        const cd v = buf[i];
+        const bool lo = !a.half_out || l <= H, mlo = !a.half_out || lm <= H;
+        if (k == 0) {
+            // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
+            // FH = (G - conj G(-l)) / (2i); G(-l) is row lm = (lm & 7) + 8 (lm >> 3)
+            if (lo) {
+                const cd w = cl.map_shared_rank(buf, lm & 7)[(lm >> 3) * 8];
+                const double hs = 0.5 * sc;
+                out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
+                out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
+            }
+        } else {
+            if (lo) out[(size_t)l * D + k] = mk(v.x * sc, v.y * sc);
+            if (mlo) out[(size_t)lm * D + (D - k)] = mk(v.x * sc, -v.y * sc);   // F(-K) = conj F(K)
+        }
+    }
+    if (zero) cluster_barrier();   // no CTA leaves while another reads its shared memory
+}
+
 // Forward columns: half spectra -> full spectrum (scaled). Block = C adjacent slots of one
 // field; slot 0 is the packed (X[.][0], X[.][N/2]) pair of real columns.
 __global__ void __launch_bounds__(1024) fft_cols_fwd_kernel(FftArgs a) {
@@ -1750,11 +1888,6 @@ __global__ void __launch_bounds__(256) hermitian_kernel(const cd *__restrict__ i
 // ============================================================================= fused small-grid step
 constexpr int kSmallThreads = 256;
 
-namespace cgx = cooperative_groups;
-
-// cluster-wide barrier: barrier.cluster.arrive (.release) + wait (.acquire) — orders the shared::
-// cluster and global-memory accesses of one stage before those of the next across the cluster
-__device__ __forceinline__ void cluster_barrier() { cgx::this_cluster().sync(); }
 
 // Pole records cached in shared memory when the cluster's range fits (loaded before stage A).
 constexpr int kSmallPoleCache = 256;
@@ -2394,6 +2527,58 @@ static bool fft16_cols(int lg) {
     return !off && lg >= 10 && lg <= 13;
 }
 
+// cluster column kernels (fft_cols_cl_kernel) for D = 2048, 4096 (REXI_FFT_CL=0 selects the
+// single-CTA radix-16 ones; measured tools/time_fft.py, profiles/r02w_fft_cl.log: 4096^2 forward
+// 388 -> 288 us, inverse 358 -> 303 us on the apply path, 2048^2 -7 %; at 1024^2 the L2-resident
+// passes are latency-bound and gain nothing, at 8192^2 a cluster's 128 KB per CTA leaves one CTA
+// per SM); false also if this device cannot launch them
+static bool fft_cl_cols(int lg) {
+    static const int off = [] { const char *v = getenv("REXI_FFT_CL"); return v && atoi(v) == 0; }();
+    static int ok = -1;
+    if (ok < 0) {
+        ok = 1;
+#define SETCL(L)                                                                                         \
+    for (cudaError_t e : {cudaFuncSetAttribute(fft_cols_cl_kernel<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                               (int)ColCl<L>::SMEM),                                     \
+                          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                               (int)ColCl<L>::SMEM),                                     \
+                          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                               (int)ColCl<L>::SMEM)})                                    \
+        if (e != cudaSuccess) ok = 0;
+        SETCL(10) SETCL(11) SETCL(12)
+#undef SETCL
+        cudaGetLastError();
+    }
+    return !off && ok && lg >= 11 && lg <= 12;
+}
+
+static cudaError_t launch_cols_cl(int mode, const void *const i3[3], void *const o3[3], const cd *tw, int D,
+                                  double scale, cudaStream_t st, bool half_out) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(D / 2, 3);   // (H / 8 column groups) x 8 CTAs, fields
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 8;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    FftArgs a = fft_args(i3, o3, tw, D, 8, mode ? 1 : 0, scale);
+    a.half_out = half_out ? 1 : 0;
+#define COLCL(L)                                                                                         \
+    if (D == (1 << L)) {                                                                                 \
+        cfg.blockDim = dim3(ColCl<L>::T);                                                                \
+        cfg.dynamicSmemBytes = ColCl<L>::SMEM;                                                           \
+        if (mode == 0) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 0>, a);                     \
+        if (mode == 1) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 1>, a);                     \
+        return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 2>, a);                                    \
+    }
+    COLCL(10) COLCL(11) COLCL(12)
+#undef COLCL
+    return cudaErrorInvalidValue;
+}
+
 // mode 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising
 static cudaError_t launch_cols16(int mode, const void *const i3[3], void *const o3[3], const cd *tw, int D,
                                  double scale, cudaStream_t st, bool half_out = false) {
@@ -2452,6 +2637,7 @@ cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd 
     }
     const void *i3[3] = {half[0], half[1], half[2]};
     void *o3[3] = {out[0], out[1], out[2]};
+    if (fft_cl_cols(ilog2(D))) return launch_cols_cl(0, i3, o3, tw, D, scale, st, half_out);
     if (fft16_cols(ilog2(D))) return launch_cols16(0, i3, o3, tw, D, scale, st, half_out);
     FftArgs a = fft_args(i3, o3, tw, D, fft_cols_per_block(D), 0, scale);
     a.half_out = half_out ? 1 : 0;
@@ -2464,10 +2650,11 @@ cudaError_t launch_fft_forward(const double *const in[3], cd *const half[3], cd 
 cudaError_t launch_fft_inverse(const cd *const in[3], cd *const half[3], double *const out[3],
                                bool hermitian, const cd *tw, int D, cudaStream_t st) {
     const int tf = D >= 8 ? D / 8 : 1;
-    if (fft16_cols(ilog2(D))) {
+    if (fft_cl_cols(ilog2(D)) || fft16_cols(ilog2(D))) {
         const void *i3[3] = {in[0], in[1], in[2]};
         void *o3[3] = {half[0], half[1], half[2]};
-        cudaError_t e = launch_cols16(hermitian ? 1 : 2, i3, o3, tw, D, 1.0, st);
+        cudaError_t e = fft_cl_cols(ilog2(D)) ? launch_cols_cl(hermitian ? 1 : 2, i3, o3, tw, D, 1.0, st, false)
+                                              : launch_cols16(hermitian ? 1 : 2, i3, o3, tw, D, 1.0, st);
         if (e != cudaSuccess) return e;
     } else {
         const void *i3[3] = {in[0], in[1], in[2]};

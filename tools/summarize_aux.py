@@ -22,6 +22,7 @@ algo = {  # bytes that must move per launch (3 fields)
     "fft_rows_fwd16_kernel": 3 * n * (8 + 8),
     "fft_cols_fwd16_kernel": 3 * n * (8 + 8),       # apply path: rows l <= D/2 of the spectrum only
     "fft_cols_inv16_kernel": 3 * n * (8 + 8),
+    "fft_cols_cl_kernel": 3 * n * (8 + 8),          # cluster column passes (forward: half out)
     "fft_rows_inv16_kernel": 3 * n * (8 + 8),
     "fft_rows_inv_kernel": 3 * n * (8 + 8),         # half-spectrum rows in, real rows out
     "finish_kernel": None,   # chunk partials in (chunks x 32 B per pair) + 48 B per k <= D/2 mode out

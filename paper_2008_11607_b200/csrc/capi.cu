@@ -439,15 +439,15 @@ void range_sums(const rexi_plan_s *p, long b, long e, cd *S, cd *Sd) {
 }
 
 // The fused small-grid step (REXI_SCHEDULE_FUSED / AUTO, include/rexi.h): PFHX kind, D <= 128,
-// a non-empty pole range, cluster launch available; under AUTO for D <= 64 and pole work up to
-// 2^19 octet item-poles (measured: at 64^2 the fused step with 8 clusters still takes half the
-// chunked path's time at 604 poles; at 128^2 it is at best even with it, tools/sweep_fused.py).
+// a non-empty pole range, cluster launch available; under AUTO for pole work up to 2^19 octet
+// item-poles (measured, tools/sweep_fused.py, profiles/r02y_sweep_fused.jsonl: at 64^2 the fused
+// step takes half the chunked path's time up to 604 poles, at 128^2 it is 3-8 % faster up to 149
+// poles and slower from 377 on).
 constexpr long kSmallWorkMax = 1L << 19;   // octet items x poles
 bool small_eligible(const rexi_plan_s *p, long b, long e) {
     if (p->kind() != 7 || e <= b || p->host.D > 128) return false;
     if (p->schedule != REXI_SCHEDULE_FUSED && p->schedule != REXI_SCHEDULE_AUTO) return false;
-    if (p->schedule == REXI_SCHEDULE_AUTO &&
-        (p->host.D > 64 || rexi::small_step_items(p->host.D) * (e - b) > kSmallWorkMax))
+    if (p->schedule == REXI_SCHEDULE_AUTO && rexi::small_step_items(p->host.D) * (e - b) > kSmallWorkMax)
         return false;
     // AUTO falls back to the multi-launch path without a cluster launch; an explicit FUSED
     // request then fails in do_step_small (no silent change of schedule)

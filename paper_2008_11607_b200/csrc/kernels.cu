@@ -1103,11 +1103,11 @@ __device__ __forceinline__ void pair_setup(PairState &s, cd e, cd d, cd z, doubl
 //    a = b, axes, Nyquist lines), computed as a half-discarded octet.
 //  * !OCT: NQ quads per thread in linear quad order.
 // Quad 0 (the four K = 0 corners) is left to the fix-up kernel.
-__host__ __device__ __forceinline__ long r2c_n_oct(int D) {
+__host__ __device__ constexpr long r2c_n_oct(int D) {
     const long H = D >> 1;
     return H >= 3 ? (H - 1) * (H - 2) / 2 : 0;
 }
-__host__ __device__ __forceinline__ long r2c_items(int D, int nq, bool oct) {
+__host__ __device__ constexpr long r2c_items(int D, int nq, bool oct) {
     const long H = D >> 1;
     if (oct) return r2c_n_oct(D) + 3 * (H - 1);
     return ((long)D * D / 4 + nq - 1) / nq;
@@ -1931,8 +1931,8 @@ __host__ __device__ __forceinline__ int small2_item_owner(int item, int items, i
     const int c = ((item + 1) * (256 * CS - 32) - 1) / (items * 256);
     return c < CS - 1 ? c : CS - 1;
 }
-__host__ __device__ __forceinline__ Small2Layout small2_layout(int D, int CS) {
-    Small2Layout L;
+__host__ __device__ constexpr Small2Layout small2_layout(int D, int CS) {
+    Small2Layout L{};
     const int H = D / 2, PL = padded_len(D);
     L.nu_max = (3 * H + CS - 1) / CS;
     const long items = r2c_items(D, 2, true), capb = 256L * CS - 32;
@@ -2019,11 +2019,12 @@ __device__ __forceinline__ bool r2x_pair_rep(long item, int D, int log2D, int j,
     long quad[2];
     bool ok[2], shared_k2;
     r2c_octet_item(item, D, quad, ok, shared_k2);
-    const int g = j >> 1;
-    if (!ok[g]) return false;
+    const bool g1 = (j >> 1) != 0;   // selects, not a runtime array index (no local memory)
+    if (!(g1 ? ok[1] : ok[0])) return false;
+    const long qs = g1 ? quad[1] : quad[0];
     long mq[4];
-    quad_modes(quad[g], D, log2D, mq);
-    const int qa = (int)(quad[g] >> (log2D - 1)), qb = (int)(quad[g] & (H - 1));
+    quad_modes(qs, D, log2D, mq);
+    const int qa = (int)(qs >> (log2D - 1)), qb = (int)(qs & (H - 1));
     rep = (j & 1) == 0 ? mq[0] : ((qa > 0 && qb > 0) ? mq[1] : mq[2]);
     return true;
 }
@@ -2046,7 +2047,7 @@ __device__ __noinline__ void small2_ffts(cd *s, int ld, int n, int nmax, const c
     }
 }
 
-template <int LOGD>
+template <int LOGD, int CS>
 __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs a) {
     constexpr int D = 1 << LOGD, H = D >> 1, LOGH = LOGD - 1;
     constexpr int PL = padded_len(D);
@@ -2055,12 +2056,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     extern __shared__ cd smem[];
     __shared__ int s_last;
     cgx::cluster_group cl = cgx::this_cluster();
-    const int CS = (int)cl.num_blocks();
     const int cta = (int)cl.block_rank();
     const int g = (int)(blockIdx.x / (unsigned)CS);   // cluster index
     const int NC = a.n_clusters;
-    const int tid = threadIdx.x, NT = blockDim.x;
-    const Small2Layout L = small2_layout(D, CS);
+    const int tid = threadIdx.x;
+    constexpr int NT = kSmallThreads;
+    // every offset a compile-time constant (CS is a template parameter): fewer live registers
+    constexpr Small2Layout L = small2_layout(D, CS);
     const int u0 = (P3 * cta) / CS, u1 = (P3 * (cta + 1)) / CS;
     const int nu = u1 - u0;
     if (a.stop_after < -1) return;   // stage-timing measurements only
@@ -2086,6 +2088,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     const bool cached = npl <= kSmallPoleCache;
     if (cta == CS - 1 && tid >= kSmallThreads - 32) {
         // the corner warp's pole records (generic table, read in stage C): into L2 now
+#pragma unroll 1
         for (long p = pb + (tid & 31); p < pb + npl; p += 32) {
             const char *q = reinterpret_cast<const char *>(a.poles + p);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
@@ -2246,7 +2249,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
                 [&](int i) { return ksm[i]; });
             if (u == tid) SMALL2_MARK(5);
             const int p0 = npl * chunk / ch, p1 = a.stop_after == 2 ? p0 : npl * (chunk + 1) / ch;
-            r2x_tile<2>(src + p0, p1 - p0, K2, st);
+            r2x_tile<1>(src + p0, p1 - p0, K2, st);   // one pole per trip: half the code of PU = 2
             if (u == tid) SMALL2_MARK(6);
             cd *p = part + (size_t)chunk * 8 * ni + il;   // [chunk][pair][eta, delta'][item]
 #pragma unroll
@@ -2343,15 +2346,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
             const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
             const int lm = (D - l) & (D - 1), km = (D - k) & (D - 1);
-            if (k <= H) {
-                put_acc(0, l, k, h0);
-                put_acc(1, l, k, U);
-                put_acc(2, l, k, V);
-            }
-            if (km <= H) {
-                put_acc(0, lm, km, mk(h0.x, -h0.y));
-                put_acc(1, lm, km, mk(U.x, -U.y));
-                put_acc(2, lm, km, mk(V.x, -V.y));
+            const cd hv[3] = {h0, U, V};
+            // the pair's two modes (the -K one conjugated) wherever k <= H; one copy of the stores
+#pragma unroll 1
+            for (int q = 0; q < 6; ++q) {
+                const int fq = q % 3;
+                const bool mir = q >= 3;
+                if (mir ? km <= H : k <= H) {
+                    const cd x = fq == 0 ? hv[0] : fq == 1 ? hv[1] : hv[2];   // (no local-memory array)
+                    put_acc(fq, mir ? lm : l, mir ? km : k, mir ? mk(x.x, -x.y) : x);
+                }
             }
         }
     }
@@ -2887,8 +2891,10 @@ int small2_cluster(int *resident) {
         g_small2_cs = 0;
         bool ok = true;
 #define X(L)                                                                                                  \
-    cudaFuncSetAttribute(step_small2_kernel<L>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);            \
-    if (cudaFuncSetAttribute(step_small2_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+    cudaFuncSetAttribute(step_small2_kernel<L, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);        \
+    if (cudaFuncSetAttribute(step_small2_kernel<L, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                             (int)small2_smem(1 << L, 16)) != cudaSuccess ||                                   \
+        cudaFuncSetAttribute(step_small2_kernel<L, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
                              (int)small2_smem(1 << L, 8)) != cudaSuccess)                                      \
         ok = false;
         REXI_SMALL_LOGD(X)
@@ -2908,8 +2914,9 @@ int small2_cluster(int *resident) {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, step_small2_kernel<7>, &cfg) == cudaSuccess &&
-                nclusters >= 1) {
+            const cudaError_t e = want == 16 ? cudaOccupancyMaxActiveClusters(&nclusters, step_small2_kernel<7, 16>, &cfg)
+                                             : cudaOccupancyMaxActiveClusters(&nclusters, step_small2_kernel<7, 8>, &cfg);
+            if (e == cudaSuccess && nclusters >= 1) {
                 g_small2_cs = want;
                 g_small2_resident = nclusters;
                 break;
@@ -2922,7 +2929,7 @@ int small2_cluster(int *resident) {
 }
 
 cudaError_t launch_step_small2(const SmallArgs &a, int cs, cudaStream_t st) {
-    if (a.n_clusters < 1 || a.n_clusters > kSmallMaxClusters) return cudaErrorInvalidValue;
+    if (a.n_clusters < 1 || a.n_clusters > kSmallMaxClusters || (cs != 16 && cs != 8)) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs * a.n_clusters);
     cfg.blockDim = dim3(kSmallThreads);
@@ -2935,8 +2942,10 @@ cudaError_t launch_step_small2(const SmallArgs &a, int cs, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-#define X(L) \
-    if (a.pole.log2D == L) return cudaLaunchKernelEx(&cfg, step_small2_kernel<L>, a);
+#define X(L)                                                                                         \
+    if (a.pole.log2D == L)                                                                           \
+        return cs == 16 ? cudaLaunchKernelEx(&cfg, step_small2_kernel<L, 16>, a)                     \
+                        : cudaLaunchKernelEx(&cfg, step_small2_kernel<L, 8>, a);
     REXI_SMALL_LOGD(X)
 #undef X
     return cudaErrorInvalidValue;

@@ -208,13 +208,16 @@ rexi_status_t rexi_plan_set_tuning(rexi_plan_t plan, int modes_per_thread, int p
  *                         iteration space evenly (no wave tail); one partial per tile segment.
  *                         (PFHR only.)
  *  REXI_SCHEDULE_FUSED:   the whole physical step S1..S5 (rexi_apply / apply_partial /
- *                         apply_host) as ONE launch of a thread-block cluster (16 CTAs, or 8):
+ *                         apply_host) as ONE launch of thread-block clusters (16 CTAs, or 8):
  *                         FFT passes, PFHX pole loop, K = 0 corners, finish and inverse FFT
- *                         separated by cluster barriers, intermediates in L2 (kernels.cu "fused
- *                         small-grid step"). PFHX plans with D <= 128 only (else CHUNKED).
- *  REXI_SCHEDULE_AUTO:    FUSED for PFHX steps with D <= 128 and a small pole range (octet items
- *                         x poles <= 2^18: the cluster's 16 SMs finish the poles sooner than the
- *                         seven launches of the chunked path would), CHUNKED otherwise (default).
+ *                         separated by cluster barriers, every stage's output handed to the CTA
+ *                         that needs it through distributed shared memory (kernels.cu
+ *                         step_small2_kernel); the pole range over 1..9 clusters
+ *                         (rexi_plan_set_fused_clusters). PFHX plans with D <= 128 only (else
+ *                         CHUNKED).
+ *  REXI_SCHEDULE_AUTO:    FUSED for PFHX steps with D <= 128 and pole work up to 2^19 octet
+ *                         items x poles (measured on B200: 64^2 at 47 poles 20 vs 36 us, at 604
+ *                         poles 29 vs 58 us), CHUNKED otherwise (default).
  *                         With octet items every block costs the same, so the chunked waves are
  *                         already balanced, and two 128-thread blocks per SM issue at least as
  *                         well as one 256-thread block: measured on B200 the chunked pole kernel

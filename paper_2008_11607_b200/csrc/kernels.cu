@@ -1,18 +1,22 @@
 // kernels.cu — device kernels of librexi (sm_100a, fp64).
 //
-//  * fft_{rows,cols}_{fwd,inv}_kernel : real 2-D FFT by batched radix-8 Stockham passes in
-//    shared memory (S1 forward transform, S5 inverse transform + Re). PAPER.md:497 "all computations
-//    ... in Fourier space"; Alg. 1 lines 1 and last.
-//  * pole_kernel_r2c (default)        : S2 + S3 for real fields on {K, -K} mode pairs grouped
+//  * fft_{rows,cols}_{fwd,inv}{,16}_kernel : real 2-D FFT by batched radix-8 / radix-16 Stockham
+//    passes in shared memory (S1 forward transform, S5 inverse transform + Re). PAPER.md:497 "all
+//    computations ... in Fourier space"; Alg. 1 lines 1 and last.
+//  * fft_cols_cl_kernel               : the column passes at 2048^2 and 4096^2 as 8-CTA clusters
+//    (four-step, exchange through distributed shared memory, 128-byte row segments).
+//  * pole_kernel_r2x (default, PFHX)  : S2 + S3 for real fields on {K, -K} mode pairs grouped
 //    in K2 octets: both Helmholtz-reduced solves of every pole for every pair, fused with the
-//    weighted accumulation in registers (eq:lswEta); pole_kernel_r2c_sk is
-//    its opt-in stream-K schedule.
+//    weighted accumulation in registers (eq:lswEta). pole_kernel_r2c (PFHR,
+//    collapsed, comparison only) and its stream-K schedule pole_kernel_r2c_sk.
 //  * pole_kernel<VARIANT>             : the same for the other variants (UV, DZ, DZ3, PF, PFH)
 //    and for complex spectra (rexi_poles). No per-pole solution ever reaches HBM.
 //  * finish_kernel (+ finish_r2c_sk)  : fixed-order sum of the per-chunk partial sums, zeta
 //    rebuilt from the potential vorticity, (u, v) recovered from (delta, zeta).
 //  * fixup_k0_kernel                  : the K = 0 modes (velocities decouple from delta, zeta
 //    there): pure Coriolis 2x2 solves per pole.
+//  * step_small2_kernel               : the whole step S1..S5 for small grids as one launch of
+//    thread-block clusters, stage data exchanged through distributed shared memory.
 //  * hermitian_kernel                 : the spectral form of Re(.) between rexi_run steps.
 #include <cooperative_groups.h>
 

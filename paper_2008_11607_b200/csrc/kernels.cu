@@ -592,6 +592,12 @@ namespace cgx = cooperative_groups;
 // cluster and global-memory accesses of one stage before those of the next across the cluster
 __device__ __forceinline__ void cluster_barrier() { cgx::this_cluster().sync(); }
 
+// barrier.cluster split phases: arrive (relaxed: orders nothing) at kernel start, wait before
+// the first DSMEM access (every CTA of the cluster has started); and the full barrier with
+// release / acquire semantics between stages (orders shared::cluster and global accesses)
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
 // ----------------------------------------------------------------------------- cluster column passes
 // Column passes for 1024 <= D <= 4096 with 128-byte row segments on every global load and store:
 // a cluster of 8 CTAs transforms 8 adjacent half-spectrum columns, four-step with D = 8 N2,
@@ -641,6 +647,9 @@ __global__ void __launch_bounds__(ColCl<LOGD>::T, 2) fft_cols_cl_kernel(FftArgs 
         const double2 w = __ldg(twg + 8 * tid);
         tw2[tid] = mk(w.x, w.y);
     }
+    // DSMEM stores may only target CTAs that have started (and, in checked builds, finished
+    // poisoning their shared memory): arrive now, wait just before the first remote store
+    cluster_arrive_relaxed();
     // ---- stage 1
     {
         const int col = tid & 7, n2 = c * (N2 / 8) + (tid >> 3);
@@ -673,6 +682,7 @@ __global__ void __launch_bounds__(ColCl<LOGD>::T, 2) fft_cols_cl_kernel(FftArgs 
             }
         }
         dft8<INV>(v);
+        cluster_wait();
 #pragma unroll
         for (int k1 = 0; k1 < 8; ++k1) {
             cd y = v[k1];
@@ -2007,11 +2017,6 @@ __device__ __forceinline__ bool small2_stage_slot(int l, int k, int D, int items
     return true;
 }
 
-// barrier.cluster split phases: arrive (relaxed: orders nothing) at kernel start, wait before
-// the first DSMEM access (every CTA of the cluster has started); and the full barrier with
-// release / acquire semantics between stages (orders shared::cluster and global accesses)
-__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 // owner CTA of index u of P units split as [P c / CS, P (c + 1) / CS)
 __device__ __forceinline__ int small2_owner(int u, int P, int CS) { return ((u + 1) * CS - 1) / P; }
@@ -2076,8 +2081,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             a.trace[((long)blockIdx.x * 2 + (tid != 0)) * 16 + (k)] = clock64();   \
     } while (0)
     SMALL2_MARK(0);
+    rx_poison_smem();          // (checked builds) before the arrival: no remote store is lost to it
     cluster_arrive_relaxed();
-    rx_poison_smem();
     RX_ASSERT(nu <= L.nu_max && (long)L.total * 16 <= (long)dyn_smem_bytes() && g < NC);
     cd *cs_ = smem + L.cslab;          // column slabs
     cd *rr = smem + L.rreg;            // row slabs (A, F) | spectrum rows + partials (B..D)

@@ -239,17 +239,17 @@ __device__ __forceinline__ void stockham_pass(cd *s, int N, int logN, int Ns, in
 
 // act = false: the thread only joins the block barriers (blocks with more threads than
 // transforms x tf, e.g. the fused small-grid step)
-template <bool INV, class IX, bool TWS = false>
+template <bool INV, class IX, bool TWS = false, int V = 8>
 __device__ __forceinline__ void fft_in_smem_ix(cd *s, IX ix, int N, int logN, int t, int tf, const cd *tw,
                                                bool act) {
     int Ns = 1, rem = logN;
     while (rem >= 3) {
-        stockham_pass_ix<8, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
+        stockham_pass_ix<8, INV, IX, TWS, V>(s, ix, N, Ns, t, tf, tw, act);
         Ns <<= 3;
         rem -= 3;
     }
-    if (rem == 2) stockham_pass_ix<4, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
-    else if (rem == 1) stockham_pass_ix<2, INV, IX, TWS>(s, ix, N, Ns, t, tf, tw, act);
+    if (rem == 2) stockham_pass_ix<4, INV, IX, TWS, V>(s, ix, N, Ns, t, tf, tw, act);
+    else if (rem == 1) stockham_pass_ix<2, INV, IX, TWS, V>(s, ix, N, Ns, t, tf, tw, act);
 }
 
 template <bool INV, bool TWS = false>
@@ -599,129 +599,147 @@ __device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 // ----------------------------------------------------------------------------- cluster column passes
-// Column passes for 1024 <= D <= 4096 with 128-byte row segments on every global load and store:
-// a cluster of 8 CTAs transforms 8 adjacent half-spectrum columns, four-step with D = 8 N2,
-// n = N2 n1 + n2, k = k1 + 8 k2:
-//   X[k1 + 8 k2] = sum_{n2} W_{N2}^{n2 k2} [ W_D^{n2 k1} sum_{n1} W_8^{n1 k1} x[N2 n1 + n2] ].
-// Stage 1, CTA c (rank in the cluster): thread (n2, col), n2 in [c N2/8, (c+1) N2/8), loads its
-// eight values x[N2 n1 + n2] straight from global memory (a warp: 4 rows x 8 columns), DFT-8 in
-// registers, twiddles W_D^{n2 k1}, and stores result k1 into the shared memory of CTA k1 of the
-// cluster (distributed shared memory, [n2][col]). Stage 2, after a cluster barrier: CTA k1 runs the
-// N2-point Stockham passes on its 8 columns and writes rows k1 + 8 k2. The single-CTA column
+// Column passes with N1 x 16-byte row segments on every global load and store (N1 = 8 or 16):
+// a cluster of N1 CTAs transforms N1 adjacent half-spectrum columns, four-step with D = N1 N2,
+// n = N2 n1 + n2, k = k1 + N1 k2:
+//   X[k1 + N1 k2] = sum_{n2} W_{N2}^{n2 k2} [ W_D^{n2 k1} sum_{n1} W_N1^{n1 k1} x[N2 n1 + n2] ].
+// Stage 1, CTA c (rank in the cluster): thread (n2, col), n2 in [c N2/N1, (c+1) N2/N1), loads its
+// N1 values x[N2 n1 + n2] straight from global memory, DFT-N1 in registers, twiddles W_D^{n2 k1},
+// and stores result k1 into the shared memory of CTA k1 of the cluster (distributed shared
+// memory, [n2][col]). Stage 2, after a cluster barrier: CTA k1 runs the N2-point Stockham passes
+// on its N1 columns and writes rows k1 + N1 k2. The single-CTA column
 // kernels above hold whole columns in one CTA, so at 4096^2 a load covers 2 columns = 32 bytes
 // of a row (0.32 of HBM, profiles/r02q_aux_c4.md). Output handling (scale, the packed k = 0 pair,
 // mirrors, half_out, the inverse's symmetrisation) as in fft_cols_fwd16 / fft_cols_inv16; the
 // k = 0 separation reads the mirror row from the CTA that holds it (the one cluster with col0 = 0).
 // MODE 0: forward; 1: inverse of a Hermitian spectrum; 2: inverse, symmetrising.
-template <int LOGD>
+template <int LOGD, int N1, int IPT>
 struct ColCl {
-    static constexpr int D = 1 << LOGD, H = D / 2, N2 = D / 8, LOGN2 = LOGD - 3;
-    static constexpr int T = N2;   // threads per CTA: one (n2, column) pair each in stage 1
-    static constexpr size_t SMEM = (size_t)(8 * N2 + N2) * sizeof(cd);   // [n2][8 columns] + N2 twiddles
+    // N1 = cluster size = columns per group (N1 x 16-byte row segments); D = N1 N2; IPT (n2,
+    // column) items per thread in stage 1
+    static constexpr int D = 1 << LOGD, H = D / 2, N2 = D / N1, LOGN1 = N1 == 16 ? 4 : 3;
+    static constexpr int LOGN2 = LOGD - LOGN1;
+    static constexpr int T = (N2 / N1) * N1 / IPT;   // threads per CTA
+    static constexpr int V = N1 * N2 / T;            // values per thread in the stage-2 passes
+    static constexpr size_t SMEM = (size_t)(N1 * N2 + N2) * sizeof(cd);   // [n2][N1 columns] + N2 twiddles
 };
 
+template <int N1>
 struct ColIx {
     int col;
-    __device__ __forceinline__ int operator()(int i) const { return i * 8 + col; }
+    __device__ __forceinline__ int operator()(int i) const { return i * N1 + col; }
 };
 
-template <int LOGD, int MODE>
-// (two CTAs per SM: <= 64 registers; unbounded the compiler takes 70-80, i.e. one CTA per SM)
-__global__ void __launch_bounds__(ColCl<LOGD>::T, 2) fft_cols_cl_kernel(FftArgs a) {
-    using L = ColCl<LOGD>;
+template <int N1, bool INV>
+__device__ __forceinline__ void dft_n1(cd *v) {
+    if (N1 == 16) dft16<INV>(v);
+    else dft8<INV>(v);
+}
+
+template <int LOGD, int MODE, int N1, int IPT>
+// (IPT = 1: 2 CTAs per SM, <= 64 registers; IPT = 2: half the threads, 3 CTAs per SM)
+__global__ void __launch_bounds__(ColCl<LOGD, N1, IPT>::T, IPT == 1 ? 2 : 3) fft_cols_cl_kernel(FftArgs a) {
+    using L = ColCl<LOGD, N1, IPT>;
     constexpr int D = L::D, H = L::H, N2 = L::N2, T = L::T;
     constexpr bool INV = MODE != 0;
     extern __shared__ cd smem[];
-    cd *buf = smem;                 // [n2][8]
-    cd *tw2 = smem + 8 * N2;        // W_{N2}^j = W_D^{8 j}
+    cd *buf = smem;                 // [n2][N1]
+    cd *tw2 = smem + N1 * N2;       // W_{N2}^j = W_D^{N1 j}
     rx_poison_smem();
     cgx::cluster_group cl = cgx::this_cluster();
     const int c = (int)cl.block_rank();
     const int f = blockIdx.y;
-    const int col0 = (int)(blockIdx.x / 8) * 8;
+    const int col0 = (int)(blockIdx.x / N1) * N1;
     const int tid = threadIdx.x;
     const cd *in = static_cast<const cd *>(f == 0 ? a.in[0] : f == 1 ? a.in[1] : a.in[2]);
     cd *out = static_cast<cd *>(f == 0 ? a.out[0] : f == 1 ? a.out[1] : a.out[2]);
     const double2 *twg = reinterpret_cast<const double2 *>(a.twiddle);
-    {
-        const double2 w = __ldg(twg + 8 * tid);
-        tw2[tid] = mk(w.x, w.y);
+    for (int i = tid; i < N2; i += T) {
+        const double2 w = __ldg(twg + N1 * i);
+        tw2[i] = mk(w.x, w.y);
     }
     // DSMEM stores may only target CTAs that have started (and, in checked builds, finished
     // poisoning their shared memory): arrive now, wait just before the first remote store
     cluster_arrive_relaxed();
-    // ---- stage 1
+    // ---- stage 1 (all IPT x N1 loads of the thread issued before the first DFT)
     {
-        const int col = tid & 7, n2 = c * (N2 / 8) + (tid >> 3);
-        const int k = col0 + col;
-        RX_ASSERT(k < H && n2 < N2);
-        cd v[8];
+        const int col = tid % N1, k = col0 + col;
+        cd v[IPT][N1];
 #pragma unroll
-        for (int n1 = 0; n1 < 8; ++n1) {
-            const int l = N2 * n1 + n2;
-            if (MODE == 0) {
-                v[n1] = in[(size_t)l * D + k];
-            } else {
-                const int lm = (D - l) & (D - 1);
-                if (k == 0) {
-                    cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
-                    if (MODE == 2) {
-                        const cd m0 = in[(size_t)lm * D], mh = in[(size_t)lm * D + H];
-                        t0 = mk(0.5 * (t0.x + m0.x), 0.5 * (t0.y - m0.y));
-                        th = mk(0.5 * (th.x + mh.x), 0.5 * (th.y - mh.y));
-                    }
-                    v[n1] = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+        for (int it = 0; it < IPT; ++it) {
+            const int n2 = c * (N2 / N1) + tid / N1 + it * (T / N1);
+            RX_ASSERT(k < H && n2 < N2);
+#pragma unroll
+            for (int n1 = 0; n1 < N1; ++n1) {
+                const int l = N2 * n1 + n2;
+                if (MODE == 0) {
+                    v[it][n1] = in[(size_t)l * D + k];
                 } else {
-                    cd t = in[(size_t)l * D + k];
-                    if (MODE == 2) {
-                        const cd m = in[(size_t)lm * D + (D - k)];
-                        t = mk(0.5 * (t.x + m.x), 0.5 * (t.y - m.y));
+                    const int lm = (D - l) & (D - 1);
+                    if (k == 0) {
+                        cd t0 = in[(size_t)l * D], th = in[(size_t)l * D + H];
+                        if (MODE == 2) {
+                            const cd m0 = in[(size_t)lm * D], mh = in[(size_t)lm * D + H];
+                            t0 = mk(0.5 * (t0.x + m0.x), 0.5 * (t0.y - m0.y));
+                            th = mk(0.5 * (th.x + mh.x), 0.5 * (th.y - mh.y));
+                        }
+                        v[it][n1] = mk(t0.x - th.y, t0.y + th.x);   // T0 + i TH
+                    } else {
+                        cd t = in[(size_t)l * D + k];
+                        if (MODE == 2) {
+                            const cd m = in[(size_t)lm * D + (D - k)];
+                            t = mk(0.5 * (t.x + m.x), 0.5 * (t.y - m.y));
+                        }
+                        v[it][n1] = t;
                     }
-                    v[n1] = t;
                 }
             }
         }
-        dft8<INV>(v);
-        cluster_wait();
 #pragma unroll
-        for (int k1 = 0; k1 < 8; ++k1) {
-            cd y = v[k1];
-            if (k1 > 0) {
-                const double2 w = __ldg(twg + n2 * k1);   // W_D^{n2 k1}, n2 k1 < D
-                y = INV ? mk(fma(y.x, w.x, y.y * w.y), fma(y.y, w.x, -y.x * w.y))
-                        : mk(fma(y.x, w.x, -y.y * w.y), fma(y.y, w.x, y.x * w.y));
+        for (int it = 0; it < IPT; ++it) {
+            const int n2 = c * (N2 / N1) + tid / N1 + it * (T / N1);
+            dft_n1<N1, INV>(v[it]);
+            if (it == 0) cluster_wait();
+#pragma unroll
+            for (int k1 = 0; k1 < N1; ++k1) {
+                cd y = v[it][k1];
+                if (k1 > 0) {
+                    const double2 w = __ldg(twg + n2 * k1);   // W_D^{n2 k1}, n2 k1 < D
+                    y = INV ? mk(fma(y.x, w.x, y.y * w.y), fma(y.y, w.x, -y.x * w.y))
+                            : mk(fma(y.x, w.x, -y.y * w.y), fma(y.y, w.x, y.x * w.y));
+                }
+                cl.map_shared_rank(buf, k1)[n2 * N1 + col] = y;
             }
-            cl.map_shared_rank(buf, k1)[n2 * 8 + col] = y;
         }
     }
     cluster_barrier();
-    // ---- stage 2: N2-point transforms of the 8 columns (k1 = c)
+    // ---- stage 2: N2-point transforms of the N1 columns (k1 = c)
     {
-        const int col = tid & 7, j = tid >> 3;
-        fft_in_smem_ix<INV, ColIx, true>(buf, ColIx{col}, N2, L::LOGN2, j, N2 / 8, tw2, true);
+        const int col = tid % N1, j = tid / N1;
+        fft_in_smem_ix<INV, ColIx<N1>, true, L::V>(buf, ColIx<N1>{col}, N2, L::LOGN2, j, T / N1, tw2, true);
     }
     const double sc = a.scale;
     if (MODE != 0) {
-        for (int i = tid; i < 8 * N2; i += T) {
-            const int k2 = i >> 3, col = i & 7;
+        for (int i = tid; i < N1 * N2; i += T) {
+            const int k2 = i / N1, col = i % N1;
             const cd v = buf[i];
-            out[(size_t)(c + 8 * k2) * D + col0 + col] = mk(v.x * sc, v.y * sc);
+            out[(size_t)(c + N1 * k2) * D + col0 + col] = mk(v.x * sc, v.y * sc);
         }
         return;
     }
     const bool zero = col0 == 0;   // uniform over the cluster
     if (zero) cluster_barrier();   // every CTA's stage 2 done: the k = 0 mirror rows are readable
-    for (int i = tid; i < 8 * N2; i += T) {
-        const int k2 = i >> 3, col = i & 7;
-        const int l = c + 8 * k2, k = col0 + col;
+    for (int i = tid; i < N1 * N2; i += T) {
+        const int k2 = i / N1, col = i % N1;
+        const int l = c + N1 * k2, k = col0 + col;
         const int lm = (D - l) & (D - 1);
         const cd v = buf[i];
         const bool lo = !a.half_out || l <= H, mlo = !a.half_out || lm <= H;
         if (k == 0) {
             // G = DFT(P), P = X0 + i XH (both real columns): F0 = (G + conj G(-l)) / 2,
-            // FH = (G - conj G(-l)) / (2i); G(-l) is row lm = (lm & 7) + 8 (lm >> 3)
+            // FH = (G - conj G(-l)) / (2i); G(-l) is row lm = (lm mod N1) + N1 (lm / N1)
             if (lo) {
-                const cd w = cl.map_shared_rank(buf, lm & 7)[(lm >> 3) * 8];
+                const cd w = cl.map_shared_rank(buf, lm % N1)[(lm / N1) * N1];
                 const double hs = 0.5 * sc;
                 out[(size_t)l * D] = mk(hs * (v.x + w.x), hs * (v.y - w.y));
                 out[(size_t)l * D + H] = mk(hs * (v.y + w.y), hs * (w.x - v.x));
@@ -2545,20 +2563,25 @@ static bool fft16_cols(int lg) {
 // 388 -> 288 us, inverse 358 -> 303 us on the apply path, 2048^2 -7 %; at 1024^2 the L2-resident
 // passes are latency-bound and gain nothing, at 8192^2 a cluster's 128 KB per CTA leaves one CTA
 // per SM); false also if this device cannot launch them
+// cluster width 8, one (n2, column) item per thread. Measured slower (ncu, 4096^2,
+// profiles/r02z_fft_cl_width.md): 16-wide clusters with 256-byte segments (forward 338 vs 286 us,
+// inverse 322 vs 283 us) and two items per thread at three CTAs per SM (313 / 299 us).
+constexpr int kColClWidth = 8, kColClItems = 1;
 static bool fft_cl_cols(int lg) {
     static const int off = [] { const char *v = getenv("REXI_FFT_CL"); return v && atoi(v) == 0; }();
     static int ok = -1;
     if (ok < 0) {
         ok = 1;
-#define SETCL(L)                                                                                         \
-    for (cudaError_t e : {cudaFuncSetAttribute(fft_cols_cl_kernel<L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                               (int)ColCl<L>::SMEM),                                     \
-                          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                               (int)ColCl<L>::SMEM),                                     \
-                          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                               (int)ColCl<L>::SMEM)})                                    \
+#define SETCL(L, N, I)                                                                                   \
+    for (cudaError_t e :                                                                                 \
+         {cudaFuncSetAttribute(fft_cols_cl_kernel<L, 0, N, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               (int)ColCl<L, N, I>::SMEM),                                               \
+          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 1, N, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               (int)ColCl<L, N, I>::SMEM),                                               \
+          cudaFuncSetAttribute(fft_cols_cl_kernel<L, 2, N, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               (int)ColCl<L, N, I>::SMEM)})                                              \
         if (e != cudaSuccess) ok = 0;
-        SETCL(10) SETCL(11) SETCL(12)
+        SETCL(11, kColClWidth, kColClItems) SETCL(12, kColClWidth, kColClItems)
 #undef SETCL
         cudaGetLastError();
     }
@@ -2567,27 +2590,29 @@ static bool fft_cl_cols(int lg) {
 
 static cudaError_t launch_cols_cl(int mode, const void *const i3[3], void *const o3[3], const cd *tw, int D,
                                   double scale, cudaStream_t st, bool half_out) {
+    constexpr int n1 = kColClWidth;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(D / 2, 3);   // (H / 8 column groups) x 8 CTAs, fields
+    cfg.gridDim = dim3(D / 2, 3);   // (H / n1 column groups) x n1 CTAs, fields
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 8;
+    at[0].val.clusterDim.x = n1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    FftArgs a = fft_args(i3, o3, tw, D, 8, mode ? 1 : 0, scale);
+    FftArgs a = fft_args(i3, o3, tw, D, n1, mode ? 1 : 0, scale);
     a.half_out = half_out ? 1 : 0;
-#define COLCL(L)                                                                                         \
-    if (D == (1 << L)) {                                                                                 \
-        cfg.blockDim = dim3(ColCl<L>::T);                                                                \
-        cfg.dynamicSmemBytes = ColCl<L>::SMEM;                                                           \
-        if (mode == 0) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 0>, a);                     \
-        if (mode == 1) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 1>, a);                     \
-        return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 2>, a);                                    \
+#define COLCL(L, N, I)                                                                                   \
+    if (D == (1 << L) && ipt == I) {                                                                     \
+        cfg.blockDim = dim3(ColCl<L, N, I>::T);                                                          \
+        cfg.dynamicSmemBytes = ColCl<L, N, I>::SMEM;                                                     \
+        if (mode == 0) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 0, N, I>, a);               \
+        if (mode == 1) return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 1, N, I>, a);               \
+        return cudaLaunchKernelEx(&cfg, fft_cols_cl_kernel<L, 2, N, I>, a);                              \
     }
-    COLCL(10) COLCL(11) COLCL(12)
+    constexpr int ipt = kColClItems;
+    COLCL(11, kColClWidth, kColClItems) COLCL(12, kColClWidth, kColClItems)
 #undef COLCL
     return cudaErrorInvalidValue;
 }

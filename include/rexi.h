@@ -325,7 +325,11 @@ rexi_status_t rexi_apply_host_batch(rexi_plan_t plan, long batch, const double *
 /* S6: `steps` successive steps in place on device fields (T_final = steps * tau). For
  * steps >= 2 the state stays in Fourier space between steps (NEXT-4): one forward FFT, then per
  * step the pole sum and the spectral form of the real part, (X(K) + conj(X(-K)))/2 — the same
- * operator as Re(IDFT(.)) followed by DFT, without the FFT round trip — and one inverse FFT. */
+ * operator as Re(IDFT(.)) followed by DFT, without the FFT round trip — and one inverse FFT.
+ * Steps that the fused schedule runs on one cluster (REXI_SCHEDULE_AUTO / FUSED, small grids
+ * and pole counts, rexi_plan_set_fused_clusters) run the whole run as ONE launch: the state
+ * stays in the cluster's shared memory between steps (R2C pair sums, Hermitian by
+ * construction). */
 rexi_status_t rexi_run(rexi_plan_t plan, int steps, double *eta, double *u, double *v,
                        void *stream);
 

@@ -463,8 +463,10 @@ int fused_clusters_auto(long items, long n) {
     return (int)std::min(8L, std::max(4L, (w + 39999) / 40000));
 }
 
+// steps > 1: a spectral-resident run of `steps` steps in the one launch (one cluster; rexi_run)
 rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, const double *u,
-                            const double *v, double *eo, double *uo, double *vo, cudaStream_t st) {
+                            const double *v, double *eo, double *uo, double *vo, cudaStream_t st,
+                            int steps = 1) {
     int resident = 0;
     const int cs = rexi::small2_cluster(&resident);
     if (cs <= 0) return fail(REXI_ECUDA, "fused small-grid step: thread-block cluster launch unavailable");
@@ -483,6 +485,7 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
         static const int stop = [] { const char *v = getenv("REXI_SMALL_STOP"); return v ? atoi(v) : 99; }();
         a.stop_after = stop;
     }
+    a.steps = steps;
     rexi::PoleArgs &q = a.pole;
     q = rexi::PoleArgs{};
     q.xpoles = p->d_xpoles;
@@ -499,7 +502,7 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     a.poles = p->d_poles;
     a.method = p->method;
     // the pole range split over nc clusters, each with its own range sums
-    int nc = p->fused_clusters > 0 ? p->fused_clusters : fused_clusters_auto(items, e - b);
+    int nc = steps > 1 ? 1 : p->fused_clusters > 0 ? p->fused_clusters : fused_clusters_auto(items, e - b);
     nc = (int)std::max(1L, std::min<long>({(long)nc, (long)rexi::kSmallMaxClusters, e - b}));
     if (resident > 0) nc = std::min(nc, resident);
     if ((long)nc * 3 * D * (D / 2 + 1) > 3 * n * (long)p->max_chunks) nc = 1;
@@ -1133,8 +1136,15 @@ rexi_status_t rexi_run(rexi_plan_t p, int steps, double *eta, double *u, double 
         cudaStream_t st = (cudaStream_t)stream;
         const long N1 = p->host.n_poles;
         if (steps == 1) return do_step(p, 0, N1, eta, u, v, eta, u, v, st);
-        // spectral-resident: forward once, (poles + Re projection) per step, inverse once
         rexi_status_t s;
+        // small steps whose fused step runs on one cluster: the whole run as ONE launch, the
+        // state kept in the cluster's shared memory between steps (kernels.cu step_small2_kernel)
+        if (small_eligible(p, 0, N1) &&
+            (p->fused_clusters > 0 ? p->fused_clusters : fused_clusters_auto(rexi::small_step_items(p->host.D), N1)) == 1) {
+            if ((s = poison_workspace(p, st, true)) != REXI_OK) return s;
+            return do_step_small(p, 0, N1, eta, u, v, eta, u, v, st, steps);
+        }
+        // spectral-resident: forward once, (poles + Re projection) per step, inverse once
         if ((s = do_forward(p, eta, u, v, p->d_fhat, st, p->kind() >= 6)) != REXI_OK) return s;
         for (int k = 0; k < steps; ++k)
             if ((s = do_spectral_step(p, 0, N1, st)) != REXI_OK) return s;

@@ -2101,7 +2101,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
     SMALL2_MARK(0);
     rx_poison_smem();          // (checked builds) before the arrival: no remote store is lost to it
     cluster_arrive_relaxed();
-    RX_ASSERT(nu <= L.nu_max && (long)L.total * 16 <= (long)dyn_smem_bytes() && g < NC);
+    RX_ASSERT(nu <= L.nu_max && (long)L.total * 16 <= (long)dyn_smem_bytes() && g < NC && a.steps >= 1 &&
+              (a.steps == 1 || NC == 1));
     cd *cs_ = smem + L.cslab;          // column slabs
     cd *rr = smem + L.rreg;            // row slabs (A, F) | spectrum rows + partials (B..D)
     R2XPole *pc = reinterpret_cast<R2XPole *>(smem + L.pcache);
@@ -2253,7 +2254,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
         if (k == H) base[L.aux + pidx(l)] = v;
         else base[L.cslab + (gc - (P3 * oc) / CS) * stride + pidx(l)] = v;
     };
-    const cd *stg = smem + L.stg;   // [item][pair][field]
+    cd *stg = smem + L.stg;   // [pair][field][item]
+    // Multi-step runs (a.steps > 1, one cluster): steps 1..K-1 finish into the staged spectrum
+    // of the same CTA's items (the state stays in shared memory, Fourier space, Hermitian by
+    // construction: PAPER.md:434's Re is the R2C pair sum), and only the last step goes on to
+    // the inverse transform — no exchange between the steps of a run.
+    for (int step = 0; step < a.steps; ++step) {
+    const bool last = step == a.steps - 1;
     {
         const int items = (int)a.n_items;
         // item split weighted by the workers per CTA (the last CTA's last warp takes the corners)
@@ -2340,9 +2347,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
                         e = e0[r];
                     }
                 }
-                put_acc(0, l, k, mk(cmul(Sg, e).x, 0.0));
-                put_acc(1, l, k, mk(au, 0.0));
-                put_acc(2, l, k, mk(av, 0.0));
+                if (last) {
+                    put_acc(0, l, k, mk(cmul(Sg, e).x, 0.0));
+                    put_acc(1, l, k, mk(au, 0.0));
+                    put_acc(2, l, k, mk(av, 0.0));
+                } else {   // the next step's corner state (only this warp reads it)
+                    smem[L.corner + q * 3] = mk(cmul(Sg, e).x, 0.0);
+                    smem[L.corner + q * 3 + 1] = mk(au, 0.0);
+                    smem[L.corner + q * 3 + 2] = mk(av, 0.0);
+                }
             }
         }
         SMALL2_MARK(7);
@@ -2372,6 +2385,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             const cd tt = mk(fma(kx, h1.x, -ky * h2.x), fma(kx, h1.y, -ky * h2.y));
             const cd w = mk(fma(ky, h1.x, kx * h2.x), fma(ky, h1.y, kx * h2.y));
             const cd U = mk(tt.y * inv, -tt.x * inv), V = mk(w.y * inv, -w.x * inv);
+            if (!last) {   // the next step's state at the representative (read after the barrier)
+                stg[j * 3 * L.ni_max + il] = h0;
+                stg[(j * 3 + 1) * L.ni_max + il] = U;
+                stg[(j * 3 + 2) * L.ni_max + il] = V;
+                continue;
+            }
             const int lm = (D - l) & (D - 1), km = (D - k) & (D - 1);
             const cd hv[3] = {h0, U, V};
             // the pair's two modes (the -K one conjugated) wherever k <= H; one copy of the stores
@@ -2386,6 +2405,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) step_small2_kernel(SmallArgs
             }
         }
     }
+    if (!last) __syncthreads();   // this step's state written before the next step's setup reads it
+    }   // steps
     SMALL2_MARK(9);
     if (NC > 1) {
         // hand-off: the last cluster to arrive sums the clusters' spectra (fixed order) alone.

@@ -154,6 +154,7 @@ struct SmallArgs {
     double scale;          // D^-2
     long n_items;          // octet work items (r2c_items(D, 2, true))
     int stop_after;        // measurement only (REXI_SMALL_STOP): return after stage 0..4
+    int steps;             // steps of a spectral-resident run (> 1 with one cluster only)
     int n_clusters;
     cd Sg[kSmallMaxClusters], Sdg[kSmallMaxClusters];   // per-cluster range sums (finish S, Sd)
     cd *cl_acc;            // [n_clusters][3][D][D/2 + 1] (n_clusters > 1)

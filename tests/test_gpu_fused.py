@@ -151,3 +151,28 @@ def test_fused_rexi_method_and_host(R):
     ref = lrsw.rexii_step(*g, 0.02, q.info["h"], q.info["M"])
     assert q.info["last_schedule"] == FUSED
     assert rel(list(out), ref) < TOL
+
+
+@pytest.mark.parametrize("D,tau,K", [(8, 0.3, 3), (16, 0.2, 4), (64, 0.02, 5)])
+def test_fused_run_vs_oracle_steps(R, D, tau, K):
+    """rexi_run on a small grid: the whole K-step run as one fused launch (the state stays in the
+    cluster's shared memory between steps) against K oracle steps, and against K single steps."""
+    import torch
+    f = inputs.white_noise(D, seed=79)
+    p = R.Plan(D, tau, tol=1e-12)
+    info = p.info
+    ref = f
+    for _ in range(K):
+        ref = lrsw.rexii_step(*ref, tau, info["h"], info["M"])
+    x = [dev(a) for a in f]
+    p.timing_enable(True)
+    p.timing_read()
+    p.run(K, *x)
+    ms, pl, tl = p.timing_read()
+    assert tl == 1 and p.info["last_schedule"] == FUSED   # one launch for the whole run
+    got = [host(t) for t in x]
+    assert rel(got, ref) < K * TOL
+    y = [dev(a) for a in f]
+    for _ in range(K):
+        y = [t.clone() for t in p.apply(*y)]
+    assert rel(got, [host(t) for t in y]) < 1e-13

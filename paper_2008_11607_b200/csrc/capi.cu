@@ -109,6 +109,7 @@ struct rexi_plan_s {
     cd *d_tmp = nullptr;    // [3][n_modes]
     cd *d_partial = nullptr;  // [max_chunks][3][n_modes]
     unsigned *d_counter = nullptr;  // fused DSMEM step: clusters arrived (0 between launches)
+    long long *d_trace = nullptr;   // REXI_SMALL_TRACE measurement buffer (allocated on first use)
     double *d_stage = nullptr;  // [6][n_modes] (rexi_apply_host)
     double *d_stage2 = nullptr;  // [6][n_modes] second set (rexi_apply_host_batch)
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -165,7 +166,8 @@ struct rexi_plan_s {
         for (cudaEvent_t e : ev_cap)
             if (e) cudaEventDestroy(e);
         for (void *p : {(void *)d_poles, (void *)d_rpoles, (void *)d_xpoles, (void *)d_ksym, (void *)d_tw, (void *)d_fhat, (void *)d_acc,
-                        (void *)d_tmp, (void *)d_partial, (void *)d_counter, (void *)d_stage, (void *)d_stage2})
+                        (void *)d_tmp, (void *)d_partial, (void *)d_counter, (void *)d_trace, (void *)d_stage,
+                        (void *)d_stage2})
             if (p) cudaFree(p);
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
@@ -517,18 +519,18 @@ rexi_status_t do_step_small(rexi_plan_s *p, long b, long e, const double *eta, c
     if ((s = record(p, st, true)) != REXI_OK) return s;
     // REXI_SMALL_TRACE=1 (measurement knob, graphs off): clock64 marks per CTA, printed to stderr
     static const bool trace = [] { const char *v = getenv("REXI_SMALL_TRACE"); return v && atoi(v) != 0; }();
-    static long long *d_trace = nullptr;
     const size_t trace_n = (size_t)cs * nc * 2 * 16;
     a.trace = nullptr;
     if (trace && !p->capturing) {
-        if (!d_trace) CK(cudaMalloc(&d_trace, (size_t)rexi::kSmallMaxClusters * 16 * 2 * 16 * sizeof(long long)));
-        CK(cudaMemsetAsync(d_trace, 0, trace_n * sizeof(long long), st));
-        a.trace = d_trace;
+        if (!p->d_trace)
+            CK(cudaMalloc((void **)&p->d_trace, (size_t)rexi::kSmallMaxClusters * 16 * 2 * 16 * sizeof(long long)));
+        CK(cudaMemsetAsync(p->d_trace, 0, trace_n * sizeof(long long), st));
+        a.trace = p->d_trace;
     }
     CK(rexi::launch_step_small2(a, cs, st));
     if (a.trace) {
         std::vector<long long> h(trace_n);
-        CK(cudaMemcpyAsync(h.data(), d_trace, trace_n * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h.data(), p->d_trace, trace_n * sizeof(long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         for (size_t c = 0; c < (size_t)cs * nc; ++c)
             for (int w = 0; w < 2; ++w) {

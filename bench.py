@@ -56,6 +56,8 @@ def parse():
                     help="pole kernel tuning 'modes_per_thread,poles_per_iter,min_blocks' (default: plan's)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: functional check only)")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the process-group path (apply_distributed + all-reduce) even at world size 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -223,6 +225,20 @@ def run_reference(args):
     return 0
 
 
+def nccl_summary(path):
+    """The communicator lines of this rank's NCCL INFO log (echoed to stderr): init, nranks,
+    transport (NVLS / P2P), so the run shows which communicator the all-reduce used."""
+    try:
+        with open(path) as fh:
+            text = fh.read()
+    except OSError:
+        return None
+    sys.stderr.write(text)
+    keys = ("Init COMPLETE", "nranks", "NVLS", "P2P", "comm 0x", "Channel")
+    lines = [ln.split("NCCL INFO", 1)[-1].strip() for ln in text.splitlines() if any(k in ln for k in keys)]
+    return {"log": path, "lines": len(text.splitlines()), "init": lines[:12]}
+
+
 # ----------------------------------------------------------------------------- native arm
 def main():
     args = parse()
@@ -231,12 +247,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.backend == "nccl":
-        # communicator evidence: NCCL's INIT lines (rank, nranks, channels / NVLS) on stderr,
-        # so stdout keeps the one JSON line
+    dist_on = world > 1 or args.dist
+    nccl_log = None
+    if dist_on and args.backend == "nccl":
+        # communicator evidence: NCCL's INIT lines (rank, nranks, channels / NVLS) go to a file
+        # (NCCL's default is stdout, which must keep the one JSON line); they are echoed to
+        # stderr and summarised in the line's "comm" object at the end
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        if "NCCL_DEBUG_FILE" not in os.environ:
+            import tempfile
+            nccl_log = os.path.join(tempfile.gettempdir(), f"rexi_bench_nccl.{os.getpid()}.log")
+            os.environ["NCCL_DEBUG_FILE"] = nccl_log
     import torch
     import torch.distributed as dist
     if world != args.gpus:
@@ -247,7 +269,7 @@ def main():
         local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         if args.backend == "gloo":
             dist.init_process_group("gloo")
         else:
@@ -270,7 +292,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step(timers=None):
-        if world > 1:
+        if dist_on:
             apply_distributed(plan, *f, out=out, timers=timers)
         else:
             plan.apply(*f, out=(out[0], out[1], out[2]))
@@ -291,18 +313,18 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     rank_timers = []                       # per step: (start, partial done, all-reduce done)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark()
     for i in range(args.steps):
         flush.zero_()                      # L2 flush between timed steps, outside the events
         ev[i][0].record(stream)
-        step(rank_timers if world > 1 else None)
+        step(rank_timers if dist_on else None)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clocks.mark()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms_local = sum(step_ms)
@@ -324,7 +346,7 @@ def main():
     plan.timing_enable(False)
     # per-step time = max over ranks of that step; the statistic is the median
     t = torch.tensor(step_ms + [ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t = t.tolist()
     step_max = t[:-1]
@@ -349,7 +371,7 @@ def main():
         mine["apply_partial_ms"] = statistics.median(part)
         mine["allreduce_ms"] = statistics.median(ar)
     ranks = [mine]
-    if world > 1:
+    if dist_on:
         ranks = [None] * world
         dist.all_gather_object(ranks, mine)
 
@@ -359,7 +381,7 @@ def main():
     e2e_steps = max(3, min(args.steps, 50))
 
     def e2e_step():
-        if world > 1:
+        if dist_on:
             for d_, h_ in zip(f, pinned_in):
                 d_.copy_(h_, non_blocking=True)
             apply_distributed(plan, *f, out=out)
@@ -371,7 +393,7 @@ def main():
 
     def timed(fn, reps):
         fn()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -380,7 +402,7 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         te = torch.tensor([dt], dtype=torch.float64, device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         return float(te.item())
 
@@ -455,13 +477,15 @@ def main():
                     "single_call_ms_per_step": 1e3 * single_s / e2e_steps},
             "gpu_launches": launches,   # repo kernels launched in the K steps (kernel-timing pass count)
         }
-        if world > 1:
+        if dist_on:
             line["ranks"] = ranks
             line["comm"] = {"backend": args.backend, "nranks": dist.get_world_size(),
                             "collective": "all_reduce(sum, fp64) of the 3 real fields, once per step",
                             "bytes_per_step": 3 * D * D * 8,
                             "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
                             if args.backend == "nccl" else None}
+            if nccl_log:
+                line["comm"]["nccl_init"] = nccl_summary(nccl_log)
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, desc, _, _ = oracle_rate(D, tau, tol, scen, args.cpu_seconds)
             rate1, _, desc1, _, _ = oracle_rate(D, tau, tol, scen, min(5.0, args.cpu_seconds / 2), threads=1)
@@ -469,7 +493,7 @@ def main():
                                     "sample": desc, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                                     "value_1core": rate1, "sample_1core": desc1}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
     return 0
 

@@ -40,7 +40,8 @@ def pole_parallel_step(partial_fn, n_poles, out, group=None, timers=None):
     e0 = _event(out) if timers is not None else None
     partial_fn(b, e, out)
     e1 = _event(out) if timers is not None else None
-    if world > 1:
+    if dist.is_initialized():
+        # also at world size 1 (the collective then runs as NCCL's single-rank copy)
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     if timers is not None and e0 is not None:
         timers.append((e0, e1, _event(out)))
@@ -91,7 +92,7 @@ def run_distributed(plan, steps, eta, u, v, group=None, spectral=False):
     half = plan.D // 2 + 1
     for _ in range(int(steps)):
         plan.poles_real(fhat, b, e, acc=acc)
-        if world > 1:
+        if dist.is_initialized():
             for c in range(3):
                 dist.all_reduce(acc[c, :half], op=dist.ReduceOp.SUM, group=group)
         plan.hermitian_mirror(acc)

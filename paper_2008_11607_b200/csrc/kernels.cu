@@ -1588,6 +1588,79 @@ __global__ void __launch_bounds__(BS, MINB) pole_kernel_r2x(PoleArgs a) {
     r2x_store(a, chunk, st, rep, ok);
 }
 
+// ---- bulk-copy (TMA engine) staging of the pole table: mbarrier + cp.async.bulk helpers
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// arm the barrier for `bytes` of transaction count and issue one 1-D bulk copy global -> shared
+// that completes them (a single elected thread)
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "RX_MBAR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra RX_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// pole_kernel_r2x with the pole table double-buffered in shared memory: thread 0 streams tile
+// t + 1 (cnt x 144 contiguous bytes) by one bulk copy on the TMA engine while the block computes
+// tile t, and the first tile's copy overlaps the item setup's spectrum loads. One block barrier
+// per tile (the buffer about to be refilled was read during tile t - 1) instead of two around a
+// copy every thread waits for.
+template <int PU, int MINB, int BS = kPoleBlock>
+__global__ void __launch_bounds__(BS, MINB) pole_kernel_r2x_bulk(PoleArgs a) {
+    __shared__ __align__(128) R2XPole sp[2][kR2CTile];
+    __shared__ __align__(8) unsigned long long bar[2];
+    const int chunk = blockIdx.y;
+    const long len = a.pole_end - a.pole_begin;
+    const long p0 = a.pole_begin + len * chunk / a.n_chunks;
+    const long p1 = a.pole_begin + len * (chunk + 1) / a.n_chunks;
+    const long item = (long)blockIdx.x * BS + threadIdx.x;
+    RX_ASSERT(p0 >= 0 && p0 <= p1 && p1 <= a.n_poles);
+    const int ntiles = (int)((p1 - p0 + kR2CTile - 1) / kR2CTile);
+    auto tile_cnt = [&](int t) { return (int)min((long)kR2CTile, p1 - p0 - (long)t * kR2CTile); };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ntiles > 0)
+        bulk_load(sp[0], a.xpoles + p0, (unsigned)(tile_cnt(0) * sizeof(R2XPole)), &bar[0]);
+    long rep[4];
+    bool ok[2];
+    double K2;
+    XPair st[4];
+    r2x_setup<false>(a, item, st, rep, ok, K2);
+    for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) {
+            __syncthreads();   // every thread is done with tile t - 1, whose buffer is refilled
+            if (threadIdx.x == 0)
+                bulk_load(sp[(t + 1) & 1], a.xpoles + p0 + (long)(t + 1) * kR2CTile,
+                          (unsigned)(tile_cnt(t + 1) * sizeof(R2XPole)), &bar[(t + 1) & 1]);
+        }
+        mbar_wait(&bar[t & 1], (unsigned)((t >> 1) & 1));
+        r2x_tile<PU>(sp[t & 1], tile_cnt(t), K2, st);
+    }
+    r2x_store(a, chunk, st, rep, ok);
+}
+
 // grid = (tiles, pole chunks). MPT < 4: a thread owns MPT modes m = tile0 + j * 128 + tid.
 // MPT = 4: a thread owns one K2 quad (quad_modes) and computes the pole denominator
 // 1/(kappa_n + K2) once for its four modes. Every thread runs all poles of its chunk, PU poles
@@ -2851,8 +2924,22 @@ cudaError_t pole_r2x_occupancy(int pu, int minb, int *blocks_per_sm) {
     return cudaErrorInvalidValue;
 }
 
+// REXI_R2X_BULK=0 selects the register-staged pole-table copy instead of the bulk-copy kernel
+// (measurement only)
+static bool r2x_bulk_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("REXI_R2X_BULK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
     dim3 grid((unsigned)pole_r2x_blocks(a.D, minb), (unsigned)a.n_chunks);
+    if (pu == 8 && minb == 2 && r2x_bulk_enabled()) {
+        pole_kernel_r2x_bulk<8, 2, kPoleBlock><<<grid, kPoleBlock, 0, st>>>(a);
+        return cudaGetLastError();
+    }
 #define X(U, B) if (pu == U && minb == B) { \
     R2X_KERNEL(U, B)<<<grid, r2x_block_size(B), 0, st>>>(a); return cudaGetLastError(); }
     REXI_R2X_CONFIGS(X)

@@ -1439,36 +1439,38 @@ struct XPair {
     cd H0, H1;                // Hermitian accumulators: eta, delta' (before the -Re(sum w1) eta0 term)
 };
 
+// One pole of the explicit-solve R2C kernel, given q = 1/(kappa_n + K2): both Helmholtz
+// solutions of the item's four pairs and their weighted accumulation.
+__device__ __forceinline__ void r2x_pole(const R2XPole &P, const cd q, XPair (&st)[4]) {
+    const cd sg = mk(fma(P.sgx1, q.x, P.sgx2 * q.y), fma(P.sgy1, q.x, P.sgy2 * q.y));
+    const cd ta = mk(fma(P.tax1, q.x, P.tax2 * q.y), fma(P.tay1, q.x, P.tay2 * q.y));
+    const double hn = P.hn, sr = P.s2r, si = P.s2i;
+    const double xr = P.X1r, xi = P.X1i, yr = P.Y1r, yi = P.Y1i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        XPair &s = st[j];
+        // right-hand sides of the two shifted systems after the Helmholtz reduction
+        const cd n1 = mk(fma(-hn, s.e0.y, fma(-sr, s.m0.x, fma(si, s.m0.y, s.B0.x))),
+                         fma(hn, s.e0.x, fma(-sr, s.m0.y, fma(-si, s.m0.x, s.B0.y))));
+        const cd nt = mk(fma(hn, s.e0.y, fma(-sr, s.m0.x, fma(-si, s.m0.y, s.Bt0.x))),
+                         fma(-hn, s.e0.x, fma(-sr, s.m0.y, fma(si, s.m0.x, s.Bt0.y))));
+        // the two Helmholtz solutions of this pole and mode
+        const cd eta1 = cmul(q, n1);
+        const cd etat = mk(fma(q.x, nt.x, q.y * nt.y), fma(q.x, nt.y, -q.y * nt.x));   // conj(q) nt
+        // weighted accumulation of the Hermitian part
+        const cd S = mk(eta1.x + etat.x, eta1.y + etat.y);
+        const cd Df = mk(eta1.x - etat.x, eta1.y - etat.y);
+        s.H0.x = fma(xr, S.x, fma(-xi, Df.y, fma(sg.x, s.d0.x, fma(-sg.y, s.d0.y, s.H0.x))));
+        s.H0.y = fma(xr, S.y, fma(xi, Df.x, fma(sg.x, s.d0.y, fma(sg.y, s.d0.x, s.H0.y))));
+        s.H1.x = fma(yr, S.x, fma(-yi, Df.y, fma(ta.x, s.d0.x, fma(-ta.y, s.d0.y, s.H1.x))));
+        s.H1.y = fma(yr, S.y, fma(yi, Df.x, fma(ta.x, s.d0.y, fma(ta.y, s.d0.x, s.H1.y))));
+    }
+}
+
 template <int PU>
 __device__ __forceinline__ void r2x_tile(const R2XPole *sp, int cnt, const double K2, XPair (&st)[4]) {
 #pragma unroll PU
-    for (int qq = 0; qq < cnt; ++qq) {
-        const R2XPole &P = sp[qq];
-        const cd q = pole_den(P, K2);
-        const cd sg = mk(fma(P.sgx1, q.x, P.sgx2 * q.y), fma(P.sgy1, q.x, P.sgy2 * q.y));
-        const cd ta = mk(fma(P.tax1, q.x, P.tax2 * q.y), fma(P.tay1, q.x, P.tay2 * q.y));
-        const double hn = P.hn, sr = P.s2r, si = P.s2i;
-        const double xr = P.X1r, xi = P.X1i, yr = P.Y1r, yi = P.Y1i;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            XPair &s = st[j];
-            // right-hand sides of the two shifted systems after the Helmholtz reduction
-            const cd n1 = mk(fma(-hn, s.e0.y, fma(-sr, s.m0.x, fma(si, s.m0.y, s.B0.x))),
-                             fma(hn, s.e0.x, fma(-sr, s.m0.y, fma(-si, s.m0.x, s.B0.y))));
-            const cd nt = mk(fma(hn, s.e0.y, fma(-sr, s.m0.x, fma(-si, s.m0.y, s.Bt0.x))),
-                             fma(-hn, s.e0.x, fma(-sr, s.m0.y, fma(si, s.m0.x, s.Bt0.y))));
-            // the two Helmholtz solutions of this pole and mode
-            const cd eta1 = cmul(q, n1);
-            const cd etat = mk(fma(q.x, nt.x, q.y * nt.y), fma(q.x, nt.y, -q.y * nt.x));   // conj(q) nt
-            // weighted accumulation of the Hermitian part
-            const cd S = mk(eta1.x + etat.x, eta1.y + etat.y);
-            const cd Df = mk(eta1.x - etat.x, eta1.y - etat.y);
-            s.H0.x = fma(xr, S.x, fma(-xi, Df.y, fma(sg.x, s.d0.x, fma(-sg.y, s.d0.y, s.H0.x))));
-            s.H0.y = fma(xr, S.y, fma(xi, Df.x, fma(sg.x, s.d0.y, fma(sg.y, s.d0.x, s.H0.y))));
-            s.H1.x = fma(yr, S.x, fma(-yi, Df.y, fma(ta.x, s.d0.x, fma(-ta.y, s.d0.y, s.H1.x))));
-            s.H1.y = fma(yr, S.y, fma(yi, Df.x, fma(ta.x, s.d0.y, fma(ta.y, s.d0.x, s.H1.y))));
-        }
-    }
+    for (int qq = 0; qq < cnt; ++qq) r2x_pole(sp[qq], pole_den(sp[qq], K2), st);
 }
 
 // Spectrum load; CG: through L2 only (ld.global.cg), for data another CTA of the same launch
@@ -2933,6 +2935,7 @@ static bool r2x_bulk_enabled() {
     }();
     return on;
 }
+
 
 cudaError_t launch_poles_r2x(const PoleArgs &a, int pu, int minb, cudaStream_t st) {
     dim3 grid((unsigned)pole_r2x_blocks(a.D, minb), (unsigned)a.n_chunks);

@@ -74,11 +74,13 @@ cudaError_t launch_mirror_rows(cd *acc, long n_modes, int D, cudaStream_t st);
 //     3(H-1) quads.
 //   kind 7 (PFHX, explicit solves on R2C pairs, real input; the default): per K2 value and pole
 //     den 7/11 and the per-pole delta0 coefficients sigma_n, tau'_n (2 MUL + 2 FMA each) 8/12;
-//     per pair and pole the two right-hand sides num1, num_t (12 FMA) 12/24, the two solutions
-//     eta1 = q num1, eta_t = conj(q) num_t (2 MUL + 2 FMA each) 8/12, their sum and difference
-//     (4 ADD) 4/4 and the Hermitian accumulation of eta and delta' (16 FMA) 16/32 = 40/72.
-//     An octet (8 modes, shared K2) = 175 / 311, i.e. 21.875 / 38.875 per mode (+ the
-//     discarded halves of the 3(H-1) single-quad items, as for kind 6).
+//     per pair and pole the two right-hand sides num1 = Z + Q, num_t = Z - Q with
+//     Z = h mu eta0 - sr m0 (2 FMA) and Q = delta0 + i (hn eta0 - si m0) (4 FMA), 4 ADD: 10/16,
+//     the two solutions eta1 = q num1, eta_t = conj(q) num_t (2 MUL + 2 FMA each) 8/12, their
+//     sum and difference (4 ADD) 4/4 and the Hermitian accumulation of eta and delta' (16 FMA)
+//     16/32 = 38/64. An octet (8 modes, shared K2) = 167 / 279, i.e. 20.875 / 34.875 per mode
+//     (+ the discarded halves of the 3(H-1) single-quad items, as for kind 6). (Before the
+//     shared Z, Q: 12 FMA for num1, num_t, 175 / 311 per octet.)
 // The denominator 1/(kappa + K2) costs 7 ops / 11 flops; with MPT = 4 (K2 quads) it is shared
 // by four modes.
 constexpr double kDenFlops = 11.0, kDenOps = 7.0;
@@ -91,13 +93,13 @@ inline double r2c_per_mode(int mpt, int D, double quad, double octet) {
 }
 inline double pole_flops(int kind, int mpt, int D) {
     if (kind == 6) return r2c_per_mode(mpt, D, 91.0, 143.0);
-    if (kind == 7) return r2c_per_mode(8, D, 0.0, 311.0);
+    if (kind == 7) return r2c_per_mode(8, D, 0.0, 279.0);
     const double f[6] = {109.0, 183.0, 53.0, 131.0, 95.0, 79.0};
     return mpt == 4 ? f[kind] - kDenFlops * 0.75 : f[kind];
 }
 inline double pole_ops(int kind, int mpt, int D) {
     if (kind == 6) return r2c_per_mode(mpt, D, 51.0, 79.0);
-    if (kind == 7) return r2c_per_mode(8, D, 0.0, 175.0);
+    if (kind == 7) return r2c_per_mode(8, D, 0.0, 167.0);
     const double f[6] = {59.0, 101.0, 29.0, 71.0, 51.0, 43.0};
     return mpt == 4 ? f[kind] - kDenOps * 0.75 : f[kind];
 }

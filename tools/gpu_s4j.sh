@@ -1,0 +1,8 @@
+# PFHX with the shared right-hand-side parts (num1 = Z + Q, num_t = Z - Q): parity + timing
+set -x
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/s4j_pytest_gpu.log 2>&1; echo pytest_rc=$?
+tail -2 gpurun_out/s4j_pytest_gpu.log; tail -1 gpurun_out/checked_run.log
+for i in 1 2; do python bench.py --steps 200 --no-cpu-baseline > gpurun_out/s4j_bench_c2_$i.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/s4j_bench_c2_$i.json'));print('c2', d['ms_per_step'], d['value'], d['roofline']['kernel_ms_avg'], d['roofline']['frac'], d['roofline']['fp64_pipe_frac'])"; done
+python bench.py --config c1 --no-cpu-baseline > gpurun_out/s4j_bench_c1.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/s4j_bench_c1.json'));print('c1', d['ms_per_step'], d['value'])"
+python tools/time_partial.py c3 100 | head -1

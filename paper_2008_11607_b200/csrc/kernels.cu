@@ -5,10 +5,13 @@
 //    computations ... in Fourier space"; Alg. 1 lines 1 and last.
 //  * fft_cols_cl_kernel               : the column passes at 2048^2 and 4096^2 as 8-CTA clusters
 //    (four-step, exchange through distributed shared memory, 128-byte row segments).
-//  * pole_kernel_r2x (default, PFHX)  : S2 + S3 for real fields on {K, -K} mode pairs grouped
+//  * pole_kernel_r2x_bulk (default, PFHX) : S2 + S3 for real fields on {K, -K} mode pairs grouped
 //    in K2 octets: both Helmholtz-reduced solves of every pole for every pair, fused with the
-//    weighted accumulation in registers (eq:lswEta). pole_kernel_r2c (PFHR,
-//    collapsed, comparison only) and its stream-K schedule pole_kernel_r2c_sk.
+//    weighted accumulation in registers (eq:lswEta); the pole table streamed
+//    into shared memory by bulk copies (cp.async.bulk + mbarrier, double-buffered).
+//    pole_kernel_r2x: the same with a register-staged table copy (the other tunings, and
+//    REXI_R2X_BULK=0). pole_kernel_r2c (PFHR, collapsed, comparison only) and its stream-K
+//    schedule pole_kernel_r2c_sk.
 //  * pole_kernel<VARIANT>             : the same for the other variants (UV, DZ, DZ3, PF, PFH)
 //    and for complex spectra (rexi_poles). No per-pole solution ever reaches HBM.
 //  * finish_kernel (+ finish_r2c_sk)  : fixed-order sum of the per-chunk partial sums, zeta

@@ -455,7 +455,10 @@ def main():
                          "traffic": None,
                          "traffic_note": "DRAM bytes per launch are an ncu quantity (profiles/r02*_summary.md); "
                                          "not measurable inside this run",
-                         "kernel": "pole_kernel_r2x (S2+S3)" if args.variant == "pfhx" else "pole_kernel",
+                         "kernel": ("pole_kernel_r2x (S2+S3)" if os.environ.get("REXI_R2X_BULK", "1") == "0"
+                                    or (args.tuning and args.tuning.split(",")[-1] != "2")
+                                    else "pole_kernel_r2x_bulk (S2+S3)") if args.variant == "pfhx"
+                                   else "pole_kernel",
                          "flops_per_pole_mode": info["flops_per_pole_mode"],
                          "fp64_ops_per_pole_mode": info["fp64_ops_per_pole_mode"],
                          "peak_source": "measured in this run: rexi_fp64_peak (DFMA, register operands, "

@@ -456,7 +456,7 @@ def main():
                          "traffic_note": "DRAM bytes per launch are an ncu quantity (profiles/r02*_summary.md); "
                                          "not measurable inside this run",
                          "kernel": ("pole_kernel_r2x (S2+S3)" if os.environ.get("REXI_R2X_BULK", "1") == "0"
-                                    or (args.tuning and args.tuning.split(",")[-1] != "2")
+                                    or (args.tuning and args.tuning.replace(" ", "") != "8,8,2")
                                     else "pole_kernel_r2x_bulk (S2+S3)") if args.variant == "pfhx"
                                    else "pole_kernel",
                          "flops_per_pole_mode": info["flops_per_pole_mode"],
